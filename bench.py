@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the Winograd-layer fwd+bwd hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--sparsity S]
+    python bench.py --impl reference ...      # the reference's own CPU path on the host cores
+
+A step = forward (with ForwardCache) + backward_weights + backward_input of one layer over
+one batch of the config (configs[1] by default: N=32, C=256, K=384, H=W=13, F(4x4,3x3),
+pad 1, 90% W_F sparsity), inputs resident in HBM.  With N>1 GPUs (torchrun) every rank runs
+its own batch (weak scaling: batch sharding) and dW_F (nnz-compact) is all-reduced over NCCL
+inside the step.  Effective GFLOP/s follows the reference convention
+(tools/wino.cpp:362, perfmodel.cpp:6-9): 2·C·K·H²·9 per image and pass, 3 passes.
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
+launching stream, with a 256 MB write between steps (outside the events) to flush the 126 MB
+L2; barrier + synchronize around the timed region; the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1702_08597_b200.synth import CONFIGS, make_inputs, with_sparsity  # noqa: E402
+
+METRIC = "Winograd layer fwd+bwd effective GFLOP/s"
+
+
+def flops_per_image(cfg) -> float:
+    """perfmodel.cpp:6-9 (flops_baseline) for one pass of one image."""
+    return 2.0 * cfg.c * cfg.k * cfg.h * cfg.w * cfg.r * cfg.r
+
+
+def workload_name(cfg, passes):
+    return (f"{cfg.name}: N={cfg.n}/GPU C={cfg.c} K={cfg.k} H=W={cfg.h} F({cfg.m}x{cfg.m},3x3) "
+            f"pad {cfg.pad}, W_F sparsity {cfg.sparsity:.0%}, {passes}")
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+# -------------------------------------------------------------------------------------
+# clocks during the timed region
+# -------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------------------------------
+# CPU side: the reference's own path (oracle/_ref) or the numpy port
+# -------------------------------------------------------------------------------------
+def cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads):
+    """One bounded sample of the reference's fwd+bwd: n_img images through the reference API
+    (winograd_forward -> backward_weights -> backward_input per image, train.cpp:169-202),
+    spread over `threads` host threads.  Returns (seconds, kind)."""
+    from oracle import ref
+
+    pad = cfg.pad
+    imgp = np.pad(img[:n_img].astype(np.float64), ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    gop = go[:n_img].astype(np.float64)
+    if ref.available():
+        t0 = time.perf_counter()
+        ref.layer_fwd_bwd_batch(imgp, w_f, gop, m=cfg.m, threads=threads, want_outputs=False)
+        return time.perf_counter() - t0, "reference"
+    from oracle import wino_oracle as wo  # numpy port, single process
+
+    t0 = time.perf_counter()
+    for i in range(n_img):
+        _, cache = wo.forward_f64(imgp[i], w_f, cfg.m)
+        wo.backward_weights_f64(gop[i], cache)
+        wo.backward_input_f64(cache, w_f)
+    return time.perf_counter() - t0, "port"
+
+
+def cpu_sample_size(cfg, threads):
+    return int(max(1, min(cfg.n, threads)))
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_img = cpu_sample_size(cfg, threads)
+    img, w_f, go = make_inputs(cfg, n=n_img)
+    flops = 3 * flops_per_image(cfg) * n_img
+    for _ in range(args.warmup):
+        cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads)
+    times = []
+    kind = "reference"
+    for _ in range(args.steps):
+        t, kind = cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads)
+        times.append(t)
+    tot = sum(times)
+    value = flops * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 normals)",
+        "config": {"workload": workload_name(cfg, "fwd+bwd") + f"; CPU sample {n_img} images/step",
+                   "n_images_per_step": n_img},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": kind,
+                         "sample": f"{n_img} of {cfg.n} images per step through the reference's "
+                                   "dense f64 per-image fwd+bwd API on a thread pool"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------------------------
+# GPU arm
+# -------------------------------------------------------------------------------------
+def kernel_bytes(cfg, layer, n):
+    """Algorithmic HBM bytes per launch of each kernel."""
+    g = layer.geometry
+    nt = n * g["t"]
+    p2 = g["p"] ** 2
+    f = 4
+    I = n * cfg.c * cfg.h * cfg.w * f
+    O = n * cfg.k * g["h_o"] * g["w_o"] * f
+    V = p2 * cfg.c * nt * f
+    Z = p2 * cfg.k * nt * f
+    nnz = layer.nnz
+    Wb = 8 * nnz + 4 * p2 * (cfg.k + 1)
+    Wt = 8 * nnz + 4 * p2 * (cfg.c + 1)
+    dw = nnz * f
+    return {
+        "input_transform": I + V, "spmm_fwd": V + Z + Wb, "output_transform": Z + O,
+        "grad_z": O + Z, "sddmm_dw": Z + V + dw + 8 * nnz + 4 * p2 * (cfg.k + 1),
+        "spmm_bwd_data": Z + Wt + V, "input_grad": V + I,
+    }
+
+
+def run_gpu(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1702_08597_b200 as wb
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = cfg.n
+    img, w_f, go = make_inputs(cfg)
+    if world > 1:  # every rank draws its own shard of the global batch
+        from paper_1702_08597_b200.synth import Stream
+
+        img = Stream(cfg.seed + 1000 * rank, "shard/I").normal(img.shape).astype(np.float32)
+        go = Stream(cfg.seed + 1000 * rank, "shard/dO").normal(go.shape).astype(np.float32)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
+    dense = cfg.sparsity == 0.0
+    layer.set_weights(w_f, dense=dense)
+    cache = layer.new_cache(n)
+    x = torch.from_numpy(img).to(dev)
+    g_o = torch.from_numpy(go).to(dev)
+    out = torch.empty((n, cfg.k, layer.ho, layer.wo), device=dev)
+    dw = torch.empty(layer.grad_w_shape(), device=dev)
+    di = torch.empty((n, cfg.c, cfg.h, cfg.w), device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+
+    def step():
+        layer.forward(x, cache, out=out)
+        layer.backward_weights(g_o, cache, out=dw)
+        if world > 1:
+            dist.all_reduce(dw)
+        layer.backward_input(cache, out=di)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    layer.profile(True)
+    layer.reset_launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = layer.launch_count()
+    prof = layer.profile_read()
+    layer.profile(False)
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    flops_step = 3 * flops_per_image(cfg) * n
+    value = world * flops_step / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers (pinned) ----
+    h_img = torch.from_numpy(img).pin_memory()
+    h_go = torch.from_numpy(go).pin_memory()
+    h_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+    h_dw = torch.empty(dw.shape, dtype=torch.float32).pin_memory()
+    h_di = torch.empty(di.shape, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        x.copy_(h_img, non_blocking=True)
+        g_o.copy_(h_go, non_blocking=True)
+        step()
+        h_out.copy_(out, non_blocking=True)
+        h_dw.copy_(dw, non_blocking=True)
+        h_di.copy_(di, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for a, b in ev2:
+        flush.zero_()
+        a.record()
+        e2e_step()
+        b.record()
+    torch.cuda.synchronize()
+    ms_e2e = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
+    t2 = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_value = world * flops_step / (float(t2.item()) * 1e-3) / 1e9
+    h2d = h_img.numel() * 4 + h_go.numel() * 4
+    d2h = (h_out.numel() + h_dw.numel() + h_di.numel()) * 4
+
+    if rank != 0:
+        return
+    pk = peaks()
+    kb = kernel_bytes(cfg, layer, n)
+    kernels = {}
+    for name, (tot_ms, cnt) in prof.items():
+        avg = tot_ms / max(cnt, 1)
+        bytes_ = kb.get(name)
+        kernels[name] = {"ms_per_launch": avg, "launches": cnt,
+                         "share": tot_ms / sum(v[0] for v in prof.values())}
+        if bytes_:
+            kernels[name]["alg_bytes"] = bytes_
+            kernels[name]["GBps"] = bytes_ / (avg * 1e-3) / 1e9
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
+    dom_gbs = kernels[dom].get("GBps")
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(f"{cfg.name}:{cfg.sparsity}:{dom}")
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": (dom_gbs / pk["hbm_gbs"]) if dom_gbs else None,
+                "traffic": traffic, "peak_source": pk["source"],
+                "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
+                         "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
+        "config": {"workload": workload_name(cfg, "fwd+bwd"), "global_batch": n * world,
+                   "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
+                   "path": "dense" if dense else "csr", "l2_flush": "256 MB write between timed steps",
+                   "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
+        "ms_per_layer": ms_max,
+        "roofline": roofline,
+        "kernels": kernels,
+        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item())},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_img = cpu_sample_size(cfg, threads)
+        t, kind = cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads)
+        line["cpu_baseline"] = {"value": 3 * flops_per_image(cfg) * n_img / t / 1e9, "unit": "GFLOP/s",
+                                "cores": threads, "kind": kind,
+                                "sample": f"{n_img} of {cfg.n} images (one step's worth per thread) "
+                                          "through the reference's dense f64 fwd+bwd API"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--sparsity", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    cfg = CONFIGS[args.config]
+    if args.sparsity is not None:
+        cfg = with_sparsity(cfg, args.sparsity)
+    if args.config == "c4":  # per-GPU shard of the global batch 512
+        from paper_1702_08597_b200.synth import LayerConfig
+
+        cfg = LayerConfig(cfg.name, max(1, cfg.n // max(1, args.gpus)), cfg.c, cfg.k, cfg.h, cfg.sparsity,
+                          cfg.pad, cfg.m, cfg.r, cfg.backward, cfg.seed)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

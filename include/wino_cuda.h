@@ -1,0 +1,163 @@
+/*
+ * wino_cuda.h — C-ABI of the B200-native Winograd layer (arXiv 1702.08597).
+ *
+ * Drop-in boundary for the reference's layer API.  Each entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj).  No C++ types, no exceptions, no CUDA headers: device
+ * buffers are plain pointers, streams are `void*` (a cudaStream_t), and every
+ * call returns a wino_status whose values map 1:1 onto the reference's
+ * exception classes; wino_last_error() holds the message (thread-local).
+ *
+ * Device layouts (row-major, fp32):
+ *   input  I  : N × C × H × W         (unpadded; `pad` is folded into φ)
+ *   output O  : N × K × Ho × Wo       Ho = H + 2·pad − r + 1
+ *   grad_in dI: N × C × H × W
+ *   grad_w    : sparse plan — nnz-compact values in CSR order, slice-major
+ *               ((i,j) row-major, then rows k, then the row's columns), i.e. the
+ *               order of PointwiseCsr<float>::values (sparse.hpp:19-38);
+ *               dense plan — K × C × p × q (the W_F layout, layer.hpp:36).
+ */
+#ifndef WINO_CUDA_H
+#define WINO_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define WINO_API __attribute__((visibility("default")))
+#else
+#define WINO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum wino_status {
+    WINO_OK = 0,
+    WINO_SHAPE_ERROR = 1,        /* wino::ShapeError         tensor.hpp:12-15     */
+    WINO_CONSISTENCY_ERROR = 2,  /* wino::ConsistencyError   layer.hpp:11-14      */
+    WINO_CORRUPT_FORMAT = 3,     /* wino::CorruptFormatError sparse.hpp:12-15     */
+    WINO_CAPABILITY_ERROR = 4,   /* wino::CapabilityError    transforms.hpp:10-13 */
+    WINO_CUDA_ERROR = 5,         /* device / runtime failure (no reference analogue) */
+    WINO_INVALID_ARGUMENT = 6    /* null pointer, bad enum (std::invalid_argument, bindings.cpp:140) */
+} wino_status;
+
+/* Mirrors wino::TileGeometry (transforms.hpp:39-53), square tiles only. */
+typedef struct wino_geometry {
+    int64_t c, h_i, w_i, h_o, w_o, h_op, w_op, h_ip, w_ip;
+    int64_t m, r, p, tiles_y, tiles_x, t;
+} wino_geometry;
+
+/* make_geometry (transforms.cpp:147-172). WINO_SHAPE_ERROR if the image is smaller
+ * than the kernel. */
+WINO_API int wino_make_geometry(int64_t c, int64_t h_i, int64_t w_i, int m, int r, wino_geometry* out);
+/* phi (transforms.cpp:179-187) / psi (transforms.cpp:189-194); WINO_SHAPE_ERROR when out of range. */
+WINO_API int wino_phi(const wino_geometry* g, int64_t t, int64_t i, int64_t j, int64_t* y, int64_t* x);
+WINO_API int wino_psi(const wino_geometry* g, int64_t y, int64_t x, int64_t* t, int64_t* i, int64_t* j);
+
+/* Transform constants exactly as the reference builds them, row-major doubles:
+ * a p×m (TransformSet::a1), b p×p (b1), g p×r (g1).  m=2,r=3 gives the fixed
+ * f2x2_3x3_transforms (transforms.cpp:7-19, chosen by bindings.cpp:41-44), every
+ * other (m,r) the Cook–Toom construction (transforms.cpp:71-145);
+ * WINO_CAPABILITY_ERROR when m+r−1 > 8. */
+WINO_API int wino_transforms(int m, int r, double* a, double* b, double* g);
+
+/* ---------------------------------------------------------------------------- */
+/* Layer plan (one Winograd layer; replaces the TransformSet/TileGeometry/weights */
+/* triple passed to winograd_forward, layer.hpp:28-43, and sparse_forward,      */
+/* sparse.hpp:78-82)                                                             */
+/* ---------------------------------------------------------------------------- */
+
+typedef struct wino_layer_desc {
+    int c, k;          /* input / output channels                            */
+    int h, w;          /* unpadded input extents                             */
+    int pad;           /* zero padding folded into φ: geometry = make_geometry(c, h+2pad, w+2pad) */
+    int m, r;          /* F(m×m, r×r); kernels are built for r=3, m ∈ {2,4,6} */
+    const double* a;   /* p×m TransformSet::a1 entries, or NULL for wino_transforms(m,r) */
+    const double* b;   /* p×p TransformSet::b1 entries, or NULL                          */
+    int device;        /* CUDA device ordinal                                            */
+} wino_layer_desc;
+
+typedef struct wino_plan wino_plan;
+typedef struct wino_cache wino_cache;
+
+WINO_API int wino_plan_create(const wino_layer_desc* desc, wino_plan** out);
+WINO_API int wino_plan_destroy(wino_plan* plan);
+/* geometry of the (padded) layer; nnz_total (−1 before weights are set); is_dense */
+WINO_API int wino_plan_info(const wino_plan* plan, wino_geometry* geom, int64_t* nnz_total, int* is_dense);
+
+/* Weights, sparse form: a PointwiseCsr<float> (sparse.hpp:19-38) given as p·q host
+ * slices in (i,j) row-major order: row_ptr[s] has K+1 entries, col_idx[s]/values[s]
+ * have nnz[s].  Fully validated (the reference's spmdm only bounds-checks columns,
+ * sparse.cpp:58, and reads row_ptr[K] unchecked): row_ptr[0]==0, monotone,
+ * row_ptr[K]==nnz[s], col_idx < C and strictly increasing within a row — any
+ * violation is WINO_CORRUPT_FORMAT.  Builds the device CSR and the CSC (W_Fᵀ)
+ * used by the backward pass.  Synchronous. */
+WINO_API int wino_set_weights_csr(wino_plan* plan, const uint64_t* const* row_ptr,
+                         const uint64_t* const* col_idx, const float* const* values,
+                         const uint64_t* nnz);
+/* Weights from a dense host W_F (K×C×p×q f64, layer.hpp:36): compress<float>
+ * (sparse.cpp:9-36, keep |v| > zero_tol, or v != 0 when zero_tol == 0) then as
+ * above.  If `dense` != 0 the plan instead keeps W_F dense and runs the dense
+ * tcgen05 contraction; dW is then K×C×p×q. */
+WINO_API int wino_set_weights(wino_plan* plan, const double* w_f, double zero_tol, int dense);
+/* Structure of the device CSR (for parity checks): per-slice nnz[p·q]; if the other
+ * pointers are non-null they receive row_ptr (p·q·(K+1), slice-local offsets),
+ * col_idx and values (nnz_total, CSR order). */
+WINO_API int wino_get_csr(const wino_plan* plan, uint64_t* nnz, uint64_t* row_ptr, uint64_t* col_idx,
+                 float* values);
+/* Device pointer to the live CSR values (nnz_total floats, CSR order) for in-place
+ * optimizer updates; wino_values_updated() refreshes the CSC copy from it. */
+WINO_API int wino_weight_values(wino_plan* plan, float** values_dev);
+WINO_API int wino_values_updated(wino_plan* plan, void* stream);
+
+/* ForwardCache (layer.hpp:19-25) on the device: Ĩ_F and dL/dZ for up to n_max images. */
+WINO_API int wino_cache_create(wino_plan* plan, int n_max, wino_cache** out);
+WINO_API int wino_cache_destroy(wino_cache* cache);
+
+/* winograd_forward (layer.cpp:45-96) / sparse_forward (sparse.cpp:190-253), batched:
+ * I (device, n×C×H×W) -> O (device, n×K×Ho×Wo).  cache may be NULL (inference);
+ * otherwise it receives Ĩ_F and loses any previous dL/dZ (layer.cpp:88). flags:
+ * WINO_FWD_RELU applies max(·,0) to O in the output-transform epilogue. */
+#define WINO_FWD_RELU 1
+WINO_API int wino_forward(wino_plan* plan, int n, const float* input, float* output, wino_cache* cache,
+                 int flags, void* stream);
+/* winograd_backward_weights (layer.cpp:98-132): dL/dO (device, n×K×Ho×Wo) ->
+ * dW (device, see header), storing dL/dZ in the cache.  WINO_BWD_RELU_MASK: dL/dO is
+ * first multiplied by [O > 0] with O = relu_out (the trainer's mask, train.cpp:193).
+ * dW receives the sum over the n images (the trainer's Σ_n before its 1/B, train.cpp:200). */
+#define WINO_BWD_RELU_MASK 1
+WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, const float* relu_out,
+                          wino_cache* cache, float* grad_w, int flags, void* stream);
+/* winograd_backward_input (layer.cpp:134-171): dI (device, n×C×H×W).
+ * WINO_CONSISTENCY_ERROR if backward_weights has not run on this cache. */
+WINO_API int wino_backward_input(wino_plan* plan, const wino_cache* cache, float* grad_input, void* stream);
+
+/* Masked SGD on the live CSR values (train.cpp:281-290 with a fixed mask: only surviving
+ * coordinates exist in the CSR, so masked ones are never touched):
+ *   v -= lr · (scale·g + l2·v/‖v‖₂)   (l2 = 0 skips the norm, train.cpp:219-229),
+ * then refreshes the CSC copy. grad is nnz-compact (device). */
+WINO_API int wino_sgd_step(wino_plan* plan, const float* grad_w, float lr, float scale, float l2,
+                  void* stream);
+
+/* ---------------------------------------------------------------------------- */
+/* Instrumentation                                                               */
+/* ---------------------------------------------------------------------------- */
+/* Number of kernels this plan has launched since creation (or the last reset). */
+WINO_API int64_t wino_launch_count(const wino_plan* plan);
+WINO_API void wino_reset_launch_count(wino_plan* plan);
+/* Per-kernel CUDA-event timing on the launching stream. enable=1 starts recording
+ * (events around every launch); wino_profile_read synchronises and returns, for up
+ * to `cap` kernel kinds, the summed milliseconds and launch counts. Names are static. */
+WINO_API int wino_profile_enable(wino_plan* plan, int enable);
+WINO_API int wino_profile_read(wino_plan* plan, int cap, const char** names, double* ms, int64_t* launches,
+                      int* n_kinds);
+
+WINO_API const char* wino_last_error(void);
+WINO_API const char* wino_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINO_CUDA_H */

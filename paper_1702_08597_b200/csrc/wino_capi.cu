@@ -1,0 +1,866 @@
+// C-ABI implementation of include/wino_cuda.h: the drop-in boundary between the
+// reference's layer API (layer.hpp:28-43, sparse.hpp:40-82) and the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/wino_cuda.h"
+#include "wino_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return set_err(WINO_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------------------
+// Cook–Toom transform generator — restatement of transforms.cpp:33-145 (same loop and
+// accumulation order so the doubles are bit-identical to the reference's; pinned by
+// tests/test_capi_host.py against the golden dump of the reference matrices).
+// ---------------------------------------------------------------------------------------
+const double kPoints[7] = {0.0, 1.0, -1.0, 2.0, -2.0, 0.5, -0.5};
+
+void poly_mul_linear(std::vector<double>& coeff, double a) {  // coeff *= (x - a)
+    std::vector<double> next(coeff.size() + 1, 0.0);
+    for (size_t d = 0; d < coeff.size(); ++d) {
+        next[d] -= coeff[d] * a;
+        next[d + 1] += coeff[d];
+    }
+    coeff.swap(next);
+}
+
+int cook_toom(int m, int r, double* a, double* b, double* g) {
+    if (m < 1 || r < 1) return set_err(WINO_CAPABILITY_ERROR, "tile and kernel extents must be >= 1");
+    const int p = m + r - 1;
+    if (p > 8)
+        return set_err(WINO_CAPABILITY_ERROR,
+                       "unsupported transform size: m+r-1 = " + std::to_string(p) + " exceeds 8");
+    std::fill(a, a + p * m, 0.0);
+    std::fill(b, b + p * p, 0.0);
+    std::fill(g, g + p * r, 0.0);
+    if (p == 1) {
+        a[0] = b[0] = g[0] = 1.0;
+        return WINO_OK;
+    }
+    const int n = p - 1;  // finite points
+    auto eval = [&](double* v, int ncoeff) {
+        for (int i = 0; i < n; ++i) {
+            double x = 1.0;
+            for (int j = 0; j < ncoeff; ++j) {
+                v[i * ncoeff + j] = x;
+                x *= kPoints[i];
+            }
+        }
+        v[(p - 1) * ncoeff + ncoeff - 1] = 1.0;
+    };
+    eval(g, r);
+    eval(a, m);
+    // Lagrange basis (inverse Vandermonde), column i = basis polynomial of point i
+    std::vector<double> inv(n * n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        std::vector<double> coeff = {1.0};
+        double denom = 1.0;
+        for (int k = 0; k < n; ++k) {
+            if (k == i) continue;
+            poly_mul_linear(coeff, kPoints[k]);
+            denom *= kPoints[i] - kPoints[k];
+        }
+        for (int j = 0; j < n; ++j) inv[j * n + i] = coeff[j] / denom;
+    }
+    std::vector<double> mpoly = {1.0};
+    for (int i = 0; i < n; ++i) poly_mul_linear(mpoly, kPoints[i]);
+    for (int j = 0; j < n; ++j) {
+        for (int i = 0; i < n; ++i) b[j * p + i] = inv[j * n + i];
+        b[j * p + p - 1] = mpoly[j];
+    }
+    b[(p - 1) * p + p - 1] = 1.0;
+    return WINO_OK;
+}
+
+int transforms(int m, int r, double* a, double* b, double* g) {
+    if (m == 2 && r == 3) {  // f2x2_3x3_transforms (transforms.cpp:7-19)
+        const double A[8] = {1, 0, 1, 1, 1, -1, 0, -1};
+        const double B[16] = {1, 0, 0, 0, 0, 1, -1, 1, -1, 1, 1, 0, 0, 0, 0, -1};
+        const double G[12] = {1, 0, 0, 0.5, 0.5, 0.5, 0.5, -0.5, 0.5, 0, 0, 1};
+        std::memcpy(a, A, sizeof A);
+        std::memcpy(b, B, sizeof B);
+        std::memcpy(g, G, sizeof G);
+        return WINO_OK;
+    }
+    return cook_toom(m, r, a, b, g);
+}
+
+int make_geometry(int64_t c, int64_t h_i, int64_t w_i, int m, int r, wino_geometry* g) {
+    if (h_i < r || w_i < r)
+        return set_err(WINO_SHAPE_ERROR, "image (" + std::to_string(c) + "x" + std::to_string(h_i) +
+                                             "x" + std::to_string(w_i) + ") smaller than kernel (" +
+                                             std::to_string(r) + "x" + std::to_string(r) + ")");
+    g->c = c;
+    g->h_i = h_i;
+    g->w_i = w_i;
+    g->m = m;
+    g->r = r;
+    g->p = m + r - 1;
+    g->h_o = h_i - r + 1;
+    g->w_o = w_i - r + 1;
+    g->tiles_y = (g->h_o + m - 1) / m;
+    g->tiles_x = (g->w_o + m - 1) / m;
+    g->h_op = g->tiles_y * m;
+    g->w_op = g->tiles_x * m;
+    g->h_ip = g->h_op + r - 1;
+    g->w_ip = g->w_op + r - 1;
+    g->t = g->tiles_y * g->tiles_x;
+    return WINO_OK;
+}
+
+enum Kind { K_INPUT = 0, K_SPMM, K_OUTPUT, K_GRADZ, K_SDDMM, K_SPMM_T, K_INGRAD, K_DENSE_FWD,
+            K_DENSE_DW, K_DENSE_DV, K_SGD, K_MISC, K_NKINDS };
+const char* kKindNames[K_NKINDS] = {"input_transform", "spmm_fwd", "output_transform", "grad_z",
+                                    "sddmm_dw", "spmm_bwd_data", "input_grad", "dense_fwd_tc",
+                                    "dense_dw_tc", "dense_dv_tc", "sgd", "misc"};
+
+struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct wino_plan {
+    int device = 0;
+    int C = 0, K = 0, H = 0, W = 0, pad = 0, m = 0, r = 0, p = 0, P2 = 0;
+    wino_geometry g{};
+    wino::Coefs cf{};
+    bool has_weights = false, dense = false;
+    int64_t nnz = 0;
+    std::vector<int64_t> slice_nnz, slice_off;
+    // CSR (global offsets) and CSC of W_F(:,:,i,j)ᵀ
+    int* d_rowptr = nullptr;
+    int* d_colidx = nullptr;
+    int* d_rowof = nullptr;
+    float* d_vals = nullptr;
+    int* d_colptr = nullptr;
+    int* d_rowidx = nullptr;
+    int* d_perm = nullptr;
+    float* d_valsT = nullptr;
+    std::vector<int> h_rowptr;  // kept for the SDDMM partition
+    int sddmm_rows = 0;
+    int64_t sddmm_max_nb = 0;
+    // dense plan (density 1): full CSR, dW scattered to K×C×p×q
+    float* d_wdense = nullptr;
+    float* d_dwc = nullptr;
+    size_t dwc_cap = 0;
+    // scratch
+    float* d_z = nullptr;
+    size_t z_cap = 0;
+    float* d_dv = nullptr;
+    size_t dv_cap = 0;
+    double* d_scalar = nullptr;
+    // instrumentation
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    double prof_ms[K_NKINDS] = {};
+    int64_t prof_n[K_NKINDS] = {};
+    int sm_count = 148;
+    int max_smem = 227 * 1024;
+};
+
+struct wino_cache {
+    wino_plan* plan = nullptr;
+    int n_max = 0;
+    int n = 0;
+    int64_t NTs = 0;
+    float* V = nullptr;
+    float* DZ = nullptr;
+    bool has_fwd = false;
+    bool has_grad_z = false;
+};
+
+namespace {
+
+void free_weights(wino_plan* p) {
+    for (void* ptr : {(void*)p->d_rowptr, (void*)p->d_colidx, (void*)p->d_rowof, (void*)p->d_vals,
+                      (void*)p->d_colptr, (void*)p->d_rowidx, (void*)p->d_perm, (void*)p->d_valsT,
+                      (void*)p->d_wdense})
+        if (ptr) cudaFree(ptr);
+    p->d_rowptr = p->d_colidx = p->d_rowof = p->d_colptr = p->d_rowidx = p->d_perm = nullptr;
+    p->d_vals = p->d_valsT = p->d_wdense = nullptr;
+    p->has_weights = false;
+}
+
+// Launch bracket: counts launches and, when profiling, records events on the stream.
+struct Launch {
+    wino_plan* p;
+    cudaStream_t st;
+    int kind;
+    ProfRec rec{};
+    Launch(wino_plan* plan, cudaStream_t s, int k) : p(plan), st(s), kind(k) {
+        ++p->launches;
+        if (p->prof) {
+            rec.kind = k;
+            cudaEventCreate(&rec.a);
+            cudaEventCreate(&rec.b);
+            cudaEventRecord(rec.a, st);
+        }
+    }
+    int done() {
+        cudaError_t e = cudaGetLastError();
+        if (p->prof) {
+            cudaEventRecord(rec.b, st);
+            p->recs.push_back(rec);
+        }
+        if (e != cudaSuccess)
+            return set_err(WINO_CUDA_ERROR, std::string("kernel ") + kKindNames[kind] +
+                                                ": " + cudaGetErrorString(e));
+        return WINO_OK;
+    }
+};
+
+int grid_for(int64_t work, int threads, int sm_count) {
+    int64_t b = (work + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sm_count * 16));
+}
+
+int ensure(float** buf, size_t* cap, size_t need) {
+    if (*cap >= need) return WINO_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaMalloc(buf, need * sizeof(float)));
+    *cap = need;
+    return WINO_OK;
+}
+
+// SpMM lane width: R floats per lane (chunk TW = 32R), the widest whose staged chunk
+// ncols×TW×4 B fits the budget (≥2 resident blocks per SM).
+int spmm_r(int ncols) {
+    const char* env = std::getenv("WINO_SPMM_R");
+    if (env) return std::atoi(env);
+    const int64_t budget = 110 * 1024;
+    if ((int64_t)ncols * 128 * 4 <= budget) return 4;
+    if ((int64_t)ncols * 64 * 4 <= budget) return 2;
+    return 1;
+}
+
+template <int R>
+int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int* col,
+                  const float* val, const float* X, float* Y, int nrows, int ncols, int64_t NT,
+                  int64_t NTs) {
+    constexpr int TW = 32 * R;
+    const size_t smem = (size_t)ncols * TW * sizeof(float);
+    if ((int)smem > p->max_smem)
+        return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
+    cudaFuncSetAttribute(wino::spmm_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int chunks = (int)((NT + TW - 1) / TW);
+    const int64_t base = (int64_t)chunks * p->P2;
+    const int per_sm = std::max(1, (int)(p->max_smem / std::max<size_t>(smem, 1)));
+    const int64_t target = (int64_t)p->sm_count * std::min(per_sm, 4) * 2;
+    int groups = (int)std::max<int64_t>(1, std::min<int64_t>((target + base - 1) / base, nrows / 8));
+    int rpb = (int)round_up((nrows + groups - 1) / groups, 8);
+    groups = (nrows + rpb - 1) / rpb;
+    Launch L(p, st, kind);
+    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), 256, smem, st>>>(rowptr, col, val, X, Y,
+                                                                       nrows, ncols, (int)NTs, rpb);
+    return L.done();
+}
+
+int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int* col,
+                const float* val, const float* X, float* Y, int nrows, int ncols, int64_t NT,
+                int64_t NTs) {
+    switch (spmm_r(ncols)) {
+        case 4: return launch_spmm_r<4>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
+        case 2: return launch_spmm_r<2>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
+        default: return launch_spmm_r<1>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
+    }
+}
+
+constexpr int kSddmmR = 2;
+
+int sddmm_smem(const wino_plan* p, int rows, int64_t nb) {
+    constexpr int TW = 32 * kSddmmR;
+    return (int)(((nb + 1) & ~1LL) * 8 + ((int64_t)p->C + rows) * TW * 4);
+}
+
+// Row-group partition of the SDDMM: the largest group count for which a group's
+// nonzeros fit the shared-memory fp64 accumulators, aiming at ≥2 waves.
+void plan_sddmm(wino_plan* p) {
+    const int K = p->K;
+    int best_rows = K;
+    int64_t best_nb = 0;
+    const int64_t target_blocks = (int64_t)p->sm_count * 4;
+    for (int rows = round_up(K, 8); rows >= 8; rows -= 8) {
+        int64_t nb = 0;
+        for (int s = 0; s < p->P2; ++s)
+            for (int r0 = 0; r0 < K; r0 += rows) {
+                const int r1 = std::min(K, r0 + rows);
+                nb = std::max<int64_t>(nb, p->h_rowptr[s * (K + 1) + r1] - p->h_rowptr[s * (K + 1) + r0]);
+            }
+        if (sddmm_smem(p, rows, nb) > p->max_smem) continue;
+        best_rows = rows;
+        best_nb = nb;
+        const int64_t blocks = (int64_t)((K + rows - 1) / rows) * p->P2;
+        if (blocks >= target_blocks && sddmm_smem(p, rows, nb) <= 100 * 1024) break;
+    }
+    p->sddmm_rows = best_rows;
+    p->sddmm_max_nb = best_nb;
+}
+
+template <int M, int P>
+int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, wino_cache* c,
+                   float* V, float* Z, int n, int64_t NT, int64_t NTs, int flags, int stage) {
+    const wino_geometry& g = p->g;
+    if (stage == 0) {
+        Launch L(p, st, K_INPUT);
+        wino::input_transform_kernel<M, P><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
+            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
+        return L.done();
+    }
+    Launch L(p, st, K_OUTPUT);
+    const int grid = grid_for((int64_t)p->K * NT, 256, p->sm_count);
+    if (flags & WINO_FWD_RELU)
+        wino::output_transform_kernel<M, P, true><<<grid, 256, 0, st>>>(
+            Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
+    else
+        wino::output_transform_kernel<M, P, false><<<grid, 256, 0, st>>>(
+            Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
+    return L.done();
+}
+
+template <int M, int P>
+int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
+                  int64_t NT, int64_t NTs, bool mask) {
+    const wino_geometry& g = p->g;
+    Launch L(p, st, K_GRADZ);
+    const int grid = grid_for((int64_t)p->K * NTs, 256, p->sm_count);
+    if (mask)
+        wino::grad_z_kernel<M, P, true><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
+                                                              (int)g.w_o, (int)g.tiles_x, (int)g.t,
+                                                              (int)NT, (int)NTs);
+    else
+        wino::grad_z_kernel<M, P, false><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
+                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
+                                                               (int)NT, (int)NTs);
+    return L.done();
+}
+
+template <int M, int P>
+int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI, int n, int64_t NTs) {
+    const wino_geometry& g = p->g;
+    const int T = (int)g.t;
+    const int64_t per_c = (int64_t)T * P * P * sizeof(float);
+    Launch L(p, st, K_INGRAD);
+    if (per_c <= 96 * 1024) {
+        int cg = (int)std::max<int64_t>(1, std::min<int64_t>(p->C, (48 * 1024) / per_c));
+        const size_t smem = (size_t)cg * per_c;
+        cudaFuncSetAttribute(wino::input_grad_kernel<M, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)std::max<size_t>(smem, 48 * 1024));
+        wino::input_grad_kernel<M, P><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
+            DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg);
+    } else {
+        const int64_t total = (int64_t)n * p->C * p->H * p->W;
+        wino::input_grad_direct_kernel<M, P><<<grid_for(total, 256, p->sm_count), 256, 0, st>>>(
+            DV, dI, p->cf, n, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs);
+    }
+    return L.done();
+}
+
+#define DISPATCH_MP(p, FN, ...)                                         \
+    ((p)->m == 4   ? FN<4, 6>(__VA_ARGS__)                              \
+     : (p)->m == 2 ? FN<2, 4>(__VA_ARGS__)                              \
+                   : FN<6, 8>(__VA_ARGS__))
+
+int check_plan(const wino_plan* p) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan has no weights (call wino_set_weights*)");
+    return WINO_OK;
+}
+
+int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<int>& col,
+               const std::vector<float>& val) {
+    const int K = p->K, C = p->C, P2 = p->P2;
+    const int64_t nnz = (int64_t)col.size();
+    // row-of-entry, CSC (counting sort per slice, ascending rows within a column) and perm
+    std::vector<int> rowof(nnz), colptr((size_t)P2 * (C + 1)), rowidx(nnz), perm(nnz);
+    std::vector<float> valsT(nnz);
+    for (int s = 0; s < P2; ++s) {
+        const int* rp = &rowptr[(size_t)s * (K + 1)];
+        int* cp = &colptr[(size_t)s * (C + 1)];
+        std::fill(cp, cp + C + 1, 0);
+        for (int k = 0; k < K; ++k)
+            for (int e = rp[k]; e < rp[k + 1]; ++e) {
+                rowof[e] = k;
+                cp[col[e] + 1]++;
+            }
+        cp[0] = rp[0];
+        for (int c = 0; c < C; ++c) cp[c + 1] += cp[c];
+        std::vector<int> fill(cp, cp + C);
+        for (int k = 0; k < K; ++k)
+            for (int e = rp[k]; e < rp[k + 1]; ++e) {
+                const int dst = fill[col[e]]++;
+                rowidx[dst] = k;
+                perm[dst] = e;
+                valsT[dst] = val[e];
+            }
+    }
+    auto up = [&](auto** dptr, const auto& hv) -> int {
+        using T = typename std::decay_t<decltype(hv)>::value_type;
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), std::max<size_t>(1, hv.size()) * sizeof(T)));
+        if (!hv.empty())
+            CUDA_TRY(cudaMemcpy(*dptr, hv.data(), hv.size() * sizeof(T), cudaMemcpyHostToDevice));
+        return WINO_OK;
+    };
+    int rc;
+    if ((rc = up(&p->d_rowptr, rowptr)) || (rc = up(&p->d_colidx, col)) || (rc = up(&p->d_rowof, rowof)) ||
+        (rc = up(&p->d_vals, val)) || (rc = up(&p->d_colptr, colptr)) || (rc = up(&p->d_rowidx, rowidx)) ||
+        (rc = up(&p->d_perm, perm)) || (rc = up(&p->d_valsT, valsT)))
+        return rc;
+    p->h_rowptr = rowptr;
+    p->nnz = nnz;
+    p->has_weights = true;
+    p->dense = false;
+    plan_sddmm(p);
+    return WINO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wino_last_error(void) { return g_err.c_str(); }
+const char* wino_version(void) { return "wino-b200 0.1 (sm_100a)"; }
+
+int wino_make_geometry(int64_t c, int64_t h_i, int64_t w_i, int m, int r, wino_geometry* out) {
+    if (!out) return set_err(WINO_INVALID_ARGUMENT, "null geometry");
+    return make_geometry(c, h_i, w_i, m, r, out);
+}
+
+int wino_phi(const wino_geometry* g, int64_t t, int64_t i, int64_t j, int64_t* y, int64_t* x) {
+    if (!g || !y || !x) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (t < 0 || i < 0 || j < 0 || t >= g->t || i >= g->p || j >= g->p)
+        return set_err(WINO_SHAPE_ERROR, "phi index (" + std::to_string(t) + "," + std::to_string(i) +
+                                             "," + std::to_string(j) + ") out of range");
+    *y = (t / g->tiles_x) * g->m + i;
+    *x = (t % g->tiles_x) * g->m + j;
+    return WINO_OK;
+}
+
+int wino_psi(const wino_geometry* g, int64_t y, int64_t x, int64_t* t, int64_t* i, int64_t* j) {
+    if (!g || !t || !i || !j) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (y < 0 || x < 0 || y >= g->h_op || x >= g->w_op)
+        return set_err(WINO_SHAPE_ERROR,
+                       "psi index (" + std::to_string(y) + "," + std::to_string(x) + ") out of range");
+    *t = (y / g->m) * g->tiles_x + x / g->m;
+    *i = y % g->m;
+    *j = x % g->m;
+    return WINO_OK;
+}
+
+int wino_transforms(int m, int r, double* a, double* b, double* g) {
+    if (!a || !b || !g) return set_err(WINO_INVALID_ARGUMENT, "null output");
+    return transforms(m, r, a, b, g);
+}
+
+int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
+    if (!d || !out) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (d->c <= 0 || d->k <= 0 || d->h <= 0 || d->w <= 0 || d->pad < 0)
+        return set_err(WINO_SHAPE_ERROR, "layer extents must be positive");
+    if (d->r != 3 || (d->m != 2 && d->m != 4 && d->m != 6))
+        return set_err(WINO_CAPABILITY_ERROR, "kernels are built for F(m,3), m in {2,4,6}; got m=" +
+                                                  std::to_string(d->m) + " r=" + std::to_string(d->r));
+    if (d->c >= 65536 || d->k >= 65536)
+        return set_err(WINO_CAPABILITY_ERROR, "channel counts must be < 65536");
+    auto* p = new wino_plan();
+    p->device = d->device;
+    p->C = d->c;
+    p->K = d->k;
+    p->H = d->h;
+    p->W = d->w;
+    p->pad = d->pad;
+    p->m = d->m;
+    p->r = d->r;
+    p->p = d->m + d->r - 1;
+    p->P2 = p->p * p->p;
+    int rc = make_geometry(d->c, d->h + 2 * d->pad, d->w + 2 * d->pad, d->m, d->r, &p->g);
+    if (rc) {
+        delete p;
+        return rc;
+    }
+    double a[64], b[64], gg[64];
+    if (d->a && d->b) {
+        std::memcpy(a, d->a, sizeof(double) * p->p * p->m);
+        std::memcpy(b, d->b, sizeof(double) * p->p * p->p);
+    } else if ((rc = transforms(d->m, d->r, a, b, gg))) {
+        delete p;
+        return rc;
+    }
+    for (int i = 0; i < p->p * p->m; ++i) p->cf.a[i] = (float)a[i];
+    for (int i = 0; i < p->p * p->p; ++i) p->cf.b[i] = (float)b[i];
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device);
+    if (e == cudaSuccess)
+        e = cudaDeviceGetAttribute(&p->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_scalar, sizeof(double));
+    if (e != cudaSuccess) {
+        delete p;
+        return set_err(WINO_CUDA_ERROR, std::string("plan_create: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return WINO_OK;
+}
+
+int wino_plan_destroy(wino_plan* p) {
+    if (!p) return WINO_OK;
+    free_weights(p);
+    if (p->d_dwc) cudaFree(p->d_dwc);
+    if (p->d_z) cudaFree(p->d_z);
+    if (p->d_dv) cudaFree(p->d_dv);
+    if (p->d_scalar) cudaFree(p->d_scalar);
+    for (auto& r : p->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    delete p;
+    return WINO_OK;
+}
+
+int wino_plan_info(const wino_plan* p, wino_geometry* geom, int64_t* nnz_total, int* is_dense) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    if (geom) *geom = p->g;
+    if (nnz_total) *nnz_total = p->has_weights ? p->nnz : -1;
+    if (is_dense) *is_dense = p->dense ? 1 : 0;
+    return WINO_OK;
+}
+
+int wino_set_weights_csr(wino_plan* p, const uint64_t* const* row_ptr, const uint64_t* const* col_idx,
+                         const float* const* values, const uint64_t* nnz) {
+    if (!p || !row_ptr || !col_idx || !values || !nnz) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    const int K = p->K, C = p->C, P2 = p->P2;
+    std::vector<int> rowptr((size_t)P2 * (K + 1));
+    std::vector<int> col;
+    std::vector<float> val;
+    int64_t off = 0;
+    for (int s = 0; s < P2; ++s) {
+        const uint64_t* rp = row_ptr[s];
+        const uint64_t n = nnz[s];
+        if (!rp || (n > 0 && (!col_idx[s] || !values[s])))
+            return set_err(WINO_CORRUPT_FORMAT, "slice " + std::to_string(s) + ": missing arrays");
+        if (rp[0] != 0 || rp[K] != n)
+            return set_err(WINO_CORRUPT_FORMAT, "slice " + std::to_string(s) +
+                                                    ": row_ptr must start at 0 and end at nnz");
+        if (off + (int64_t)n >= (int64_t)1 << 31)
+            return set_err(WINO_CAPABILITY_ERROR, "more than 2^31 nonzeros");
+        for (int k = 0; k < K; ++k) {
+            if (rp[k + 1] < rp[k] || rp[k + 1] > n)
+                return set_err(WINO_CORRUPT_FORMAT, "slice " + std::to_string(s) + ": row_ptr not monotone");
+            for (uint64_t e = rp[k]; e < rp[k + 1]; ++e) {
+                const uint64_t cidx = col_idx[s][e];
+                if (cidx >= (uint64_t)C)
+                    return set_err(WINO_CORRUPT_FORMAT, "spmdm: column index out of bounds");
+                if (e > rp[k] && cidx <= col_idx[s][e - 1])
+                    return set_err(WINO_CORRUPT_FORMAT, "slice " + std::to_string(s) +
+                                                            ": column indices not strictly increasing");
+            }
+        }
+        for (int k = 0; k <= K; ++k) rowptr[(size_t)s * (K + 1) + k] = (int)(off + (int64_t)rp[k]);
+        for (uint64_t e = 0; e < n; ++e) {
+            col.push_back((int)col_idx[s][e]);
+            val.push_back(values[s][e]);
+        }
+        off += (int64_t)n;
+    }
+    free_weights(p);
+    p->slice_nnz.assign(nnz, nnz + P2);
+    p->slice_off.resize(P2);
+    for (int s = 0, o = 0; s < P2; o += (int)nnz[s], ++s) p->slice_off[s] = o;
+    CUDA_TRY(cudaSetDevice(p->device));
+    return upload_csr(p, rowptr, col, val);
+}
+
+int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense) {
+    if (!p || !w_f) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    const int K = p->K, C = p->C, P = p->p, P2 = p->P2;
+    CUDA_TRY(cudaSetDevice(p->device));
+    if (dense) {  // every coordinate is a weight (zeros included): full CSR
+        std::vector<int> rowptr((size_t)P2 * (K + 1)), col((size_t)P2 * K * C);
+        std::vector<float> val((size_t)P2 * K * C);
+        for (int s = 0; s < P2; ++s) {
+            for (int k = 0; k <= K; ++k) rowptr[(size_t)s * (K + 1) + k] = (int)((int64_t)s * K * C + (int64_t)k * C);
+            for (int k = 0; k < K; ++k)
+                for (int c = 0; c < C; ++c) {
+                    const size_t e = ((size_t)s * K + k) * C + c;
+                    col[e] = c;
+                    val[e] = (float)w_f[((size_t)k * C + c) * P2 + s];
+                }
+        }
+        free_weights(p);
+        p->slice_nnz.assign(P2, (int64_t)K * C);
+        p->slice_off.resize(P2);
+        for (int s = 0; s < P2; ++s) p->slice_off[s] = (int64_t)s * K * C;
+        int rc = upload_csr(p, rowptr, col, val);
+        p->dense = true;
+        return rc;
+    }
+    // compress<float> (sparse.cpp:9-36): slices (i,j) row-major, rows k, columns c ascending
+    std::vector<std::vector<uint64_t>> rps(P2), cols(P2);
+    std::vector<std::vector<float>> vals(P2);
+    std::vector<uint64_t> nnz(P2);
+    for (int i = 0; i < P; ++i)
+        for (int j = 0; j < P; ++j) {
+            const int s = i * P + j;
+            rps[s].assign(K + 1, 0);
+            for (int k = 0; k < K; ++k) {
+                for (int c = 0; c < C; ++c) {
+                    const double v = w_f[((size_t)k * C + c) * P2 + s];
+                    if (std::abs(v) > zero_tol || (zero_tol == 0.0 && v != 0.0)) {
+                        cols[s].push_back((uint64_t)c);
+                        vals[s].push_back((float)v);
+                    }
+                }
+                rps[s][k + 1] = vals[s].size();
+            }
+            nnz[s] = vals[s].size();
+        }
+    std::vector<const uint64_t*> prp(P2), pcol(P2);
+    std::vector<const float*> pval(P2);
+    for (int s = 0; s < P2; ++s) {
+        prp[s] = rps[s].data();
+        pcol[s] = cols[s].data();
+        pval[s] = vals[s].data();
+    }
+    return wino_set_weights_csr(p, prp.data(), pcol.data(), pval.data(), nnz.data());
+}
+
+int wino_get_csr(const wino_plan* p, uint64_t* nnz, uint64_t* row_ptr, uint64_t* col_idx, float* values) {
+    if (!p || !nnz) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan holds no CSR weights");
+    const int K = p->K, P2 = p->P2;
+    for (int s = 0; s < P2; ++s) nnz[s] = (uint64_t)p->slice_nnz[s];
+    if (row_ptr)
+        for (int s = 0; s < P2; ++s)
+            for (int k = 0; k <= K; ++k)
+                row_ptr[(size_t)s * (K + 1) + k] =
+                    (uint64_t)(p->h_rowptr[(size_t)s * (K + 1) + k] - p->slice_off[s]);
+    if (col_idx || values) {
+        std::vector<int> col(p->nnz);
+        std::vector<float> val(p->nnz);
+        CUDA_TRY(cudaMemcpy(col.data(), p->d_colidx, p->nnz * sizeof(int), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(val.data(), p->d_vals, p->nnz * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t e = 0; e < p->nnz; ++e) {
+            if (col_idx) col_idx[e] = (uint64_t)col[e];
+            if (values) values[e] = val[e];
+        }
+    }
+    return WINO_OK;
+}
+
+int wino_weight_values(wino_plan* p, float** values_dev) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!values_dev) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    *values_dev = p->d_vals;
+    return WINO_OK;
+}
+
+int wino_values_updated(wino_plan* p, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Launch L(p, st, K_MISC);
+    wino::gather_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_valsT, p->d_vals, p->d_perm, p->nnz);
+    return L.done();
+}
+
+int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
+    if (!p || !out || n_max <= 0) return set_err(WINO_INVALID_ARGUMENT, "bad argument");
+    CUDA_TRY(cudaSetDevice(p->device));
+    auto* c = new wino_cache();
+    c->plan = p;
+    c->n_max = n_max;
+    const int64_t NTs = round_up((int64_t)n_max * p->g.t, 4);
+    cudaError_t e = cudaMalloc(&c->V, (size_t)p->P2 * p->C * NTs * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&c->DZ, (size_t)p->P2 * p->K * NTs * sizeof(float));
+    if (e != cudaSuccess) {
+        if (c->V) cudaFree(c->V);
+        delete c;
+        return set_err(WINO_CUDA_ERROR, std::string("cache_create: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return WINO_OK;
+}
+
+int wino_cache_destroy(wino_cache* c) {
+    if (!c) return WINO_OK;
+    if (c->V) cudaFree(c->V);
+    if (c->DZ) cudaFree(c->DZ);
+    delete c;
+    return WINO_OK;
+}
+
+int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_cache* cache, int flags,
+                 void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!input || !output) return set_err(WINO_INVALID_ARGUMENT, "null buffer");
+    if (n <= 0) return set_err(WINO_SHAPE_ERROR, "batch must be positive");
+    if (cache && (cache->plan != p || n > cache->n_max))
+        return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t NT = (int64_t)n * p->g.t;
+    const int64_t NTs = round_up(NT, 4);
+    float* V;
+    if (cache) {
+        V = cache->V;
+    } else {
+        if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
+        V = p->d_dv;  // inference: the backward scratch doubles as Ĩ_F
+    }
+    if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0)))
+        return rc;
+    rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_colidx, p->d_vals, V, p->d_z, p->K, p->C, NT, NTs);
+    if (rc) return rc;
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1)))
+        return rc;
+    if (cache) {
+        cache->n = n;
+        cache->NTs = NTs;
+        cache->has_fwd = true;
+        cache->has_grad_z = false;  // layer.cpp:88
+    }
+    return WINO_OK;
+}
+
+int wino_backward_weights(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c,
+                          float* grad_w, int flags, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!c || !grad_output || !grad_w) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (c->plan != p || !c->has_fwd)
+        return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
+    const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
+    if (mask && !relu_out) return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
+    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask))) return rc;
+    float* dwc = grad_w;
+    if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
+    if (p->dense) dwc = p->d_dwc;
+    {
+        const int rows = p->sddmm_rows;
+        const int smem = sddmm_smem(p, rows, p->sddmm_max_nb);
+        cudaFuncSetAttribute(wino::sddmm_kernel<kSddmmR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        Launch L(p, st, K_SDDMM);
+        wino::sddmm_kernel<kSddmmR><<<dim3((p->K + rows - 1) / rows, p->P2), 256, smem, st>>>(
+            p->d_rowptr, p->d_colidx, p->d_rowof, c->DZ, c->V, dwc, p->K, p->C, (int)NT, (int)NTs, rows);
+        if ((rc = L.done())) return rc;
+    }
+    if (p->dense) {  // [s][k][c] -> K×C×p×q
+        Launch L(p, st, K_MISC);
+        wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
+            dwc, grad_w, p->K, p->C, p->P2);
+        if ((rc = L.done())) return rc;
+    }
+    c->has_grad_z = true;
+    return WINO_OK;
+}
+
+int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!c || !grad_input) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (c->plan != p || !c->has_fwd)
+        return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
+    if (!c->has_grad_z)
+        return set_err(WINO_CONSISTENCY_ERROR, "backward_input: dL/dZ missing; run backward_weights first");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
+    if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
+    rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_rowidx, p->d_valsT, c->DZ, p->d_dv, p->C, p->K,
+                     NT, NTs);
+    if (rc) return rc;
+    return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
+}
+
+int wino_sgd_step(wino_plan* p, const float* grad_w, float lr, float scale, float l2, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!grad_w) return set_err(WINO_INVALID_ARGUMENT, "null gradient");
+    cudaStream_t st = (cudaStream_t)stream;
+    float* vals = p->d_vals;
+    float l2n = 0.f;
+    if (l2 != 0.f) {
+        {
+            Launch L(p, st, K_SGD);
+            wino::sumsq_kernel<<<1, 1024, 0, st>>>(vals, p->nnz, p->d_scalar);
+            if ((rc = L.done())) return rc;
+        }
+        double ss = 0.0;
+        CUDA_TRY(cudaMemcpyAsync(&ss, p->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        l2n = ss > 0.0 ? (float)(l2 / std::sqrt(ss)) : 0.f;
+    }
+    {
+        Launch L(p, st, K_SGD);
+        wino::sgd_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(vals, grad_w, p->nnz, lr, scale, l2n);
+        if ((rc = L.done())) return rc;
+    }
+    return wino_values_updated(p, stream);
+}
+
+int64_t wino_launch_count(const wino_plan* p) { return p ? p->launches : -1; }
+void wino_reset_launch_count(wino_plan* p) {
+    if (p) p->launches = 0;
+}
+
+int wino_profile_enable(wino_plan* p, int enable) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    p->prof = enable != 0;
+    return WINO_OK;
+}
+
+int wino_profile_read(wino_plan* p, int cap, const char** names, double* ms, int64_t* launches, int* n_kinds) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    for (auto& r : p->recs) {
+        CUDA_TRY(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+        p->prof_ms[r.kind] += t;
+        p->prof_n[r.kind] += 1;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    p->recs.clear();
+    const int n = std::min(cap, (int)K_NKINDS);
+    for (int k = 0; k < n; ++k) {
+        if (names) names[k] = kKindNames[k];
+        if (ms) ms[k] = p->prof_ms[k];
+        if (launches) launches[k] = p->prof_n[k];
+        p->prof_ms[k] = 0.0;
+        p->prof_n[k] = 0;
+    }
+    if (n_kinds) *n_kinds = n;
+    return WINO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,322 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the reference.
+
+Three anchors, strongest first:
+  * bitwise: the forward equals the reference's own f32 sparse_forward (golden vectors the
+    reference produced) and the f32 operation-order mirror (oracle/wino_oracle.py); dĨ_F/dI
+    equal the mirror bitwise too;
+  * tolerance: O, dI and dW_F (on the mask) within |d| <= 1e-5 + 1e-4·|ref| of the reference's
+    f64 dense layer, every element (BASELINE.json north_star);
+  * properties at full BASELINE sizes: determinism, sampled-oracle agreement, CSR structure.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import LAYER_CASES, assert_parity, fail_fraction, golden_csr_slices, load_layer
+from oracle import wino_oracle as wo
+import paper_1702_08597_b200 as wb
+from paper_1702_08597_b200.synth import CONFIGS, make_inputs, with_sparsity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    assert wb._lib.LIB_PATH.exists(), "libwino_b200.so not built"
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def run_layer(img, w_f, grad_o, m, pad, dense=None):
+    n, c, h, w = img.shape
+    k = w_f.shape[0]
+    layer = wb.WinogradLayer(c, k, h, w, pad=pad, m=m)
+    layer.set_weights(w_f, dense=dense)
+    cache = layer.new_cache(n)
+    o = layer.forward(dev(img), cache)
+    out = {"layer": layer, "o": o.cpu().numpy()}
+    if grad_o is not None:
+        dw = layer.backward_weights(dev(grad_o), cache)
+        di = layer.backward_input(cache)
+        torch.cuda.synchronize()
+        out["dw_raw"] = dw.cpu().numpy()
+        out["di"] = di.cpu().numpy()
+        out["dw"] = (out["dw_raw"].astype(np.float64) if layer.is_dense
+                     else layer.compact_to_dense(out["dw_raw"].astype(np.float64)))
+    return out
+
+
+@pytest.mark.parametrize("name", LAYER_CASES)
+def test_layer_vs_reference_golden(name):
+    d = load_layer(name)
+    r = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"])
+    # forward: bit-identical to the reference's f32 sparse_forward
+    assert np.array_equal(r["o"].astype(np.float64), d["o_sparse_f32"]), "forward not bitwise"
+    assert_parity(r["o"], d["o_f64"], "O vs f64 reference")
+    assert_parity(r["di"], d["grad_in_f64"], "dI vs f64 reference")
+    if r["layer"].is_dense:
+        assert_parity(r["dw"], d["grad_wf_f64"], "dW_F (dense) vs f64 reference")
+    else:
+        mask = d["w_f"] != 0
+        assert_parity(r["dw"][mask], d["grad_wf_f64"][mask], "dW_F on the mask vs f64 reference")
+        assert np.all(r["dw"][~mask] == 0)
+
+
+@pytest.mark.parametrize("name", LAYER_CASES)
+def test_layer_vs_f32_mirror_bitwise(name):
+    d = load_layer(name)
+    r = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False)
+    mir = wo.layer_f32(d["img"], wo.compress(d["w_f"]), d["grad_o"], m=d["m"], pad=d["pad"])
+    assert np.array_equal(r["o"], mir["o"])
+    assert np.array_equal(r["di"], mir["di"]), "dI not bitwise equal to the mirror"
+    dw_ref = np.concatenate(mir["dw"]) if mir["dw"] else np.zeros(0)
+    np.testing.assert_allclose(r["dw_raw"], dw_ref, rtol=2e-6, atol=1e-6 * max(1.0, np.abs(dw_ref).max()))
+
+
+@pytest.mark.parametrize("name", ["c0", "f63"])
+def test_device_csr_matches_reference_compress(name):
+    d = load_layer(name)
+    layer = wb.WinogradLayer(d["c"], d["k"], d["h"], d["w"], pad=d["pad"], m=d["m"])
+    layer.set_weights(d["w_f"], dense=False)
+    csr = layer.get_csr()
+    rps, cols, vals = golden_csr_slices(d)
+    for s in range(len(rps)):
+        assert np.array_equal(csr.row_ptr[s].astype(np.int64), rps[s])
+        assert np.array_equal(csr.col_idx[s].astype(np.int64), cols[s])
+        assert np.array_equal(csr.values[s], vals[s])
+    assert layer.nnz == int(d["csr_nnz"].sum())
+
+
+def test_set_weights_csr_equals_set_weights():
+    d = load_layer("c0")
+    a = run_layer(d["img"], d["w_f"], d["grad_o"], 4, 1, dense=False)
+    layer = wb.WinogradLayer(d["c"], d["k"], d["h"], d["w"], pad=1, m=4)
+    layer.set_weights_csr(wb.compress(d["w_f"]))
+    cache = layer.new_cache(1)
+    o = layer.forward(dev(d["img"]), cache).cpu().numpy()
+    assert np.array_equal(o, a["o"])
+
+
+def test_corrupt_csr_rejected():
+    # test_sparse.cpp:155-168 — and the row_ptr length / monotonicity the reference never checks
+    layer = wb.WinogradLayer(2, 2, 6, 6, pad=0, m=4)
+    csr = wb.compress(np.ones((2, 2, 6, 6)))
+    bad = wb.PointwiseCsr(csr.k, csr.c, csr.p, list(csr.row_ptr), list(csr.col_idx), list(csr.values))
+    bad.col_idx[3] = bad.col_idx[3].copy()
+    bad.col_idx[3][0] = 5  # out of bounds
+    with pytest.raises(wb.CorruptFormatError):
+        layer.set_weights_csr(bad)
+    bad = wb.PointwiseCsr(csr.k, csr.c, csr.p, list(csr.row_ptr), list(csr.col_idx), list(csr.values))
+    bad.row_ptr[0] = np.array([0, 3, 2], dtype=np.uint64)  # not monotone / wrong end
+    with pytest.raises(wb.CorruptFormatError):
+        layer.set_weights_csr(bad)
+    bad = wb.PointwiseCsr(csr.k, csr.c, csr.p, list(csr.row_ptr), list(csr.col_idx), list(csr.values))
+    bad.col_idx[0] = np.array([1, 0, 0, 1], dtype=np.uint64)  # not increasing within a row
+    with pytest.raises(wb.CorruptFormatError):
+        layer.set_weights_csr(bad)
+
+
+def test_backward_input_requires_backward_weights():
+    # test_layer.cpp:132-140 (ConsistencyError)
+    d = load_layer("f43_tiny")
+    layer = wb.WinogradLayer(d["c"], d["k"], d["h"], d["w"], pad=d["pad"], m=4)
+    layer.set_weights(d["w_f"])
+    cache = layer.new_cache(1)
+    with pytest.raises(wb.ConsistencyError):
+        layer.backward_input(cache)
+    layer.forward(dev(d["img"]), cache)
+    with pytest.raises(wb.ConsistencyError):
+        layer.backward_input(cache)
+    layer.backward_weights(dev(d["grad_o"]), cache)
+    layer.backward_input(cache)
+    layer.forward(dev(d["img"]), cache)  # a new forward clears dL/dZ (layer.cpp:88)
+    with pytest.raises(wb.ConsistencyError):
+        layer.backward_input(cache)
+
+
+def test_shape_errors():
+    layer = wb.WinogradLayer(3, 4, 8, 8, pad=1, m=4)
+    with pytest.raises(wb.ConsistencyError):
+        layer.forward(dev(np.zeros((1, 3, 8, 8))))  # no weights yet
+    layer.set_weights(np.ones((4, 3, 6, 6)))
+    with pytest.raises(wb.ShapeError):
+        layer.forward(dev(np.zeros((1, 2, 8, 8))))
+    with pytest.raises(wb.ShapeError):
+        layer.set_weights(np.ones((4, 3, 4, 4)))
+    cache = layer.new_cache(1)
+    with pytest.raises(wb.ShapeError):
+        layer.forward(dev(np.zeros((2, 3, 8, 8))), cache)  # batch exceeds the cache
+
+
+@pytest.mark.parametrize("sparsity", [0.0, 0.5, 0.9, 1.0])
+def test_densities_against_f64_oracle(sparsity):
+    """acceptance.cpp:114-152 style sweep incl. the all-zero (density 0) and full-density CSR."""
+    cfg = with_sparsity(CONFIGS["c0"], sparsity)
+    img, w_f, go = make_inputs(cfg, n=2)
+    r = run_layer(img, w_f, go, 4, 1, dense=False)
+    imgp = np.pad(img.astype(np.float64), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    gw = np.zeros_like(w_f)
+    for i in range(2):
+        o, cache = wo.forward_f64(imgp[i], w_f, 4)
+        assert_parity(r["o"][i], o, f"O[{i}]")
+        gw += wo.backward_weights_f64(go[i].astype(np.float64), cache)
+        assert_parity(r["di"][i], wo.backward_input_f64(cache, w_f)[:, 1:-1, 1:-1], f"dI[{i}]")
+    mask = w_f != 0
+    assert_parity(r["dw"][mask], gw[mask], "dW on mask")
+
+
+def test_dense_plan_against_f64_oracle():
+    cfg = with_sparsity(CONFIGS["c0"], 0.0)
+    img, w_f, go = make_inputs(cfg, n=2)
+    w_f[0, 0, 0, 0] = 0.0  # an exact zero still gets a gradient on the dense path
+    r = run_layer(img, w_f, go, 4, 1, dense=True)
+    assert r["layer"].is_dense and r["dw"].shape == w_f.shape
+    imgp = np.pad(img.astype(np.float64), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    gw = np.zeros_like(w_f)
+    for i in range(2):
+        o, cache = wo.forward_f64(imgp[i], w_f, 4)
+        assert_parity(r["o"][i], o, "O")
+        gw += wo.backward_weights_f64(go[i].astype(np.float64), cache)
+    assert_parity(r["dw"], gw, "dense dW")
+    assert r["dw"][0, 0, 0, 0] != 0.0
+
+
+def _f64_batched(img, w_f, go, pad, m=4):
+    """Fast f64 restatement (per-slice BLAS) of layer.cpp over a batch, for large parity cases."""
+    n, c, h, w = img.shape
+    g = wo.padded_geometry(c, h, w, pad, m)
+    a, b, _ = wo.transforms(m)
+    p = g.p
+    imgp = np.zeros((n, c, g.h_ip, g.w_ip))
+    imgp[:, :, pad:pad + h, pad:pad + w] = img
+    til = np.stack([imgp[:, :, (t // g.tiles_x) * m:(t // g.tiles_x) * m + p,
+                         (t % g.tiles_x) * m:(t % g.tiles_x) * m + p] for t in range(g.t)], axis=2)
+    v = np.einsum("ki,nctkl,lj->ijcnt", b, til, b).reshape(p * p, c, n * g.t)
+    wsl = w_f.transpose(2, 3, 0, 1).reshape(p * p, w_f.shape[0], c)
+    z = np.matmul(wsl, v)
+    k = w_f.shape[0]
+    zz = z.reshape(p, p, k, n, g.tiles_y, g.tiles_x)
+    ot = np.einsum("iy,ijknab,jx->nkaybx", a, zz, a).reshape(n, k, g.h_op, g.w_op)[:, :, :g.h_o, :g.w_o]
+    full = np.zeros((n, k, g.h_op, g.w_op))
+    full[:, :, :g.h_o, :g.w_o] = go
+    dot = full.reshape(n, k, g.tiles_y, m, g.tiles_x, m)
+    dz = np.einsum("iy,nkaybx,jx->ijknab", a, dot, a).reshape(p * p, k, n * g.t)
+    dw = np.matmul(dz, v.transpose(0, 2, 1)).reshape(p, p, k, c).transpose(2, 3, 0, 1)
+    dv = np.matmul(wsl.transpose(0, 2, 1), dz).reshape(p, p, c, n, g.tiles_y, g.tiles_x)
+    gt = np.einsum("ik,klcnab,jl->ncabij", b, dv, b)
+    di = np.zeros((n, c, g.h_ip, g.w_ip))
+    for ty in range(g.tiles_y):
+        for tx in range(g.tiles_x):
+            di[:, :, ty * m:ty * m + p, tx * m:tx * m + p] += gt[:, :, ty, tx]
+    return ot, dw, di[:, :, pad:pad + h, pad:pad + w]
+
+
+def test_c1_full_batch_parity():
+    """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%): every element."""
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg)
+    r = run_layer(img, w_f, go, 4, 1, dense=False)
+    o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
+    assert_parity(r["o"], o, "c1 O")
+    assert_parity(r["di"], di, "c1 dI")
+    mask = w_f != 0
+    frac = fail_fraction(r["dw"][mask], dw[mask])
+    assert frac == 0.0, f"c1 dW_F: {frac:.2e} of surviving entries outside tolerance"
+    # and bitwise against the f32 mirror (reference association order) for the forward
+    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
+    assert np.array_equal(r["o"], mir["o"])
+
+
+def test_determinism_and_repeatability():
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg, n=8)
+    a = run_layer(img, w_f, go, 4, 1, dense=False)
+    b = run_layer(img, w_f, go, 4, 1, dense=False)
+    for key in ("o", "di", "dw_raw"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.slow
+def test_c3_sparse_sampled_parity():
+    """configs[3] (N=64, C=K=256, H=56) at 90%: full-size run, oracle on sampled images."""
+    cfg = CONFIGS["c3"]
+    img, w_f, go = make_inputs(cfg)
+    r = run_layer(img, w_f, go, 4, 1, dense=False)
+    sub = [0, 37]
+    o, _, di = _f64_batched(img[sub].astype(np.float64), w_f, go[sub].astype(np.float64), 1)
+    assert_parity(r["o"][sub], o, "c3 O (sampled images)")
+    assert_parity(r["di"][sub], di, "c3 dI (sampled images)")
+    # dW needs the whole batch: check sampled rows of every slice against an f64 dot product
+    v, g = wo.input_transform_f32(img, 4, 1)
+    dz = wo.grad_z_f32(go, g, 4)
+    csr = wo.compress(w_f)
+    off = 0
+    worst = 0.0
+    for s in range(36):
+        n = len(csr.values[s])
+        e = np.arange(0, n, 97)
+        rows = np.repeat(np.arange(cfg.k), np.diff(csr.row_ptr[s]))[e]
+        cols = csr.col_idx[s][e]
+        ref_ = np.einsum("et,et->e", dz[s][rows].astype(np.float64), v[s][cols].astype(np.float64))
+        got = r["dw_raw"][off + e]
+        worst = max(worst, float(np.max(np.abs(got - ref_) / (1e-5 + 1e-4 * np.abs(ref_)))))
+        off += n
+    assert worst <= 1.0, f"c3 dW sampled: worst error / tolerance = {worst:.3f}"
+
+
+def test_relu_flags_and_sgd():
+    d = load_layer("c0")
+    layer = wb.WinogradLayer(d["c"], d["k"], d["h"], d["w"], pad=1, m=4)
+    layer.set_weights(d["w_f"])
+    cache = layer.new_cache(1)
+    o = layer.forward(dev(d["img"]), cache, relu=True).cpu().numpy()
+    mir = wo.layer_f32(d["img"], wo.compress(d["w_f"]), None, m=4, pad=1)
+    assert np.array_equal(o, np.maximum(mir["o"], 0))
+    o_dev = dev(o)
+    dw = layer.backward_weights(dev(d["grad_o"]), cache, relu_out=o_dev)
+    masked = d["grad_o"] * (o > 0)
+    mir2 = wo.layer_f32(d["img"], wo.compress(d["w_f"]), masked, m=4, pad=1)
+    np.testing.assert_allclose(dw.cpu().numpy(), np.concatenate(mir2["dw"]), rtol=2e-6, atol=1e-5)
+    # masked SGD: only surviving values move; v -= lr*(scale*g + l2*v/||v||)
+    vals0 = np.concatenate(wb.compress(d["w_f"]).values).astype(np.float64)
+    layer.sgd_step(dw, lr=0.1, scale=0.5, l2=0.01)
+    torch.cuda.synchronize()
+    vals1 = np.concatenate(layer.get_csr().values)
+    g = dw.cpu().numpy().astype(np.float64)
+    expect = vals0 - 0.1 * (0.5 * g + 0.01 * vals0 / np.sqrt(np.sum(vals0 ** 2)))
+    np.testing.assert_allclose(vals1, expect, rtol=1e-5, atol=1e-7)
+
+
+def test_api_reference_surface():
+    """python/tests/test_smoke.py cases, served by the GPU (fp32 tolerances)."""
+    rng = np.random.default_rng(0)
+    img = rng.standard_normal((3, 9, 11))
+    w = rng.standard_normal((2, 3, 3, 3))
+    out = wb.conv_winograd(img, wb.lift(w), m=2)
+    assert out.shape == (2, 7, 9)
+    np.testing.assert_allclose(out, wo.direct_conv_f64(img, w), atol=1e-4)
+    img = rng.standard_normal((2, 12, 12))
+    w = rng.standard_normal((2, 2, 3, 3))
+    np.testing.assert_allclose(wb.conv_winograd(img, wb.lift(w, m=4), m=4), wo.direct_conv_f64(img, w),
+                               atol=1e-4)
+    img = rng.standard_normal((1, 6, 6))
+    w_f = rng.standard_normal((2, 1, 4, 4))
+    out = wb.conv_winograd(img, w_f)
+    gw, gi = wb.conv_winograd_grad(img, w_f, out)
+    o64, cache = wo.forward_f64(img, w_f, 2)
+    np.testing.assert_allclose(gw, wo.backward_weights_f64(o64, cache), rtol=1e-4, atol=1e-4)
+    np.testing.assert_allclose(gi, wo.backward_input_f64(cache, w_f), rtol=1e-4, atol=1e-4)
+    batch = rng.standard_normal((2, 3, 8, 8))
+    w_f = rng.standard_normal((4, 3, 4, 4))
+    w_f[np.abs(w_f) < 0.8] = 0.0
+    out = wb.sparse_conv(batch, w_f, workers=1)
+    assert np.array_equal(out, wb.sparse_conv(batch, w_f, workers=4))
+    for n in range(2):
+        np.testing.assert_allclose(out[n], wo.forward_f64(batch[n], w_f, 2)[0], rtol=1e-4, atol=1e-4)
+    with pytest.raises(wb.CapabilityError):
+        wb.sparse_conv(batch, w_f, precision="f64")
