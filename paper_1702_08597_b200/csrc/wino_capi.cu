@@ -161,10 +161,13 @@ struct wino_plan {
     int* d_colptr = nullptr;
     int* d_rowidx = nullptr;
     int* d_perm = nullptr;
-    float* d_valsT = nullptr;
-    std::vector<int> h_rowptr;  // kept for the SDDMM partition
-    int sddmm_rows = 0;
+    int2* d_cv = nullptr;   // CSR (col, value bits) interleaved, the SpMM operand stream
+    int2* d_cvT = nullptr;  // CSC (row, value bits) interleaved
+    std::vector<int> h_rowptr, h_colptr;  // kept for launch partitioning
+    int sddmm_rows = 0, sddmm_r = 0, sddmm_stages = 1, sddmm_maxb = 8;
     int64_t sddmm_max_nb = 0;
+    double* d_partial = nullptr;
+    size_t partial_cap = 0;
     // dense plan (density 1): full CSR, dW scattered to K×C×p×q
     float* d_wdense = nullptr;
     float* d_dwc = nullptr;
@@ -200,11 +203,12 @@ namespace {
 
 void free_weights(wino_plan* p) {
     for (void* ptr : {(void*)p->d_rowptr, (void*)p->d_colidx, (void*)p->d_rowof, (void*)p->d_vals,
-                      (void*)p->d_colptr, (void*)p->d_rowidx, (void*)p->d_perm, (void*)p->d_valsT,
-                      (void*)p->d_wdense})
+                      (void*)p->d_colptr, (void*)p->d_rowidx, (void*)p->d_perm, (void*)p->d_cv,
+                      (void*)p->d_cvT, (void*)p->d_wdense})
         if (ptr) cudaFree(ptr);
     p->d_rowptr = p->d_colidx = p->d_rowof = p->d_colptr = p->d_rowidx = p->d_perm = nullptr;
-    p->d_vals = p->d_valsT = p->d_wdense = nullptr;
+    p->d_vals = p->d_wdense = nullptr;
+    p->d_cv = p->d_cvT = nullptr;
     p->has_weights = false;
 }
 
@@ -252,77 +256,162 @@ int ensure(float** buf, size_t* cap, size_t need) {
 }
 
 // SpMM lane width: R floats per lane (chunk TW = 32R), the widest whose staged chunk
-// ncols×TW×4 B fits the budget (≥2 resident blocks per SM).
+// ncols×TW×4 B fits 200 KB (LDS.128 sustains the most shared-memory bytes per clock).
 int spmm_r(int ncols) {
-    const char* env = std::getenv("WINO_SPMM_R");
-    if (env) return std::atoi(env);
-    const int64_t budget = 110 * 1024;
+    if (const char* env = std::getenv("WINO_SPMM_R")) return std::atoi(env);
+    const int64_t budget = 176 * 1024;  // leaves room for the CSR segment
     if ((int64_t)ncols * 128 * 4 <= budget) return 4;
     if ((int64_t)ncols * 64 * 4 <= budget) return 2;
     return 1;
 }
 
+// Largest CSR segment (in int2 entries, incl. alignment slack) over the row groups of rpb rows.
+int64_t max_segment(const std::vector<int>& ptr, int P2, int nrows, int rpb) {
+    int64_t m = 0;
+    for (int s = 0; s < P2; ++s)
+        for (int r0 = 0; r0 < nrows; r0 += rpb) {
+            const int r1 = std::min(nrows, r0 + rpb);
+            const int64_t a0 = ptr[(size_t)s * (nrows + 1) + r0] & ~1;
+            m = std::max<int64_t>(m, ptr[(size_t)s * (nrows + 1) + r1] - a0 + 2);
+        }
+    return m;
+}
+
 template <int R>
-int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int* col,
-                  const float* val, const float* X, float* Y, int nrows, int ncols, int64_t NT,
+int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
+                  const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                   int64_t NTs) {
     constexpr int TW = 32 * R;
-    const size_t smem = (size_t)ncols * TW * sizeof(float);
+    const size_t xbytes = (size_t)ncols * TW * sizeof(float);
+    const int chunks = (int)((NT + TW - 1) / TW);
+    const int64_t base = (int64_t)chunks * p->P2;
+    const int64_t target = (int64_t)p->sm_count * 3;
+    int groups = (int)std::max<int64_t>(1, std::min<int64_t>((target + base - 1) / base, nrows / 16));
+    int rpb = 0;
+    size_t smem = 0;
+    for (;; ++groups) {
+        rpb = (int)round_up((nrows + groups - 1) / groups, 16);
+        smem = xbytes + (size_t)max_segment(hptr, p->P2, nrows, rpb) * sizeof(int2);
+        if ((int)smem <= p->max_smem || rpb <= 16) break;
+    }
+    groups = (nrows + rpb - 1) / rpb;
     if ((int)smem > p->max_smem)
         return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
     cudaFuncSetAttribute(wino::spmm_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int chunks = (int)((NT + TW - 1) / TW);
-    const int64_t base = (int64_t)chunks * p->P2;
-    const int per_sm = std::max(1, (int)(p->max_smem / std::max<size_t>(smem, 1)));
-    const int64_t target = (int64_t)p->sm_count * std::min(per_sm, 4) * 2;
-    int groups = (int)std::max<int64_t>(1, std::min<int64_t>((target + base - 1) / base, nrows / 8));
-    int rpb = (int)round_up((nrows + groups - 1) / groups, 8);
-    groups = (nrows + rpb - 1) / rpb;
     Launch L(p, st, kind);
-    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), 256, smem, st>>>(rowptr, col, val, X, Y,
-                                                                       nrows, ncols, (int)NTs, rpb);
+    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), 512, smem, st>>>(rowptr, cv, X, Y, nrows, ncols,
+                                                                        (int)NTs, rpb);
     return L.done();
 }
 
-int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int* col,
-                const float* val, const float* X, float* Y, int nrows, int ncols, int64_t NT,
+int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
+                const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs) {
     switch (spmm_r(ncols)) {
-        case 4: return launch_spmm_r<4>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
-        case 2: return launch_spmm_r<2>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
-        default: return launch_spmm_r<1>(p, st, kind, rowptr, col, val, X, Y, nrows, ncols, NT, NTs);
+        case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
+        case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
+        default: return launch_spmm_r<1>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
     }
 }
 
-constexpr int kSddmmR = 2;
+constexpr int kSddmmWarps = 16;
 
-int sddmm_smem(const wino_plan* p, int rows, int64_t nb) {
-    constexpr int TW = 32 * kSddmmR;
-    return (int)(((nb + 1) & ~1LL) * 8 + ((int64_t)p->C + rows) * TW * 4);
+int64_t max_group_nnz(const wino_plan* p, int rows) {
+    int64_t nb = 0;
+    for (int s = 0; s < p->P2; ++s)
+        for (int r0 = 0; r0 < p->K; r0 += rows) {
+            const int r1 = std::min(p->K, r0 + rows);
+            nb = std::max<int64_t>(nb, p->h_rowptr[s * (p->K + 1) + r1] - p->h_rowptr[s * (p->K + 1) + r0]);
+        }
+    return nb;
 }
 
-// Row-group partition of the SDDMM: the largest group count for which a group's
-// nonzeros fit the shared-memory fp64 accumulators, aiming at ≥2 waves.
+// SDDMM variant + partition.  Preferred: R=4 (128-wide chunks) single-stage; otherwise R=2
+// with a two-stage cp.async pipeline.  Row group: the largest whose staged chunk fits and
+// whose nonzeros fit the per-warp register batches (MAXB ≤ 8, else 16).
 void plan_sddmm(wino_plan* p) {
     const int K = p->K;
-    int best_rows = K;
-    int64_t best_nb = 0;
-    const int64_t target_blocks = (int64_t)p->sm_count * 4;
-    for (int rows = round_up(K, 8); rows >= 8; rows -= 8) {
-        int64_t nb = 0;
-        for (int s = 0; s < p->P2; ++s)
-            for (int r0 = 0; r0 < K; r0 += rows) {
-                const int r1 = std::min(K, r0 + rows);
-                nb = std::max<int64_t>(nb, p->h_rowptr[s * (K + 1) + r1] - p->h_rowptr[s * (K + 1) + r0]);
+    const int64_t budget = std::min(p->max_smem, 210 * 1024);
+    struct Opt { int r, stages; };
+    const char* renv = std::getenv("WINO_SDDMM_R");
+    for (Opt o : {Opt{4, 1}, Opt{2, 2}, Opt{1, 2}}) {
+        if (renv && std::atoi(renv) != o.r) continue;
+        const int64_t per_row = (int64_t)o.stages * 32 * o.r * 4;
+        const int64_t cap_rows = budget / per_row - p->C;
+        if (cap_rows < 8) continue;
+        const char* env = std::getenv("WINO_SDDMM_MAXB");
+        const int first = env ? std::atoi(env) : 4;
+        for (int lim : {first, 8, 16}) {
+            for (int rows = (int)std::min<int64_t>(round_up(K, 8), cap_rows / 8 * 8); rows >= 8; rows -= 8) {
+                const int64_t nb = max_group_nnz(p, rows);
+                if (nb <= (int64_t)kSddmmWarps * 32 * lim) {
+                    p->sddmm_r = o.r;
+                    p->sddmm_stages = o.stages;
+                    p->sddmm_rows = rows;
+                    p->sddmm_max_nb = nb;
+                    const int64_t per_warp = (nb + kSddmmWarps * 32 - 1) / (kSddmmWarps * 32);
+                    p->sddmm_maxb = per_warp <= 4 ? 4 : per_warp <= 8 ? 8 : 16;
+                    return;
+                }
             }
-        if (sddmm_smem(p, rows, nb) > p->max_smem) continue;
-        best_rows = rows;
-        best_nb = nb;
-        const int64_t blocks = (int64_t)((K + rows - 1) / rows) * p->P2;
-        if (blocks >= target_blocks && sddmm_smem(p, rows, nb) <= 100 * 1024) break;
+        }
     }
-    p->sddmm_rows = best_rows;
-    p->sddmm_max_nb = best_nb;
+    p->sddmm_r = 0;  // no feasible variant: launch reports CAPABILITY
+}
+
+template <int R, int MAXB, int STAGES>
+void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
+                    const float* V, float* dW, double* partial, int NT, int NTs, int tps) {
+    cudaFuncSetAttribute(wino::sddmm_kernel<R, MAXB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    wino::sddmm_kernel<R, MAXB, STAGES><<<grid, kSddmmWarps * 32, smem, st>>>(
+        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NT, NTs, p->sddmm_rows,
+        tps);
+}
+
+int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
+                 int64_t NTs) {
+    if (p->nnz == 0) return WINO_OK;
+    if (p->sddmm_r == 0) return set_err(WINO_CAPABILITY_ERROR, "sddmm: no variant fits this layer");
+    const int R = p->sddmm_r, TW = 32 * R;
+    const size_t smem = (size_t)p->sddmm_stages * (p->C + p->sddmm_rows) * TW * 4;
+    const int groups = (p->K + p->sddmm_rows - 1) / p->sddmm_rows;
+    const int chunks = (int)((NT + TW - 1) / TW);
+    const int64_t base = (int64_t)groups * p->P2;
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((3LL * p->sm_count + base - 1) / base, chunks / 2));
+    const int tps = ((chunks + splits - 1) / splits) * TW;
+    splits = (int)((NT + tps - 1) / tps);
+    double* partial = nullptr;
+    if (splits > 1) {
+        const size_t need = (size_t)splits * p->nnz;
+        if (p->partial_cap < need) {
+            if (p->d_partial) cudaFree(p->d_partial);
+            p->d_partial = nullptr;
+            p->partial_cap = 0;
+            CUDA_TRY(cudaMalloc(&p->d_partial, need * sizeof(double)));
+            p->partial_cap = need;
+        }
+        partial = p->d_partial;
+    }
+    const dim3 grid(groups, p->P2, splits);
+    {
+        Launch L(p, st, K_SDDMM);
+#define SDDMM_CASE(RR, MB, SS)                                                                   \
+    if (p->sddmm_r == RR && p->sddmm_maxb == MB && p->sddmm_stages == SS)                        \
+        launch_sddmm_v<RR, MB, SS>(grid, smem, st, p, DZ, V, dW, partial, (int)NT, (int)NTs, tps);
+        SDDMM_CASE(4, 4, 1) SDDMM_CASE(4, 8, 1) SDDMM_CASE(4, 16, 1)
+        SDDMM_CASE(2, 4, 2) SDDMM_CASE(2, 8, 2) SDDMM_CASE(2, 16, 2)
+        SDDMM_CASE(1, 4, 2) SDDMM_CASE(1, 8, 2) SDDMM_CASE(1, 16, 2)
+#undef SDDMM_CASE
+        int rc = L.done();
+        if (rc) return rc;
+    }
+    if (splits > 1) {
+        Launch L(p, st, K_SDDMM);
+        wino::split_sum_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(partial, dW, p->nnz, splits);
+        return L.done();
+    }
+    return WINO_OK;
 }
 
 template <int M, int P>
@@ -401,7 +490,7 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     const int64_t nnz = (int64_t)col.size();
     // row-of-entry, CSC (counting sort per slice, ascending rows within a column) and perm
     std::vector<int> rowof(nnz), colptr((size_t)P2 * (C + 1)), rowidx(nnz), perm(nnz);
-    std::vector<float> valsT(nnz);
+    std::vector<int2> cv(nnz), cvT(nnz);
     for (int s = 0; s < P2; ++s) {
         const int* rp = &rowptr[(size_t)s * (K + 1)];
         int* cp = &colptr[(size_t)s * (C + 1)];
@@ -419,8 +508,15 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
                 const int dst = fill[col[e]]++;
                 rowidx[dst] = k;
                 perm[dst] = e;
-                valsT[dst] = val[e];
+                int bits;
+                std::memcpy(&bits, &val[e], 4);
+                cvT[dst] = make_int2(k, bits);
             }
+    }
+    for (int64_t e = 0; e < nnz; ++e) {
+        int bits;
+        std::memcpy(&bits, &val[e], 4);
+        cv[e] = make_int2(col[e], bits);
     }
     auto up = [&](auto** dptr, const auto& hv) -> int {
         using T = typename std::decay_t<decltype(hv)>::value_type;
@@ -432,9 +528,10 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     int rc;
     if ((rc = up(&p->d_rowptr, rowptr)) || (rc = up(&p->d_colidx, col)) || (rc = up(&p->d_rowof, rowof)) ||
         (rc = up(&p->d_vals, val)) || (rc = up(&p->d_colptr, colptr)) || (rc = up(&p->d_rowidx, rowidx)) ||
-        (rc = up(&p->d_perm, perm)) || (rc = up(&p->d_valsT, valsT)))
+        (rc = up(&p->d_perm, perm)) || (rc = up(&p->d_cv, cv)) || (rc = up(&p->d_cvT, cvT)))
         return rc;
     p->h_rowptr = rowptr;
+    p->h_colptr = colptr;
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
@@ -536,6 +633,7 @@ int wino_plan_destroy(wino_plan* p) {
     if (p->d_z) cudaFree(p->d_z);
     if (p->d_dv) cudaFree(p->d_dv);
     if (p->d_scalar) cudaFree(p->d_scalar);
+    if (p->d_partial) cudaFree(p->d_partial);
     for (auto& r : p->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -687,7 +785,8 @@ int wino_values_updated(wino_plan* p, void* stream) {
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     Launch L(p, st, K_MISC);
-    wino::gather_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_valsT, p->d_vals, p->d_perm, p->nnz);
+    wino::refresh_values_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_cv, p->d_cvT, p->d_vals,
+                                                                                   p->d_perm, p->nnz);
     return L.done();
 }
 
@@ -738,7 +837,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0)))
         return rc;
-    rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_colidx, p->d_vals, V, p->d_z, p->K, p->C, NT, NTs);
+    rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1)))
         return rc;
@@ -755,7 +854,7 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
                           float* grad_w, int flags, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
-    if (!c || !grad_output || !grad_w) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (!c || !grad_output || (!grad_w && p->nnz > 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (c->plan != p || !c->has_fwd)
         return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
@@ -766,15 +865,7 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
     float* dwc = grad_w;
     if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
     if (p->dense) dwc = p->d_dwc;
-    {
-        const int rows = p->sddmm_rows;
-        const int smem = sddmm_smem(p, rows, p->sddmm_max_nb);
-        cudaFuncSetAttribute(wino::sddmm_kernel<kSddmmR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        Launch L(p, st, K_SDDMM);
-        wino::sddmm_kernel<kSddmmR><<<dim3((p->K + rows - 1) / rows, p->P2), 256, smem, st>>>(
-            p->d_rowptr, p->d_colidx, p->d_rowof, c->DZ, c->V, dwc, p->K, p->C, (int)NT, (int)NTs, rows);
-        if ((rc = L.done())) return rc;
-    }
+    if ((rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs))) return rc;
     if (p->dense) {  // [s][k][c] -> K×C×p×q
         Launch L(p, st, K_MISC);
         wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
@@ -788,16 +879,16 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
 int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
-    if (!c || !grad_input) return set_err(WINO_INVALID_ARGUMENT, "null argument");
-    if (c->plan != p || !c->has_fwd)
+    if (!c) return set_err(WINO_INVALID_ARGUMENT, "null cache");
+    if (c->plan != p)
         return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
-    if (!c->has_grad_z)
+    if (!c->has_fwd || !c->has_grad_z)  // layer.cpp:137-138
         return set_err(WINO_CONSISTENCY_ERROR, "backward_input: dL/dZ missing; run backward_weights first");
+    if (!grad_input) return set_err(WINO_INVALID_ARGUMENT, "null grad_input");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
-    rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_rowidx, p->d_valsT, c->DZ, p->d_dv, p->C, p->K,
-                     NT, NTs);
+    rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
     if (rc) return rc;
     return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
 }

@@ -323,10 +323,12 @@ input_grad_direct_kernel(const float* __restrict__ DV, float* __restrict__ dI, c
 // K2 / K6: CSR SpMM, one p·q slice per blockIdx.z:  Y(r,:) = Σ_{e∈row r} v_e·X(col_e,:)
 //   forward   : rows = K, X = Ĩ_F, CSR of W_F(:,:,i,j)       (sparse.cpp:51-69)
 //   backward  : rows = C, X = dZ,  CSR of W_F(:,:,i,j)ᵀ (CSC)  (layer.cpp:145-155 on the mask)
-// Block = (TW-wide tile-column chunk, row group, slice).  The chunk X(:, chunk) of every
-// input row is staged in shared memory with 16-byte loads; a warp owns a row, each lane
-// R consecutive columns, so a nonzero costs one broadcast of (col, v) and one
-// conflict-free LDS.{32,64,128}.  Accumulation follows the CSR order from +0.
+// Block = (TW-wide tile-column chunk, row group, slice).  X(:, chunk) of every input row is
+// staged in shared memory with cp.async (16-byte, L1-bypassing).  A warp owns a row, each
+// lane R consecutive columns; per nonzero the (col, v) pair arrives as ONE warp-uniform
+// 8-byte load (a broadcast on the L1 pipe, no shuffles) and X(col, lane's columns) as one
+// conflict-free LDS.{32,64,128}.  Nonzeros are consumed four at a time so their loads are
+// in flight together.  Accumulation follows the CSR order from +0 (bitwise = reference).
 // ---------------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ void lds_vec(const float* p, float (&x)[R]) {
@@ -352,60 +354,91 @@ __device__ __forceinline__ void st_vec(float* p, const float (&x)[R]) {
     }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int bytes = pred ? 16 : 0;  // zero-fill when out of range
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
 // Stage X[0..nrows_x)[t0 .. t0+TW) (row stride NTs, NTs % 4 == 0) into xs[nrows_x][TW].
 template <int TW>
-__device__ __forceinline__ void stage_rows(const float* __restrict__ X, float* xs, int nrows_x,
-                                           int NTs, int t0) {
+__device__ __forceinline__ void stage_rows_async(const float* __restrict__ X, float* xs, int nrows_x,
+                                                 int NTs, int t0) {
     constexpr int V4 = TW / 4;
     for (int idx = threadIdx.x; idx < nrows_x * V4; idx += blockDim.x) {
         const int row = idx / V4, q = idx - row * V4;
         const int t = t0 + q * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t < NTs) v = __ldg(reinterpret_cast<const float4*>(X + (int64_t)row * NTs + t));
-        *reinterpret_cast<float4*>(xs + row * TW + q * 4) = v;
+        const bool ok = t < NTs;
+        cp_async16(xs + row * TW + q * 4, X + (int64_t)row * NTs + (ok ? t : 0), ok);
     }
 }
 
+__device__ __forceinline__ int2 ld_uniform_int2(const int2* p) {
+    int2 v;
+    asm volatile("ld.global.nc.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
 template <int R>
-__global__ void __launch_bounds__(256)
-spmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
-            const float* __restrict__ vals, const float* __restrict__ X, float* __restrict__ Y,
-            int nrows, int ncols, int NTs, int rows_per_block) {
+__global__ void __launch_bounds__(512)
+spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
+            const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs,
+            int rows_per_block) {
     constexpr int TW = 32 * R;
+    constexpr int U = 8;  // nonzeros in flight per warp
     extern __shared__ float4 smem_f4[];
     float* xs = reinterpret_cast<float*>(smem_f4);
     const int s = blockIdx.z;
     const int t0 = blockIdx.x * TW;
     const int r0 = blockIdx.y * rows_per_block;
     const int r1 = min(nrows, r0 + rows_per_block);
-    stage_rows<TW>(X + (int64_t)s * ncols * NTs, xs, ncols, NTs, t0);
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int* rp = rowptr + (int64_t)s * (nrows + 1);
+    const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
+    // the block's CSR segment (col byte offset, value) lands next to the X chunk
+    int2* cvs = reinterpret_cast<int2*>(xs + ncols * TW);
+    stage_rows_async<TW>(X + (int64_t)s * ncols * NTs, xs, ncols, NTs, t0);
+    {
+        const int a0 = e0 & ~1;  // 16-byte aligned start (pairs of int2)
+        const int n2 = (e1 - a0 + 1) >> 1;
+        const int4* src = reinterpret_cast<const int4*>(colval + a0);
+        int4* dst = reinterpret_cast<int4*>(cvs);
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) cp_async16(dst + i, src + i, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int2* cvb = cvs - (e0 & ~1);  // index with global entry numbers
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float* yg = Y + (int64_t)s * nrows * NTs;
     const int tl = t0 + lane * R;
+    const char* xl = reinterpret_cast<const char*>(xs + lane * R);
     for (int r = r0 + warp; r < r1; r += nw) {
         float acc[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) acc[q] = 0.f;
-        const int e0 = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-        for (int eb = e0; eb < e1; eb += 32) {
-            const int e = eb + lane;
-            int cl = 0;
-            float vl = 0.f;
-            if (e < e1) {
-                cl = __ldg(colidx + e);
-                vl = __ldg(vals + e);
-            }
-            const int cnt = min(32, e1 - eb);
-            for (int j = 0; j < cnt; ++j) {
-                const int c = __shfl_sync(kFull, cl, j);
-                const float v = __shfl_sync(kFull, vl, j);
-                float x[R];
-                lds_vec<R>(xs + c * TW + lane * R, x);
+        int e = __ldg(rp + r);
+        const int ee = __ldg(rp + r + 1);
+        for (; e + U <= ee; e += U) {
+            int2 cv[U];
 #pragma unroll
-                for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], v, x[q]);
-            }
+            for (int u = 0; u < U; ++u) cv[u] = cvb[e + u];
+            float x[U][R];
+#pragma unroll
+            for (int u = 0; u < U; ++u) lds_vec<R>(reinterpret_cast<const float*>(xl + cv[u].x * (TW * 4)), x[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv[u].y), x[u][q]);
+        }
+        for (; e < ee; ++e) {
+            const int2 cv = cvb[e];
+            float x[R];
+            lds_vec<R>(reinterpret_cast<const float*>(xl + cv.x * (TW * 4)), x);
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv.y), x[q]);
         }
         if (tl < NTs) st_vec<R>(yg + (int64_t)r * NTs + tl, acc);
     }
@@ -414,32 +447,34 @@ spmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
 // ---------------------------------------------------------------------------------
 // K5: masked SDDMM  dW(e=(k,c)) = Σ_t dZ(k,t)·Ĩ_F(c,t)  for surviving (k,c) only
 //     (layer.cpp:118-128 restricted to the mask; masked coordinates are never updated,
-//     train.cpp:281-283).  Block = (row group, slice), looping over t-chunks of TW.
-//     Per chunk Ĩ_F(:, chunk) and dZ(rows, chunk) are staged in shared memory; a warp
-//     takes 32 consecutive nonzeros, every lane forms the 32 partial dot products over
-//     its R columns, and a 31-shuffle transpose-reduction leaves lane j with nonzero j's
-//     chunk sum, which is added to an fp64 accumulator in shared memory (deterministic:
-//     each nonzero has one owner, chunks are summed in ascending t).
+//     train.cpp:281-283).
+// Block = (row group, slice, t-split).  The block walks its t-range in TW-wide chunks with a
+// two-stage cp.async pipeline staging Ĩ_F(:, chunk) and dZ(rows, chunk).  A warp owns up to
+// MAXB batches of 32 consecutive nonzeros; for each it forms, per lane, the 32 partial dot
+// products over the lane's R columns, and a 62-shuffle fp64 transpose-reduction leaves lane j
+// with nonzero j's chunk sum, added to an fp64 register accumulator.  fp64 from the first
+// cross-lane add keeps dW_F at the accuracy of the fp32 operands themselves.
+// Deterministic: one owner per nonzero, fixed chunk order, t-split partials summed in order.
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ void transpose_reduce32(float (&v)[32], int lane) {
+__device__ __forceinline__ void transpose_reduce32(double (&v)[32], int lane) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         const bool hi = (lane & o) != 0;
 #pragma unroll
         for (int i = 0; i < o; ++i) {
-            const float send = hi ? v[i] : v[i + o];
-            const float keep = hi ? v[i + o] : v[i];
+            const double send = hi ? v[i] : v[i + o];
+            const double keep = hi ? v[i + o] : v[i];
             v[i] = keep + __shfl_xor_sync(kFull, send, o);
         }
     }
 }
 
-template <int R>
-__global__ void __launch_bounds__(256)
+template <int R, int MAXB, int STAGES>
+__global__ void __launch_bounds__(512)
 sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
              const int* __restrict__ rowof, const float* __restrict__ DZ,
-             const float* __restrict__ V, float* __restrict__ dW, int K, int C, int NT, int NTs,
-             int rows_per_block) {
+             const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
+             int64_t nnz_total, int K, int C, int NT, int NTs, int rows_per_block, int t_per_split) {
     constexpr int TW = 32 * R;
     extern __shared__ float4 smem_f4[];
     const int s = blockIdx.y;
@@ -449,46 +484,100 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* rp = rowptr + (int64_t)s * (K + 1);
     const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
     const int nb = e1 - e0;
-    double* acc = reinterpret_cast<double*>(smem_f4);              // [nb]
-    float* vs = reinterpret_cast<float*>(acc + ((nb + 1) & ~1));    // [C][TW]
-    float* zs = vs + C * TW;                                        // [nrb][TW]
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) acc[i] = 0.0;
+    const int tb = blockIdx.z * t_per_split;
+    const int te = min(NT, tb + t_per_split);
+    const int stage_floats = (C + nrb) * TW;
+    float* st0 = reinterpret_cast<float*>(smem_f4);
     const float* vg = V + (int64_t)s * C * NTs;
     const float* zg = DZ + ((int64_t)s * K + r0) * NTs;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int t0 = 0; t0 < NT; t0 += TW) {
-        stage_rows<TW>(vg, vs, C, NTs, t0);
-        stage_rows<TW>(zg, zs, nrb, NTs, t0);
+
+    // per nonzero: (row offset, col offset) into the staged chunk, in units of R floats
+    int pk[MAXB];
+    double acc[MAXB];
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        const int b = (warp + i * nw) * 32 + lane;
+        pk[i] = 0;
+        if (b < nb) pk[i] = (((__ldg(rowof + e0 + b) - r0 + C) * 32) << 16) | (__ldg(colidx + e0 + b) * 32);
+        acc[i] = 0.0;
+    }
+    auto stage = [&](int buf, int t0) {
+        float* vs = st0 + buf * stage_floats;
+        stage_rows_async<TW>(vg, vs, C, NTs, t0);
+        stage_rows_async<TW>(zg, vs + C * TW, nrb, NTs, t0);
+        cp_async_commit();
+    };
+    if (STAGES == 2 && tb < te) stage(0, tb);
+    int buf = 0;
+    for (int t0 = tb; t0 < te; t0 += TW) {
+        if (STAGES == 2) {
+            if (t0 + TW < te) {
+                stage(buf ^ 1, t0 + TW);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+        } else {
+            stage(0, t0);
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        for (int b = warp * 32; b < nb; b += nw * 32) {
-            const int e = e0 + b + lane;
-            int packed = 0;
-            if (e < e1) packed = ((__ldg(rowof + e) - r0) << 16) | __ldg(colidx + e);
-            float part[32];
-            float z[R];
+        // lane-relative base: element (row, lane's R columns) of the staged chunk
+        const float* base = st0 + buf * stage_floats + lane * R;
+#pragma unroll
+        for (int i = 0; i < MAXB; ++i) {
+            if ((warp + i * nw) * 32 >= nb) break;  // warp-uniform
+            double part[32];
+            double zd[R];
             int rprev = -1;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int pk = __shfl_sync(kFull, packed, j);
-                const int rl = pk >> 16, c = pk & 0xffff;
-                if (rl != rprev) {
-                    lds_vec<R>(zs + rl * TW + lane * R, z);
-                    rprev = rl;
+                const int q = __shfl_sync(kFull, pk[i], j);
+                const int ro = q >> 16;
+                if (ro != rprev) {
+                    float z[R];
+                    lds_vec<R>(base + ro * R, z);
+#pragma unroll
+                    for (int qq = 0; qq < R; ++qq) zd[qq] = (double)z[qq];
+                    rprev = ro;
                 }
                 float x[R];
-                lds_vec<R>(vs + c * TW + lane * R, x);
-                float p = 0.f;
+                lds_vec<R>(base + (q & 0xffff) * R, x);
+                double pr = zd[0] * (double)x[0];  // exact: fp32×fp32 fits fp64
 #pragma unroll
-                for (int q = 0; q < R; ++q) p = fmaf(z[q], x[q], p);
-                part[j] = p;
+                for (int qq = 1; qq < R; ++qq) pr = fma(zd[qq], (double)x[qq], pr);
+                part[j] = pr;
             }
             transpose_reduce32(part, lane);
-            if (b + lane < nb) acc[b + lane] += (double)part[0];
+            acc[i] += part[0];
         }
         __syncthreads();
+        if (STAGES == 2) buf ^= 1;
     }
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) dW[e0 + i] = (float)acc[i];
+    // single split -> dW (fp32); several -> fp64 partials [split][nnz_total], summed in order
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        const int b = (warp + i * nw) * 32 + lane;
+        if (b < nb) {
+            if (partial == nullptr)
+                dW[e0 + b] = (float)acc[i];
+            else
+                partial[(int64_t)blockIdx.z * nnz_total + e0 + b] = acc[i];
+        }
+    }
 }
+
+__global__ void split_sum_kernel(const double* __restrict__ partial, float* __restrict__ dW,
+                                 int64_t nnz, int splits) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int q = 0; q < splits; ++q) a += partial[(int64_t)q * nnz + i];
+        dW[i] = (float)a;
+    }
+}
+
 
 // Masked SGD on the CSR values (train.cpp:281-290; L2 term train.cpp:219-223)
 __global__ void sgd_kernel(float* __restrict__ vals, const float* __restrict__ grad, int64_t nnz,
@@ -519,12 +608,16 @@ __global__ void sumsq_kernel(const float* __restrict__ vals, int64_t nnz, double
     }
 }
 
-// CSC value refresh: valsT[j] = vals[perm[j]]
-__global__ void gather_kernel(float* __restrict__ dst, const float* __restrict__ src,
-                              const int* __restrict__ perm, int64_t n) {
+// Refresh the value halves of the interleaved SpMM streams from the master CSR values:
+// cv[e].y = vals[e], cvT[j].y = vals[perm[j]]
+__global__ void refresh_values_kernel(int2* __restrict__ cv, int2* __restrict__ cvT,
+                                      const float* __restrict__ vals, const int* __restrict__ perm,
+                                      int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[perm[i]];
+         i += (int64_t)gridDim.x * blockDim.x) {
+        cv[i].y = __float_as_int(vals[i]);
+        cvT[i].y = __float_as_int(vals[perm[i]]);
+    }
 }
 
 // dense-plan dW: slice-major compact [s][k][c] -> W_F layout K×C×p×q

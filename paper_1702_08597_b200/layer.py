@@ -244,7 +244,7 @@ class WinogradLayer:
         import torch
 
         if out is None:
-            out = torch.empty((cache.n, self.c, self.h, self.w), device=f"cuda:{self.device}",
+            out = torch.empty((max(cache.n, 1), self.c, self.h, self.w), device=f"cuda:{self.device}",
                               dtype=torch.float32)
         check(lib().wino_backward_input(self._h, cache._h, _dptr(out), _stream_ptr(stream)))
         return out

@@ -216,17 +216,39 @@ def _f64_batched(img, w_f, go, pad, m=4):
     return ot, dw, di[:, :, pad:pad + h, pad:pad + w]
 
 
+def _floor_dw(img, go, csr, pad=1, m=4):
+    """dW_F as an exact f64 dot product of the fp32 operands the kernels store (Ĩ_F, dZ in the
+    reference's fp32 association order) — the accuracy floor of any fp32-storage dW_F."""
+    v, g = wo.input_transform_f32(img, m, pad)
+    dz = wo.grad_z_f32(go, g, m)
+    return np.concatenate(wo.sddmm_f64(csr, dz, v))
+
+
 def test_c1_full_batch_parity():
-    """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%): every element."""
+    """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%).
+
+    O and dI: every element within |d| <= 1e-5 + 1e-4·|ref| of the f64 reference.
+    dW_F: a 512-term dot product with heavy cancellation.  Its accuracy floor with fp32
+    Ĩ_F/dZ storage (exact f64 dot of the stored operands) already misses the strict bound on
+    ~5e-5 of the surviving entries (19/353,647 here; SURVEY §8a measured the same effect).
+    So dW_F must (a) match that floor within the strict bound elementwise — the kernel adds
+    no error of its own — and (b) miss the strict bound vs the reference on no entry the
+    floor does not also miss."""
     cfg = CONFIGS["c1"]
     img, w_f, go = make_inputs(cfg)
     r = run_layer(img, w_f, go, 4, 1, dense=False)
     o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
     assert_parity(r["o"], o, "c1 O")
     assert_parity(r["di"], di, "c1 dI")
+    csr = wo.compress(w_f)
+    floor = _floor_dw(img, go, csr)
+    assert_parity(r["dw_raw"], floor, "c1 dW_F vs exact dot of the stored fp32 operands")
     mask = w_f != 0
-    frac = fail_fraction(r["dw"][mask], dw[mask])
-    assert frac == 0.0, f"c1 dW_F: {frac:.2e} of surviving entries outside tolerance"
+    got_bad = np.abs(r["dw"][mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
+    floor_dense = r["layer"].compact_to_dense(floor)
+    floor_bad = np.abs(floor_dense[mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
+    assert not np.any(got_bad & ~floor_bad), "dW_F misses the tolerance where the fp32 floor does not"
+    assert got_bad.mean() <= 1e-4, f"strict-tolerance misses {got_bad.mean():.2e}"
     # and bitwise against the f32 mirror (reference association order) for the forward
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(r["o"], mir["o"])
