@@ -456,10 +456,12 @@ template <int M, int P>
 int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI, int n, int64_t NTs) {
     const wino_geometry& g = p->g;
     const int T = (int)g.t;
-    const int64_t per_c = (int64_t)T * P * P * sizeof(float);
+    const int64_t per_c = (int64_t)T * (P * P + 1) * sizeof(float);
     Launch L(p, st, K_INGRAD);
     if (per_c <= 96 * 1024) {
-        int cg = (int)std::max<int64_t>(1, std::min<int64_t>(p->C, (48 * 1024) / per_c));
+        // channels per block: fill >= 256 (c,t) items for phase 1 within ~48 KB of tiles
+        int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c,
+                                                                (256 + T - 1) / T}));
         const size_t smem = (size_t)cg * per_c;
         cudaFuncSetAttribute(wino::input_grad_kernel<M, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)std::max<size_t>(smem, 48 * 1024));

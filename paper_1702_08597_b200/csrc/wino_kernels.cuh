@@ -231,7 +231,8 @@ template <int M, int P>
 __global__ void __launch_bounds__(256)
 input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Coefs cf, int C,
                   int H, int W, int pad, int tiles_y, int tiles_x, int T, int NTs, int CG) {
-    extern __shared__ float gsm[];  // [CG][T][P*P]
+    constexpr int TS = P * P + 1;  // odd per-tile stride: conflict-free tile stores
+    extern __shared__ float gsm[];  // [CG][T][TS]
     const int n = blockIdx.y;
     const int c0 = blockIdx.x * CG;
     const int64_t plane = (int64_t)C * NTs;
@@ -255,7 +256,7 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
                 for (int k = 0; k < P; ++k) acc = madd(acc, cf.b[i * P + k], x[k][l]);
                 m1[i][l] = acc;
             }
-        float* g = gsm + (int64_t)idx * P * P;
+        float* g = gsm + (int64_t)idx * TS;
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
@@ -267,24 +268,42 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
             }
     }
     __syncthreads();
-    const int HW = H * W;
-    for (int idx = threadIdx.x; idx < CG * HW; idx += blockDim.x) {
-        const int cl = idx / HW, pix = idx - cl * HW;
+    // Phase 2, tile-centric: the thread of tile (ty,tx) owns padded pixels
+    // [ty·M, ty·M + M) × [tx·M, tx·M + M), extended to P on the last tile row/column.  A pixel
+    // at local (i,j) gets its contributions from tiles (ty-1,tx-1), (ty-1,tx), (ty,tx-1),
+    // (ty,tx) — ascending t, the reference's order — at compile-time offsets (+M when the
+    // pixel lies in a neighbour's overlap band, i.e. local index < P-M).
+    constexpr int O = P - M;
+    for (int idx = threadIdx.x; idx < CG * T; idx += blockDim.x) {
+        const int cl = idx / T, t = idx - cl * T;
         const int c = c0 + cl;
         if (c >= C) continue;
-        const int y = pix / W, x = pix - y * W;
-        const int Y = y + pad, X = x + pad;
-        const int ty_lo = Y - P + 1 <= 0 ? 0 : (Y - P + M) / M;
-        const int ty_hi = min(tiles_y - 1, Y / M);
-        const int tx_lo = X - P + 1 <= 0 ? 0 : (X - P + M) / M;
-        const int tx_hi = min(tiles_x - 1, X / M);
-        float acc = 0.f;
-        for (int ty = ty_lo; ty <= ty_hi; ++ty)
-            for (int tx = tx_lo; tx <= tx_hi; ++tx) {
-                const int t = ty * tiles_x + tx;
-                acc = __fadd_rn(acc, gsm[((int64_t)cl * T + t) * P * P + (Y - ty * M) * P + (X - tx * M)]);
+        const int ty = t / tiles_x, tx = t - ty * tiles_x;
+        const float* g0 = gsm + (int64_t)idx * TS;
+        const float* gu = g0 - tiles_x * TS;       // (ty-1, tx)
+        const float* gl = g0 - TS;                 // (ty, tx-1)
+        const float* gul = gu - TS;                // (ty-1, tx-1)
+        const bool up = ty > 0, left = tx > 0;
+        const int ni = ty == tiles_y - 1 ? P : M, nj = tx == tiles_x - 1 ? P : M;
+        float* dst = dI + ((int64_t)n * C + c) * H * W;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (i >= ni) break;
+            const int y = ty * M + i - pad;
+            if ((unsigned)y >= (unsigned)H) continue;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                if (j >= nj) break;
+                const int x = tx * M + j - pad;
+                if ((unsigned)x >= (unsigned)W) continue;
+                float acc = 0.f;
+                if (i < O && j < O && up && left) acc = __fadd_rn(acc, gul[(i + M) * P + j + M]);
+                if (i < O && up) acc = __fadd_rn(acc, gu[(i + M) * P + j]);
+                if (j < O && left) acc = __fadd_rn(acc, gl[i * P + j + M]);
+                acc = __fadd_rn(acc, g0[i * P + j]);
+                dst[y * W + x] = acc;
             }
-        dI[((int64_t)n * C + c) * HW + pix] = acc;
+        }
     }
 }
 
