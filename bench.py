@@ -212,7 +212,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         go = Stream(cfg.seed + 1000 * rank, "shard/dO").normal(go.shape).astype(np.float32)
     layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
     dense = cfg.sparsity == 0.0
-    layer.set_weights(w_f, dense=dense)
+    layer.set_weights(w_f, dense=("tc" if args.dense_tc else True) if dense else False)
     cache = layer.new_cache(n)
     x = torch.from_numpy(img).to(dev)
     g_o = torch.from_numpy(go).to(dev)
@@ -310,23 +310,37 @@ def run_gpu(args, cfg, rank, world, local_rank):
             kernels[name]["alg_bytes"] = bytes_
             kernels[name]["GBps"] = bytes_ / (avg * 1e-3) / 1e9
     dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
-    dom_gbs = kernels[dom].get("GBps")
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(f"{cfg.name}:{cfg.sparsity}:{dom}")
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": (dom_gbs / pk["hbm_gbs"]) if dom_gbs else None,
-                "traffic": traffic, "peak_source": pk["source"],
-                "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
-                         "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
+    if dom.startswith("dense_"):
+        # tensor-pipe roofline: 3xTF32 issues 3 TF32 products per useful MAC; TF32 dense peak is
+        # taken as half the measured bf16 GEMM peak (MEASURED_PEAKS.json)
+        g = layer.geometry
+        useful = 2.0 * (g["p"] ** 2) * cfg.k * cfg.c * n * g["t"]
+        avg_s = prof[dom][0] / max(prof[dom][1], 1) * 1e-3
+        issued_tf = 3 * useful / avg_s / 1e12
+        peak_tf = pk["bf16_tflops"] / 2
+        roofline = {"bound": "tensor", "kernel": dom, "achieved": issued_tf, "peak": peak_tf,
+                    "unit": "TFLOP/s", "frac": issued_tf / peak_tf, "traffic": traffic,
+                    "peak_source": pk["source"] + " (bf16/2 for tf32)",
+                    "note": "issued TF32 FLOP/s of the 3xTF32 GEMM (useful = 1/3)"}
+    else:
+        dom_gbs = kernels[dom].get("GBps")
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": (dom_gbs / pk["hbm_gbs"]) if dom_gbs else None,
+                    "traffic": traffic, "peak_source": pk["source"],
+                    "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
+                             "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
         "config": {"workload": workload_name(cfg, "fwd+bwd"), "global_batch": n * world,
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
-                   "path": "dense" if dense else "csr", "l2_flush": "256 MB write between timed steps",
+                   "path": ("dense-tcgen05-3xtf32" if args.dense_tc else "dense-exact") if dense else "csr",
+                   "l2_flush": "256 MB write between timed steps",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
         "roofline": roofline,
@@ -356,6 +370,8 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dense-tc", action="store_true",
+                    help="at 0%% sparsity run the dense contractions on the tensor cores (3xTF32)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     cfg = CONFIGS[args.config]

@@ -97,10 +97,14 @@ WINO_API int wino_plan_info(const wino_plan* plan, wino_geometry* geom, int64_t*
 WINO_API int wino_set_weights_csr(wino_plan* plan, const uint64_t* const* row_ptr,
                          const uint64_t* const* col_idx, const float* const* values,
                          const uint64_t* nnz);
-/* Weights from a dense host W_F (K×C×p×q f64, layer.hpp:36): compress<float>
- * (sparse.cpp:9-36, keep |v| > zero_tol, or v != 0 when zero_tol == 0) then as
- * above.  If `dense` != 0 the plan instead keeps W_F dense and runs the dense
- * tcgen05 contraction; dW is then K×C×p×q. */
+/* Weights from a dense host W_F (K×C×p×q f64, layer.hpp:36).
+ *   dense = 0: compress<float> (sparse.cpp:9-36, keep |v| > zero_tol, or v != 0 when
+ *              zero_tol == 0) then as above; dW is nnz-compact.
+ *   dense = 1: every coordinate is a weight (zeros included, the dense layer's semantics);
+ *              exact reference-order kernels; dW is K×C×p×q.
+ *   dense = 2: as 1, but Z, dĨ_F and dW_F run as 3xTF32 tcgen05 GEMMs (tensor cores): ~1e-6
+ *              normwise error on O/dI, ~2e-5 on dW_F (fp32 TMEM accumulation over n·T);
+ *              layers whose C or K is not a multiple of 4 (TMA strides) use the dense=1 kernels. */
 WINO_API int wino_set_weights(wino_plan* plan, const double* w_f, double zero_tol, int dense);
 /* Structure of the device CSR (for parity checks): per-slice nnz[p·q]; if the other
  * pointers are non-null they receive row_ptr (p·q·(K+1), slice-local offsets),

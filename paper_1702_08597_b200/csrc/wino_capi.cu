@@ -12,7 +12,9 @@
 #include <vector>
 
 #include "../../include/wino_cuda.h"
+#include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
+#include "wino_tmap.h"
 
 namespace {
 
@@ -168,8 +170,15 @@ struct wino_plan {
     int64_t sddmm_max_nb = 0;
     double* d_partial = nullptr;
     size_t partial_cap = 0;
-    // dense plan (density 1): full CSR, dW scattered to K×C×p×q
+    // dense plan (density 1): full CSR (dW via the exact SDDMM, scattered to K×C×p×q) plus the
+    // tcgen05 operands: W and Wᵀ split into tf32 hi/lo, [36][K][C] and [36][C][K]
     float* d_wdense = nullptr;
+    float* d_wh = nullptr;
+    float* d_wl = nullptr;
+    float* d_wth = nullptr;
+    float* d_wtl = nullptr;
+    CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
+    bool tc_ready = false;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
     // scratch
@@ -204,8 +213,11 @@ namespace {
 void free_weights(wino_plan* p) {
     for (void* ptr : {(void*)p->d_rowptr, (void*)p->d_colidx, (void*)p->d_rowof, (void*)p->d_vals,
                       (void*)p->d_colptr, (void*)p->d_rowidx, (void*)p->d_perm, (void*)p->d_cv,
-                      (void*)p->d_cvT, (void*)p->d_wdense})
+                      (void*)p->d_cvT, (void*)p->d_wdense, (void*)p->d_wh, (void*)p->d_wl, (void*)p->d_wth,
+                      (void*)p->d_wtl})
         if (ptr) cudaFree(ptr);
+    p->d_wh = p->d_wl = p->d_wth = p->d_wtl = nullptr;
+    p->tc_ready = false;
     p->d_rowptr = p->d_colidx = p->d_rowof = p->d_colptr = p->d_rowidx = p->d_perm = nullptr;
     p->d_vals = p->d_wdense = nullptr;
     p->d_cv = p->d_cvT = nullptr;
@@ -480,6 +492,87 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
      : (p)->m == 2 ? FN<2, 4>(__VA_ARGS__)                              \
                    : FN<6, 8>(__VA_ARGS__))
 
+// Dense plan: (re)build the tcgen05 operands from the live values (full CSR order = W[s][k][c]).
+int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
+    const int64_t n = (int64_t)p->P2 * p->K * p->C;
+    if (p->C % 4 || p->K % 4) {  // TMA row strides must be multiples of 16 bytes: CSR kernels instead
+        p->tc_ready = false;
+        return WINO_OK;
+    }
+    if (!p->d_wh) {
+        CUDA_TRY(cudaMalloc(&p->d_wh, n * 4));
+        CUDA_TRY(cudaMalloc(&p->d_wl, n * 4));
+        CUDA_TRY(cudaMalloc(&p->d_wth, n * 4));
+        CUDA_TRY(cudaMalloc(&p->d_wtl, n * 4));
+        const int K = p->K, C = p->C;
+        bool ok = wino::make_map_3d(&p->map_wh, p->d_wh, C, K, p->P2, (uint64_t)C * 4, (uint64_t)K * C * 4, 32, 128) &&
+                  wino::make_map_3d(&p->map_wl, p->d_wl, C, K, p->P2, (uint64_t)C * 4, (uint64_t)K * C * 4, 32, 128) &&
+                  wino::make_map_3d(&p->map_wth, p->d_wth, K, C, p->P2, (uint64_t)K * 4, (uint64_t)K * C * 4, 32, 128) &&
+                  wino::make_map_3d(&p->map_wtl, p->d_wtl, K, C, p->P2, (uint64_t)K * 4, (uint64_t)K * C * 4, 32, 128);
+        if (!ok)
+            return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the weight operands (CUresult " +
+                                                std::to_string(wino::last_tmap_error()) + ")");
+    }
+    wino::split_tf32_kernel<<<grid_for(n, 256, p->sm_count), 256, 0, st>>>(p->d_vals, p->d_wh, p->d_wl, p->d_wth,
+                                                                           p->d_wtl, p->K, p->C, p->P2);
+    ++p->launches;
+    CUDA_TRY(cudaGetLastError());
+    p->tc_ready = true;
+    return WINO_OK;
+}
+
+template <bool A_SPLIT, bool B_MN>
+int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
+              const CUtensorMap& b, float* D, int M, int N, int Kd, int64_t ldd, int splits) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::SMEM_BYTES));
+        attr = true;
+    }
+    const int kb_total = (Kd + wino::tc::BK - 1) / wino::tc::BK;
+    const int kb_per = (kb_total + splits - 1) / splits;
+    const dim3 grid((unsigned)((N + wino::tc::BN - 1) / wino::tc::BN), (M + wino::tc::BM - 1) / wino::tc::BM,
+                    p->P2 * splits);
+    Launch L(p, st, kind);
+    wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN><<<grid, wino::tc::THREADS, wino::tc::SMEM_BYTES, st>>>(
+        ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per);
+    return L.done();
+}
+
+// D[s] = W-operand[s] · B[s] on the tensor cores; B = [P2][Kd][NTs] activations (MN-major).
+int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
+                   const float* B, float* D, int M, int Kd, int64_t NTs) {
+    CUtensorMap mb;
+    if (!wino::make_map_3d(&mb, B, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true))
+        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the activation operand (CUresult " +
+                                            std::to_string(wino::last_tmap_error()) + ")");
+    return launch_tc<false, true>(p, st, kind, ah, al, mb, D, M, (int)NTs, Kd, NTs, 1);
+}
+
+// dW_F = dZ·Ĩ_Fᵀ on the tensor cores, split over NT, partials summed in fp64 -> K×C×p×q.
+int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs) {
+    CUtensorMap ma, mb;
+    if (!wino::make_map_3d(&ma, DZ, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128) ||
+        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, 256))
+        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for dZ / Ĩ_F (CUresult " +
+                                            std::to_string(wino::last_tmap_error()) + ")");
+    const int tiles = ((p->C + wino::tc::BN - 1) / wino::tc::BN) * ((p->K + wino::tc::BM - 1) / wino::tc::BM) * p->P2;
+    const int kb_total = (int)((NTs + wino::tc::BK - 1) / wino::tc::BK);
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * p->sm_count + tiles - 1) / tiles, kb_total / 4));
+    if (const char* e = std::getenv("WINO_DW_SPLITS")) splits = std::max(1, std::atoi(e));
+    const size_t need = (size_t)splits * p->P2 * p->K * p->C;
+    float* part = nullptr;
+    int rc = ensure(&p->d_dwc, &p->dwc_cap, need);
+    if (rc) return rc;
+    part = p->d_dwc;
+    if ((rc = launch_tc<true, false>(p, st, K_DENSE_DW, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits))) return rc;
+    Launch L(p, st, K_DENSE_DW);
+    wino::tc::reduce_dw_kernel<<<grid_for((int64_t)p->P2 * p->K * p->C, 256, p->sm_count), 256, 0, st>>>(
+        part, dW, p->K, p->C, p->P2, splits);
+    return L.done();
+}
+
 int check_plan(const wino_plan* p) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
     if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan has no weights (call wino_set_weights*)");
@@ -719,6 +812,10 @@ int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense
         for (int s = 0; s < P2; ++s) p->slice_off[s] = (int64_t)s * K * C;
         int rc = upload_csr(p, rowptr, col, val);
         p->dense = true;
+        if (rc == WINO_OK && dense == 2) {
+            rc = refresh_tc_operands(p, nullptr);
+            if (rc == WINO_OK) CUDA_TRY(cudaDeviceSynchronize());
+        }
         return rc;
     }
     // compress<float> (sparse.cpp:9-36): slices (i,j) row-major, rows k, columns c ascending
@@ -789,7 +886,9 @@ int wino_values_updated(wino_plan* p, void* stream) {
     Launch L(p, st, K_MISC);
     wino::refresh_values_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_cv, p->d_cvT, p->d_vals,
                                                                                    p->d_perm, p->nnz);
-    return L.done();
+    rc = L.done();
+    if (rc == WINO_OK && p->dense && p->tc_ready) rc = refresh_tc_operands(p, st);
+    return rc;
 }
 
 int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
@@ -839,7 +938,10 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0)))
         return rc;
-    rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
+    if (p->dense && p->tc_ready)
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
+    else
+        rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1)))
         return rc;
@@ -864,15 +966,19 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask))) return rc;
-    float* dwc = grad_w;
-    if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
-    if (p->dense) dwc = p->d_dwc;
-    if ((rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs))) return rc;
-    if (p->dense) {  // [s][k][c] -> K×C×p×q
-        Launch L(p, st, K_MISC);
-        wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
-            dwc, grad_w, p->K, p->C, p->P2);
-        if ((rc = L.done())) return rc;
+    if (p->dense && p->tc_ready) {
+        if ((rc = launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs))) return rc;  // tensor cores (opt-in)
+    } else {
+        float* dwc = grad_w;
+        if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
+        if (p->dense) dwc = p->d_dwc;
+        if ((rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs))) return rc;
+        if (p->dense) {  // [s][k][c] -> K×C×p×q
+            Launch L(p, st, K_MISC);
+            wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
+                dwc, grad_w, p->K, p->C, p->P2);
+            if ((rc = L.done())) return rc;
+        }
     }
     c->has_grad_z = true;
     return WINO_OK;
@@ -890,7 +996,10 @@ int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, vo
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
-    rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
+    if (p->dense && p->tc_ready)
+        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
+    else
+        rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
     if (rc) return rc;
     return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
 }

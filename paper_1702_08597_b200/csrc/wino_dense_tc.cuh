@@ -1,0 +1,316 @@
+// Dense contraction on the 5th-generation tensor cores (tcgen05), used by the dense plan
+// (W_F without zeros, e.g. BASELINE configs[3] at 0% sparsity):
+//     D[s] (M×N) = A[s] (M×Kd) · B[s] (Kd×N)      for every Winograd slice s = (i,j)
+//   forward    : M=K, Kd=C, A = W_F(:,:,i,j) [K][C],   B = Ĩ_F [C][NT]   -> Z   (layer.cpp:61-71)
+//   bwd data   : M=C, Kd=K, A = W_F(:,:,i,j)ᵀ [C][K], B = dZ [K][NT]    -> dĨ_F (layer.cpp:145-155)
+//   bwd weights: M=K, N=C, Kd=NT, A = dZ [K][NT] (K-major, split on the fly), B = Ĩ_Fᵀ (Ĩ_F [C][NT]
+//                is K-major for this product), split over NT into fp32 partials that
+//                reduce_dw_kernel sums in fp64 in split order              -> dW_F (layer.cpp:118-128)
+//
+// Precision: 3xTF32 (D += Ah·Bh + Ah·Bl + Al·Bh, X = Xh + Xl with Xh = rna_tf32(X),
+// Xl = rna_tf32(X − Xh)): ~2^-22 relative error per product, fp32 accumulation in TMEM.  A is
+// split once on the host (weights); B is split per stage in shared memory by converter warps
+// (an elementwise op, so the TMA swizzle layout is preserved).
+//
+// Structure (one 128×256 output tile per CTA, 256 threads):
+//   warp 0     : TMA producer — A_hi, A_lo (K-major, 128B swizzle) and B (MN-major, 128B swizzle)
+//   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 4..7 : B hi/lo split per stage, then the epilogue (tcgen05.ld 32x32b.x32 -> global)
+// Two-stage ring: full (TMA tx) -> split (128 arrivals) -> MMA -> tcgen05.commit -> empty.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wino {
+namespace tc {
+
+constexpr int BM = 128;      // UMMA M (cta_group::1)
+constexpr int BN = 256;      // UMMA N
+constexpr int BK = 32;       // fp32 elements per stage along the reduction (one 128-byte row)
+constexpr int UK = 8;        // K per tcgen05.mma for kind::tf32 (32 bytes)
+constexpr int STAGES = 2;
+constexpr int THREADS = 256;
+constexpr int A_TILE = BM * BK * 4;       // 16 KB
+constexpr int B_TILE = BK * BN * 4;       // 32 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;   // A_hi, A_lo, B(hi in place), B_lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// Shared-memory matrix descriptor (SM100 UMMA): start>>4 [0,14), LBO>>4 [16,30), SBO>>4
+// [32,46), version=1 [46,48), layout type [61,64): 2 = SWIZZLE_128B (K-major tf32),
+// 1 = SWIZZLE_128B_BASE32B (the layout MN-major 32-bit operands require; produced by TMA's
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+constexpr uint32_t kLayoutSW128 = 2;
+constexpr uint32_t kLayoutSW128Base32 = 1;
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B tf32 (2), A K-major (bit 15 = 0),
+// B major (bit 16: 1 = MN-major, 0 = K-major), N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t make_idesc(bool b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void split_tile(uint8_t* hi_buf, uint8_t* lo_buf, int bytes, int t, int nthreads) {
+    const uint32_t h0 = smem_u32(hi_buf), l0 = smem_u32(lo_buf);
+#pragma unroll 4
+    for (int i = t * 16; i < bytes; i += nthreads * 16) {
+        float4 x;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(h0 + i));
+        float4 h, l;
+#ifdef WINO_TC_NOSPLIT
+        h = x;
+        l = make_float4(0.f, 0.f, 0.f, 0.f);
+#else
+        h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+        h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+        h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+        h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+#endif
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(h0 + i), "f"(h.x), "f"(h.y), "f"(h.z), "f"(h.w));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(l0 + i), "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w));
+    }
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
+// grid = (ceil(N/BN), ceil(M/BM), slices·splits); blockIdx.z = s·splits + q.  The CTA reduces
+// k-blocks [q·kb_per, (q+1)·kb_per) and writes D + (q·slices + s)·M·ldd (rows < M, cols < N).
+// A_SPLIT: A arrives raw through mapAh and is split in shared memory (mapAl unused); otherwise
+// mapAh/mapAl hold the pre-split weights.  B_MN: B is MN-major [Kd][N] (else K-major [N][Kd]).
+template <bool A_SPLIT, bool B_MN>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
+                   const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N, int Kd,
+                   int64_t ldd, int slices, int splits, int kb_per) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;                 // [STAGES] TMA landed
+    uint64_t* split = bars + STAGES;       // [STAGES] hi/lo ready (128 arrivals)
+    uint64_t* empty = bars + 2 * STAGES;   // [STAGES] MMAs done reading the stage
+    uint64_t* tmem_full = bars + 3 * STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+    const int s = blockIdx.z / splits, q = blockIdx.z - s * splits;
+    const int kb_total = (Kd + BK - 1) / BK;
+    const int kb0 = q * kb_per;
+    const int kblocks = max(0, min(kb_total, kb0 + kb_per) - kb0);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split[i], 128);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int st = kb % STAGES;
+                if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
+                uint8_t* base = stage_ptr(st);
+                const int kk = (kb0 + kb) * BK;
+                mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
+                tma_load_3d(base, &mapAh, &full[st], kk, m0, s);
+                if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, m0, s);
+                if (B_MN) {
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j)  // 8 MN atoms of 32 columns × BK rows
+                        tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], n0 + 32 * j, kk, s);
+                } else {
+                    tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, n0, s);  // BN rows × 128 B
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(B_MN);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int st = kb % STAGES;
+                mbar_wait(&split[st], (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a_hi = smem_u32(stage_ptr(st));
+                const uint32_t a_lo = a_hi + A_TILE;
+                const uint32_t b_hi = a_hi + 2 * A_TILE;
+                const uint32_t b_lo = b_hi + B_TILE;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); +32 B per
+                    // K step inside the 128-byte swizzle row.
+                    const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
+                    const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
+                    uint64_t dbh, dbl;
+                    if (B_MN) {
+                        // MN-major SW128 with 32-byte atoms: 32-column (128 B) atoms BK*128 B apart
+                        // (LBO), 4-row K groups 512 B apart (SBO); +8 rows = 1024 B per K step.
+                        dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                        dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                    } else {
+                        dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
+                        dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
+                    }
+                    const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                    mma_tf32(tmem, dah, dbh, idesc, acc0);
+                    mma_tf32(tmem, dah, dbl, idesc, 1u);
+                    mma_tf32(tmem, dal, dbh, idesc, 1u);
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(tmem_full);
+        }
+    } else if (warp >= 4) {
+        const int t = threadIdx.x - 128;  // 0..127
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int st = kb % STAGES;
+            mbar_wait(&full[st], (kb / STAGES) & 1);
+            uint8_t* base = stage_ptr(st);
+            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t, 128);
+            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t, 128);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+            mbar_arrive(&split[st]);
+        }
+        // epilogue: TMEM lane = output row (warp quarter), columns = output columns
+        const int qd = warp & 3;
+        const int row = m0 + qd * 32 + lane;
+        float* drow = D + (((int64_t)q * slices + s) * M + row) * ldd;
+        if (kblocks == 0) {
+            if (row < M)
+                for (int c = 0; c < BN; ++c)
+                    if (n0 + c < N) drow[n0 + c] = 0.f;
+        } else {
+            mbar_wait(tmem_full, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int col = n0 + c;
+                if (row < M) {
+                    if (col + 32 <= N && (ldd & 3) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(drow + col + j) =
+                                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col + j < N) drow[col + j] = __uint_as_float(v[j]);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+}
+
+// dW_F from the split-K partials [splits][P2][K][C]: fp64 sum in split order, written in the
+// W_F layout K×C×p×q (layer.hpp:36).
+__global__ void reduce_dw_kernel(const float* __restrict__ part, float* __restrict__ dw, int K, int C, int P2,
+                                 int splits) {
+    const int64_t total = (int64_t)P2 * K * C;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int q = 0; q < splits; ++q) a += (double)part[(int64_t)q * total + i];
+        const int64_t s = i / ((int64_t)K * C), kc = i - s * K * C;
+        dw[kc * P2 + s] = (float)a;
+    }
+}
+
+}  // namespace tc
+}  // namespace wino

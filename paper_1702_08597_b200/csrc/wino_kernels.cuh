@@ -639,6 +639,27 @@ __global__ void refresh_values_kernel(int2* __restrict__ cv, int2* __restrict__ 
     }
 }
 
+// Dense plan: split W[s][k][c] into tf32 hi/lo (rna), both as W and as Wᵀ[s][c][k].
+__global__ void split_tf32_kernel(const float* __restrict__ w, float* __restrict__ wh, float* __restrict__ wl,
+                                  float* __restrict__ wth, float* __restrict__ wtl, int K, int C, int P2) {
+    const int64_t total = (int64_t)P2 * K * C;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = w[i];
+        uint32_t h, l;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+        const float r = x - __uint_as_float(h);
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+        wh[i] = __uint_as_float(h);
+        wl[i] = __uint_as_float(l);
+        const int64_t s = i / ((int64_t)K * C), kc = i - s * K * C;
+        const int k = (int)(kc / C), c = (int)(kc - (int64_t)k * C);
+        const int64_t t = (s * C + c) * K + k;
+        wth[t] = __uint_as_float(h);
+        wtl[t] = __uint_as_float(l);
+    }
+}
+
 // dense-plan dW: slice-major compact [s][k][c] -> W_F layout K×C×p×q
 __global__ void slice_major_to_kcpq_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                            int K, int C, int P2) {

@@ -139,8 +139,9 @@ class WinogradLayer:
         self.ho, self.wo = self.geometry["h_o"], self.geometry["w_o"]
 
     # -- weights ------------------------------------------------------------------
-    def set_weights(self, w_f, zero_tol: float = 0.0, dense: bool | None = None):
-        """W_F (K×C×p×q).  dense=None picks the dense path when no entry is dropped."""
+    def set_weights(self, w_f, zero_tol: float = 0.0, dense: bool | str | None = None):
+        """W_F (K×C×p×q).  dense=None picks the dense layer when no entry is dropped; dense='tc'
+        runs the dense contractions on the tensor cores (3xTF32 tcgen05, approximate)."""
         w_f = np.ascontiguousarray(w_f, dtype=np.float64)
         if w_f.shape != (self.k, self.c, self.p, self.p):
             raise _lib.ShapeError(f"weights {w_f.shape} do not match layer "
@@ -148,7 +149,8 @@ class WinogradLayer:
         if dense is None:
             kept = (np.abs(w_f) > zero_tol) | ((zero_tol == 0.0) & (w_f != 0.0))
             dense = bool(kept.all())
-        check(lib().wino_set_weights(self._h, w_f.ctypes.data_as(_lib._pd), zero_tol, int(dense)))
+        mode = 2 if dense == "tc" else int(bool(dense))
+        check(lib().wino_set_weights(self._h, w_f.ctypes.data_as(_lib._pd), zero_tol, mode))
 
     def set_weights_csr(self, csr: PointwiseCsr):
         n = self.p * self.p
