@@ -361,6 +361,116 @@ def run_gpu(args, cfg, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_gpu_stack(args, cfg, rank, world, local_rank):
+    """BASELINE configs[4]: data-parallel training step of a 4-layer stack (C=K=256, H=W=28,
+    ReLU between layers, 90% fixed masks), global batch 512 sharded by rank, one bucketed
+    NCCL all-reduce of the nnz-compact dW_F, masked SGD.  Effective FLOPs: 4 forward + 4
+    backward-weights + 3 backward-input passes (no dI for layer 0, train.cpp:201)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_08597_b200.dist import shard
+    from paper_1702_08597_b200.stack import WinogradStack
+    from paper_1702_08597_b200.synth import LayerConfig, Stream
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n_global = CONFIGS["c4"].n
+    _, n = shard(n_global, rank, world)
+    layers = 4
+    weights = [make_inputs(LayerConfig("c4", 1, cfg.c, cfg.k, cfg.h, cfg.sparsity, seed=cfg.seed), layer=l)[1]
+               for l in range(layers)]
+    img = Stream(cfg.seed + 1000 * rank, "c4/I").normal((n, cfg.c, cfg.h, cfg.w)).astype(np.float32)
+    go = Stream(cfg.seed + 1000 * rank, "c4/dO").normal((n, cfg.k, cfg.h, cfg.w)).astype(np.float32)
+    st = WinogradStack(weights, cfg.c, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank, n_max=n)
+    x = torch.from_numpy(img).to(dev)
+    g_o = torch.from_numpy(go).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+
+    def step():
+        st.step(x, g_o, lr=1e-4, n_global=n_global)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for lay in st.layers:
+        lay.profile(True)
+        lay.reset_launch_count()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = st.launch_count()
+    prof = {}
+    for lay in st.layers:
+        for k, (t, c) in lay.profile_read().items():
+            a0 = prof.get(k, (0.0, 0))
+            prof[k] = (a0[0] + t, a0[1] + c)
+        lay.profile(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    passes = 3 * layers - 1
+    value = passes * flops_per_image(cfg) * n_global / (ms_max * 1e-3) / 1e9
+    # end to end: host shard in, reduced gradient bucket out
+    h_img = torch.from_numpy(img).pin_memory()
+    h_go = torch.from_numpy(go).pin_memory()
+    h_b = torch.empty(st.bucket.flat.shape, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        x.copy_(h_img, non_blocking=True)
+        g_o.copy_(h_go, non_blocking=True)
+        step()
+        h_b.copy_(st.bucket.flat, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev2:
+        flush.zero_()
+        a.record()
+        e2e_step()
+        b.record()
+    torch.cuda.synchronize()
+    t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2) / args.steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    if rank != 0:
+        return
+    tot = sum(v[0] for v in prof.values())
+    kernels = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1], "share": v[0] / tot}
+               for k, v in prof.items()}
+    line = {
+        "metric": METRIC.replace("layer", "4-layer training step"), "value": value, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded splitmix64 normals)",
+        "config": {"workload": f"c4: 4-layer Winograd stack C=K=256 H=W=28 F(4x4,3x3) pad 1, ReLU, "
+                               f"90% fixed masks, global batch {n_global} sharded over {world} GPU(s), "
+                               "masked SGD, one NCCL all-reduce of nnz-compact dW_F per step",
+                   "global_batch": n_global, "n_per_gpu": n, "parallelism": f"dp{world}",
+                   "l2_flush": "256 MB write between timed steps"},
+        "kernels": kernels,
+        "e2e": {"value": passes * flops_per_image(cfg) * n_global / (float(t2.item()) * 1e-3) / 1e9,
+                "unit": "GFLOP/s", "h2d_bytes_per_step": (h_img.numel() + h_go.numel()) * 4,
+                "d2h_bytes_per_step": h_b.numel() * 4, "ms_per_step": float(t2.item())},
+        "gpu_launches": launches, "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,11 +487,6 @@ def main():
     cfg = CONFIGS[args.config]
     if args.sparsity is not None:
         cfg = with_sparsity(cfg, args.sparsity)
-    if args.config == "c4":  # per-GPU shard of the global batch 512
-        from paper_1702_08597_b200.synth import LayerConfig
-
-        cfg = LayerConfig(cfg.name, max(1, cfg.n // max(1, args.gpus)), cfg.c, cfg.k, cfg.h, cfg.sparsity,
-                          cfg.pad, cfg.m, cfg.r, cfg.backward, cfg.seed)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -395,7 +500,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_gpu(args, cfg, rank, world, local_rank)
+        if args.config == "c4":
+            run_gpu_stack(args, cfg, rank, world, local_rank)
+        else:
+            run_gpu(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

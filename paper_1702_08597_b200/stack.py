@@ -1,0 +1,72 @@
+"""Batched training step of a stack of Winograd layers (BASELINE configs[4]).
+
+The reference trainer runs one sample at a time (train.cpp:167) through run_forward
+(conv -> ReLU per layer, train.cpp:66-87) and the backward chain (relu-mask multiply,
+backward_weights, Σ_n·(1/B), backward_input for l > 0; train.cpp:189-211), then the masked
+SGD update of train_step (train.cpp:281-290).  Here one call per layer and minibatch does the
+same on the device: ReLU is fused into the output-transform epilogue, the mask into the dZ
+kernel, dW_F of all layers lands in one GradBucket that is all-reduced once (data parallel),
+and the update runs on the live CSR values (masked coordinates do not exist in the CSR, so
+they stay exactly zero — the fine-tune invariant check_masks enforces, train.cpp:340-347).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .dist import GradBucket
+from .layer import WinogradLayer
+
+
+class WinogradStack:
+    def __init__(self, weights, c, h, w, pad=1, m=4, device=0, n_max=1):
+        """weights: list of K×C×p×p W_F arrays (exact zeros = pruned)."""
+        import torch
+
+        self.device = device
+        self.layers = []
+        self.caches = []
+        cin = c
+        for w_f in weights:
+            w_f = np.asarray(w_f)
+            lay = WinogradLayer(cin, w_f.shape[0], h, w, pad=pad, m=m, device=device)
+            lay.set_weights(w_f, dense=False)
+            self.layers.append(lay)
+            self.caches.append(lay.new_cache(n_max))
+            cin = w_f.shape[0]
+            h, w = lay.ho, lay.wo
+        self.bucket = GradBucket.allocate([lay.nnz for lay in self.layers], device=f"cuda:{device}")
+        self.n_max = n_max
+        self.outs = [None] * len(self.layers)
+        self._torch = torch
+
+    def forward(self, x):
+        """run_forward (train.cpp:66-87): conv -> ReLU for every layer; returns the last output."""
+        cur = x
+        for i, (lay, cache) in enumerate(zip(self.layers, self.caches)):
+            if self.outs[i] is None or self.outs[i].shape[0] != cur.shape[0]:
+                self.outs[i] = self._torch.empty((cur.shape[0], lay.k, lay.ho, lay.wo), device=cur.device)
+            cur = lay.forward(cur, cache, relu=True, out=self.outs[i])
+        return cur
+
+    def backward(self, grad_out):
+        """The backward chain of minibatch_grad (train.cpp:189-211) for the whole minibatch:
+        fills the gradient bucket with Σ_n dW_F per layer; no dI for layer 0 (train.cpp:201)."""
+        g = grad_out
+        for i in range(len(self.layers) - 1, -1, -1):
+            lay, cache = self.layers[i], self.caches[i]
+            lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.bucket.views[i])
+            if i > 0:
+                g = lay.backward_input(cache)
+        return self.bucket
+
+    def step(self, x, grad_out, lr, n_global, l2=0.0, group=None):
+        """One data-parallel training step: forward, backward, ONE all-reduce of the bucket,
+        masked SGD with the 1/B scaling of train.cpp:166,200."""
+        self.forward(x)
+        self.backward(grad_out)
+        self.bucket.allreduce(group)
+        for lay, g in zip(self.layers, self.bucket.views):
+            lay.sgd_step(g, lr=lr, scale=1.0 / float(n_global), l2=l2)
+
+    def launch_count(self):
+        return sum(lay.launch_count() for lay in self.layers)

@@ -374,3 +374,37 @@ def test_api_reference_surface():
         np.testing.assert_allclose(out[n], wo.forward_f64(batch[n], w_f, 2)[0], rtol=1e-4, atol=1e-4)
     with pytest.raises(wb.CapabilityError):
         wb.sparse_conv(batch, w_f, precision="f64")
+
+
+def test_stack_training_step_matches_mirror():
+    """Two-layer stack (configs[0] shapes): forward with fused ReLU, relu-masked backward
+    chain, one bucketed reduction, masked SGD — against the f32 mirror chained by hand."""
+    from paper_1702_08597_b200.stack import WinogradStack
+
+    cfg = CONFIGS["c0"]
+    img, w1, go = make_inputs(cfg, n=3)
+    w2 = w1[:, :, ::-1, ::-1].copy()
+    st = WinogradStack([w1, w2], cfg.c, cfg.h, cfg.w, pad=1, m=4, n_max=3)
+    x = dev(img)
+    st.forward(x)
+    bucket = st.backward(dev(go))
+    torch.cuda.synchronize()
+    got = bucket.flat.cpu().numpy().astype(np.float64)
+    # mirror: O1 = relu(L1(img)); O2 = relu(L2(O1)); dO2 = go·[O2>0]; dO1 = dI2·[O1>0]
+    c1, c2 = wo.compress(w1), wo.compress(w2)
+    o1 = np.maximum(wo.layer_f32(img, c1, None, m=4, pad=1)["o"], 0)
+    r2 = wo.layer_f32(o1, c2, go * (wo.layer_f32(o1, c2, None, m=4, pad=1)["o"] > 0), m=4, pad=1)
+    o2 = np.maximum(r2["o"], 0)
+    assert np.array_equal(st.outs[1].cpu().numpy(), o2)
+    r1 = wo.layer_f32(img, c1, r2["di"] * (o1 > 0), m=4, pad=1)
+    want = np.concatenate([np.concatenate(r1["dw"]), np.concatenate(r2["dw"])])
+    np.testing.assert_allclose(got, want, rtol=2e-6, atol=1e-5)
+    # masked SGD: v -= lr·g/B on surviving coordinates only
+    vals0 = [np.concatenate(wb.compress(w).values).astype(np.float64) for w in (w1, w2)]
+    for lay, g in zip(st.layers, st.bucket.views):
+        lay.sgd_step(g, lr=0.05, scale=1.0 / 3)
+    torch.cuda.synchronize()
+    for lay, v0, g in zip(st.layers, vals0, st.bucket.views):
+        v1 = np.concatenate(lay.get_csr().values)
+        np.testing.assert_allclose(v1, v0 - 0.05 * g.cpu().numpy() / 3, rtol=1e-5, atol=1e-7)
+        assert lay.nnz == len(v0)  # the mask is fixed: pruned coordinates never reappear
