@@ -174,6 +174,20 @@ def run_reference(args, cfg, rank):
 # -------------------------------------------------------------------------------------
 # GPU arm
 # -------------------------------------------------------------------------------------
+def capture(step, args):
+    """CUDA-graph the step (paper_1702_08597_b200.graph.GraphedStep) unless --no-graph; falls
+    back to eager launches if capture fails (reported in the JSON line)."""
+    if args.no_graph:
+        return step, "eager"
+    from paper_1702_08597_b200.graph import GraphedStep
+
+    try:
+        g = GraphedStep(step)
+        return g.replay, "cuda-graph (one graph launch per step)"
+    except Exception as e:  # noqa: BLE001
+        return step, f"eager (graph capture failed: {type(e).__name__}: {e})"
+
+
 def kernel_bytes(cfg, layer, n):
     """Algorithmic HBM bytes per launch of each kernel."""
     g = layer.geometry
@@ -231,29 +245,38 @@ def run_gpu(args, cfg, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    layer.reset_launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step_launches = layer.launch_count()
+    run, graph_note = capture(step, args)
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     sampler = ClockSampler(local_rank)
     sampler.start()
-    layer.profile(True)
-    layer.reset_launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     for a, b in ev:
         flush.zero_()
         a.record()
-        step()
+        run()
         b.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = layer.launch_count()
+    clocks = sampler.stop()
+    launches = per_step_launches * args.steps
+    # per-kernel times for the roofline: eager steps with CUDA events around every launch
+    layer.profile(True)
+    for _ in range(3):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
     prof = layer.profile_read()
     layer.profile(False)
-    clocks = sampler.stop()
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -272,7 +295,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     def e2e_step():
         x.copy_(h_img, non_blocking=True)
         g_o.copy_(h_go, non_blocking=True)
-        step()
+        run()
         h_out.copy_(out, non_blocking=True)
         h_dw.copy_(dw, non_blocking=True)
         h_di.copy_(di, non_blocking=True)
@@ -348,6 +371,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item())},
         "gpu_launches": launches,
+        "launch_mode": graph_note,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -393,24 +417,32 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    for lay in st.layers:
+        lay.reset_launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step_launches = st.launch_count()
+    run, graph_note = capture(step, args)
     if world > 1:
         dist.barrier()
-    for lay in st.layers:
-        lay.profile(True)
-        lay.reset_launch_count()
     sampler = ClockSampler(local_rank)
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for a, b in ev:
         flush.zero_()
         a.record()
-        step()
+        run()
         b.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    launches = st.launch_count()
+    launches = per_step_launches * args.steps
+    for lay in st.layers:
+        lay.profile(True)
+    flush.zero_()
+    step()
+    torch.cuda.synchronize()
     prof = {}
     for lay in st.layers:
         for k, (t, c) in lay.profile_read().items():
@@ -432,7 +464,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     def e2e_step():
         x.copy_(h_img, non_blocking=True)
         g_o.copy_(h_go, non_blocking=True)
-        step()
+        run()
         h_b.copy_(st.bucket.flat, non_blocking=True)
 
     e2e_step()
@@ -466,7 +498,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
         "e2e": {"value": passes * flops_per_image(cfg) * n_global / (float(t2.item()) * 1e-3) / 1e9,
                 "unit": "GFLOP/s", "h2d_bytes_per_step": (h_img.numel() + h_go.numel()) * 4,
                 "d2h_bytes_per_step": h_b.numel() * 4, "ms_per_step": float(t2.item())},
-        "gpu_launches": launches, "clocks": clocks,
+        "gpu_launches": launches, "launch_mode": graph_note, "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
 
@@ -480,6 +512,7 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--dense-tc", action="store_true",
                     help="at 0%% sparsity run the dense contractions on the tensor cores (3xTF32)")
     args = ap.parse_args()

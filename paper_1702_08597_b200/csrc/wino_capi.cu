@@ -252,6 +252,25 @@ struct Launch {
     }
 };
 
+// cudaFuncSetAttribute once per kernel and size (keeps launches capturable in CUDA graphs and
+// off the per-launch host path)
+template <typename K>
+void set_smem_attr(K kernel, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    const void* key = reinterpret_cast<const void*>(kernel);
+    for (auto& d : done)
+        if (d.first == key) {
+            if (d.second >= bytes) return;
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            d.second = bytes;
+            return;
+        }
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.emplace_back(key, bytes);
+}
+
 int grid_for(int64_t work, int threads, int sm_count) {
     int64_t b = (work + threads - 1) / threads;
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sm_count * 16));
@@ -309,7 +328,7 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
     groups = (nrows + rpb - 1) / rpb;
     if ((int)smem > p->max_smem)
         return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
-    cudaFuncSetAttribute(wino::spmm_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_attr(wino::spmm_kernel<R>, (int)smem);
     Launch L(p, st, kind);
     wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), 512, smem, st>>>(rowptr, cv, X, Y, nrows, ncols,
                                                                         (int)NTs, rpb);
@@ -326,7 +345,8 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
     }
 }
 
-constexpr int kSddmmWarps = 16;
+constexpr int kSddmmBatch = 16;    // nonzeros per warp batch
+constexpr int kSddmmWarps = 24;    // 768 threads (≤ 85 registers: no spills at R=4)
 
 int64_t max_group_nnz(const wino_plan* p, int rows) {
     int64_t nb = 0;
@@ -356,12 +376,12 @@ void plan_sddmm(wino_plan* p) {
         for (int lim : {first, 8, 16}) {
             for (int rows = (int)std::min<int64_t>(round_up(K, 8), cap_rows / 8 * 8); rows >= 8; rows -= 8) {
                 const int64_t nb = max_group_nnz(p, rows);
-                if (nb <= (int64_t)kSddmmWarps * 32 * lim) {
+                if (nb <= (int64_t)kSddmmWarps * kSddmmBatch * lim) {
                     p->sddmm_r = o.r;
                     p->sddmm_stages = o.stages;
                     p->sddmm_rows = rows;
                     p->sddmm_max_nb = nb;
-                    const int64_t per_warp = (nb + kSddmmWarps * 32 - 1) / (kSddmmWarps * 32);
+                    const int64_t per_warp = (nb + kSddmmWarps * kSddmmBatch - 1) / (kSddmmWarps * kSddmmBatch);
                     p->sddmm_maxb = per_warp <= 4 ? 4 : per_warp <= 8 ? 8 : 16;
                     return;
                 }
@@ -374,9 +394,10 @@ void plan_sddmm(wino_plan* p) {
 template <int R, int MAXB, int STAGES>
 void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
                     const float* V, float* dW, double* partial, int NT, int NTs, int tps) {
-    cudaFuncSetAttribute(wino::sddmm_kernel<R, MAXB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    wino::sddmm_kernel<R, MAXB, STAGES><<<grid, kSddmmWarps * 32, smem, st>>>(
+    constexpr int TH = kSddmmWarps * 32;
+    static_assert(TH <= 1024, "block too large");
+    set_smem_attr(wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH>, (int)smem);
+    wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH><<<grid, TH, smem, st>>>(
         p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NT, NTs, p->sddmm_rows,
         tps);
 }
@@ -475,8 +496,7 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
         int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c,
                                                                 (256 + T - 1) / T}));
         const size_t smem = (size_t)cg * per_c;
-        cudaFuncSetAttribute(wino::input_grad_kernel<M, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)std::max<size_t>(smem, 48 * 1024));
+        set_smem_attr(wino::input_grad_kernel<M, P>, (int)std::max<size_t>(smem, 48 * 1024));
         wino::input_grad_kernel<M, P><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
             DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg);
     } else {

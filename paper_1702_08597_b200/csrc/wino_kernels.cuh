@@ -488,8 +488,24 @@ __device__ __forceinline__ void transpose_reduce32(double (&v)[32], int lane) {
     }
 }
 
-template <int R, int MAXB, int STAGES>
-__global__ void __launch_bounds__(512)
+// 16 values per lane -> lane l (and l^16) ends with the total of value (l & 15): 15 exchange
+// steps over lane bits 3..0, then one across bit 4.
+__device__ __forceinline__ void transpose_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = hi ? v[i] : v[i + o];
+            const double keep = hi ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(kFull, send, o);
+        }
+    }
+    v[0] += __shfl_xor_sync(kFull, v[0], 16);
+}
+
+template <int R, int MAXB, int STAGES, int BATCH, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
              const int* __restrict__ rowof, const float* __restrict__ DZ,
              const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
@@ -516,7 +532,7 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
     double acc[MAXB];
 #pragma unroll
     for (int i = 0; i < MAXB; ++i) {
-        const int b = (warp + i * nw) * 32 + lane;
+        const int b = (warp + i * nw) * BATCH + (lane & (BATCH - 1));
         pk[i] = 0;
         if (b < nb) pk[i] = (((__ldg(rowof + e0 + b) - r0 + C) * 32) << 16) | (__ldg(colidx + e0 + b) * 32);
         acc[i] = 0.0;
@@ -546,12 +562,12 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
         const float* base = st0 + buf * stage_floats + lane * R;
 #pragma unroll
         for (int i = 0; i < MAXB; ++i) {
-            if ((warp + i * nw) * 32 >= nb) break;  // warp-uniform
-            double part[32];
+            if ((warp + i * nw) * BATCH >= nb) break;  // warp-uniform
+            double part[BATCH];
             double zd[R];
             int rprev = -1;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < BATCH; ++j) {
                 const int q = __shfl_sync(kFull, pk[i], j);
                 const int ro = q >> 16;
                 if (ro != rprev) {
@@ -568,7 +584,10 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                 for (int qq = 1; qq < R; ++qq) pr = fma(zd[qq], (double)x[qq], pr);
                 part[j] = pr;
             }
-            transpose_reduce32(part, lane);
+            if constexpr (BATCH == 32)
+                transpose_reduce32(part, lane);
+            else
+                transpose_reduce16(part, lane);
             acc[i] += part[0];
         }
         __syncthreads();
@@ -577,8 +596,8 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
     // single split -> dW (fp32); several -> fp64 partials [split][nnz_total], summed in order
 #pragma unroll
     for (int i = 0; i < MAXB; ++i) {
-        const int b = (warp + i * nw) * 32 + lane;
-        if (b < nb) {
+        const int b = (warp + i * nw) * BATCH + lane;
+        if (lane < BATCH && b < nb) {
             if (partial == nullptr)
                 dW[e0 + b] = (float)acc[i];
             else
