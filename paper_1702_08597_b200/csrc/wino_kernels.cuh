@@ -452,6 +452,19 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
 #pragma unroll
                 for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv[u].y), x[u][q]);
         }
+        if (e + 4 <= ee) {
+            int2 cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cv[u] = cvb[e + u];
+            float x[4][R];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) lds_vec<R>(reinterpret_cast<const float*>(xl + cv[u].x * (TW * 4)), x[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv[u].y), x[u][q]);
+            e += 4;
+        }
         for (; e < ee; ++e) {
             const int2 cv = cvb[e];
             float x[R];
