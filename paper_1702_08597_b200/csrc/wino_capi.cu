@@ -330,7 +330,8 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
         return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
     set_smem_attr(wino::spmm_kernel<R>, (int)smem);
     Launch L(p, st, kind);
-    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), 512, smem, st>>>(rowptr, cv, X, Y, nrows, ncols,
+    const int threads = std::getenv("WINO_SPMM_THREADS") ? std::atoi(std::getenv("WINO_SPMM_THREADS")) : 1024;
+    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols,
                                                                         (int)NTs, rpb);
     return L.done();
 }

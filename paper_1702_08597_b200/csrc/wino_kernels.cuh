@@ -402,7 +402,7 @@ __device__ __forceinline__ int2 ld_uniform_int2(const int2* p) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs,
             int rows_per_block) {
@@ -440,10 +440,22 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
         for (int q = 0; q < R; ++q) acc[q] = 0.f;
         int e = __ldg(rp + r);
         const int ee = __ldg(rp + r + 1);
+        if ((e & 1) && e < ee) {  // peel to a 16-byte-aligned pair boundary
+            const int2 cv = cvb[e];
+            float x[R];
+            lds_vec<R>(reinterpret_cast<const float*>(xl + cv.x * (TW * 4)), x);
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv.y), x[q]);
+            ++e;
+        }
         for (; e + U <= ee; e += U) {
             int2 cv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) cv[u] = cvb[e + u];
+            for (int u = 0; u < U; u += 2) {  // one broadcast LDS.128 per two nonzeros
+                const int4 two = *reinterpret_cast<const int4*>(cvb + e + u);
+                cv[u] = make_int2(two.x, two.y);
+                cv[u + 1] = make_int2(two.z, two.w);
+            }
             float x[U][R];
 #pragma unroll
             for (int u = 0; u < U; ++u) lds_vec<R>(reinterpret_cast<const float*>(xl + cv[u].x * (TW * 4)), x[u]);
@@ -455,7 +467,11 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
         if (e + 4 <= ee) {
             int2 cv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) cv[u] = cvb[e + u];
+            for (int u = 0; u < 4; u += 2) {
+                const int4 two = *reinterpret_cast<const int4*>(cvb + e + u);
+                cv[u] = make_int2(two.x, two.y);
+                cv[u + 1] = make_int2(two.z, two.w);
+            }
             float x[4][R];
 #pragma unroll
             for (int u = 0; u < 4; ++u) lds_vec<R>(reinterpret_cast<const float*>(xl + cv[u].x * (TW * 4)), x[u]);
