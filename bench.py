@@ -226,7 +226,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         go = Stream(cfg.seed + 1000 * rank, "shard/dO").normal(go.shape).astype(np.float32)
     layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
     dense = cfg.sparsity == 0.0
-    layer.set_weights(w_f, dense=("tc" if args.dense_tc else True) if dense else False)
+    layer.set_weights(w_f, dense=(args.dense or "tc") if dense else False)
     cache = layer.new_cache(n)
     x = torch.from_numpy(img).to(dev)
     g_o = torch.from_numpy(go).to(dev)
@@ -362,7 +362,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
         "config": {"workload": workload_name(cfg, "fwd+bwd"), "global_batch": n * world,
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
-                   "path": ("dense-tcgen05-3xtf32" if args.dense_tc else "dense-exact") if dense else "csr",
+                   "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
+                             "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else "csr",
                    "l2_flush": "256 MB write between timed steps",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
@@ -513,8 +514,9 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
-    ap.add_argument("--dense-tc", action="store_true",
-                    help="at 0%% sparsity run the dense contractions on the tensor cores (3xTF32)")
+    ap.add_argument("--dense", default=None, choices=["tc", "tc-fast", "exact"],
+                    help="dense path at 0%% sparsity: 'tc' (default: 3xTF32 tcgen05, per-k-block fp64 "
+                         "folding), 'tc-fast' (one TMEM chain), 'exact' (reference-order SIMT)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     cfg = CONFIGS[args.config]

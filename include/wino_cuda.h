@@ -102,9 +102,12 @@ WINO_API int wino_set_weights_csr(wino_plan* plan, const uint64_t* const* row_pt
  *              zero_tol == 0) then as above; dW is nnz-compact.
  *   dense = 1: every coordinate is a weight (zeros included, the dense layer's semantics);
  *              exact reference-order kernels; dW is K×C×p×q.
- *   dense = 2: as 1, but Z, dĨ_F and dW_F run as 3xTF32 tcgen05 GEMMs (tensor cores): ~1e-6
- *              normwise error on O/dI, ~2e-5 on dW_F (fp32 TMEM accumulation over n·T);
- *              layers whose C or K is not a multiple of 4 (TMA strides) use the dense=1 kernels. */
+ *   dense = 2: as 1, but Z, dĨ_F and dW_F run as 3xTF32 tcgen05 GEMMs on the tensor cores with
+ *              every 32-wide k-block accumulated in a fresh TMEM accumulator and folded into
+ *              fp64 by the epilogue (error ~2e-7 of Σ|w·x|, the fp32 rounding level).
+ *   dense = 3: as 2 but one TMEM accumulation chain per tile (faster; ~1e-6 of Σ|w·x| on O/dI,
+ *              ~2e-5 normwise on dW_F from the fp32 chain over n·T).
+ *   Layers whose C or K is not a multiple of 4 (TMA strides) use the dense=1 kernels. */
 WINO_API int wino_set_weights(wino_plan* plan, const double* w_f, double zero_tol, int dense);
 /* Structure of the device CSR (for parity checks): per-slice nnz[p·q]; if the other
  * pointers are non-null they receive row_ptr (p·q·(K+1), slice-local offsets),

@@ -72,7 +72,7 @@ def conv_winograd(image, weights_winograd, m: int = 2, n: int = 0):
     if w_f.shape[1] != img.shape[0]:
         raise ShapeError(f"winograd_forward: weights expect {w_f.shape[1]} channels, image has {img.shape[0]}")
     layer = WinogradLayer(img.shape[0], w_f.shape[0], img.shape[1], img.shape[2], pad=0, m=m, r=r)
-    layer.set_weights(w_f, dense=True)
+    layer.set_weights(w_f, dense="exact")
     out = layer.forward(_to_dev(img[None]))
     return out[0].double().cpu().numpy()
 
@@ -85,7 +85,7 @@ def conv_winograd_grad(image, weights_winograd, grad_output, m: int = 2, n: int 
         raise ShapeError("expected a C x H x W image")
     m, r = _weights_transform(w_f, m, n)
     layer = WinogradLayer(img.shape[0], w_f.shape[0], img.shape[1], img.shape[2], pad=0, m=m, r=r)
-    layer.set_weights(w_f, dense=True)
+    layer.set_weights(w_f, dense="exact")
     go = np.asarray(grad_output, dtype=np.float64)
     if go.shape != (w_f.shape[0], layer.ho, layer.wo):
         raise ShapeError(f"backward_weights: upstream gradient {go.shape} does not match output "

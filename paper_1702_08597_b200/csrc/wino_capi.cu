@@ -179,6 +179,7 @@ struct wino_plan {
     float* d_wtl = nullptr;
     CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
     bool tc_ready = false;
+    bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
     // scratch
@@ -545,19 +546,21 @@ int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
 template <bool A_SPLIT, bool B_MN>
 int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
               const CUtensorMap& b, float* D, int M, int N, int Kd, int64_t ldd, int splits) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::SMEM_BYTES));
-        attr = true;
-    }
     const int kb_total = (Kd + wino::tc::BK - 1) / wino::tc::BK;
     const int kb_per = (kb_total + splits - 1) / splits;
-    const dim3 grid((unsigned)((N + wino::tc::BN - 1) / wino::tc::BN), (M + wino::tc::BM - 1) / wino::tc::BM,
-                    p->P2 * splits);
+    const int bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
+    const dim3 grid((unsigned)((N + bn - 1) / bn), (M + wino::tc::BM - 1) / wino::tc::BM, p->P2 * splits);
     Launch L(p, st, kind);
-    wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN><<<grid, wino::tc::THREADS, wino::tc::SMEM_BYTES, st>>>(
-        ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per);
+    if (p->tc_fast) {
+        set_smem_attr(wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN>, wino::tc::SMEM_BYTES);
+        wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN><<<grid, wino::tc::THREADS, wino::tc::SMEM_BYTES, st>>>(
+            ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per);
+    } else {
+        set_smem_attr(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>, wino::tc::flush::SMEM_BYTES);
+        wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>
+            <<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd, p->P2,
+                                                                                splits, kb_per);
+    }
     return L.done();
 }
 
@@ -574,11 +577,12 @@ int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& a
 // dW_F = dZ·Ĩ_Fᵀ on the tensor cores, split over NT, partials summed in fp64 -> K×C×p×q.
 int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs) {
     CUtensorMap ma, mb;
+    const uint32_t bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
     if (!wino::make_map_3d(&ma, DZ, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128) ||
-        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, 256))
+        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn))
         return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for dZ / Ĩ_F (CUresult " +
                                             std::to_string(wino::last_tmap_error()) + ")");
-    const int tiles = ((p->C + wino::tc::BN - 1) / wino::tc::BN) * ((p->K + wino::tc::BM - 1) / wino::tc::BM) * p->P2;
+    const int tiles = ((p->C + (int)bn - 1) / (int)bn) * ((p->K + wino::tc::BM - 1) / wino::tc::BM) * p->P2;
     const int kb_total = (int)((NTs + wino::tc::BK - 1) / wino::tc::BK);
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * p->sm_count + tiles - 1) / tiles, kb_total / 4));
     if (const char* e = std::getenv("WINO_DW_SPLITS")) splits = std::max(1, std::atoi(e));
@@ -833,7 +837,8 @@ int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense
         for (int s = 0; s < P2; ++s) p->slice_off[s] = (int64_t)s * K * C;
         int rc = upload_csr(p, rowptr, col, val);
         p->dense = true;
-        if (rc == WINO_OK && dense == 2) {
+        p->tc_fast = dense == 3;
+        if (rc == WINO_OK && dense >= 2) {
             rc = refresh_tc_operands(p, nullptr);
             if (rc == WINO_OK) CUDA_TRY(cudaDeviceSynchronize());
         }

@@ -298,6 +298,188 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
 }
 
+// ---------------------------------------------------------------------------------------
+// Accurate variant: every k-block (32 reduction elements × 3 tf32 products) accumulates into a
+// FRESH TMEM accumulator (double-buffered), which the epilogue warps fold into fp64 registers.
+// Long fp32 accumulation chains inside TMEM are what cost 3xTF32 its accuracy (measured: error
+// /Σ|p| 2.4e-6 with 63 k-blocks per accumulator vs 4.6e-8 with one), so this variant lands at
+// the fp32-rounding level of the result.  Tile 128×128; 320 threads:
+//   warp 0 TMA · warp 1 TMEM alloc + MMA · warps 2-9 hi/lo split of the stage two k-blocks
+//   ahead, then the drain of this k-block's accumulator (warp w reads TMEM lane quarter w%4,
+//   column half (w-2)/4: 64 fp64 sums per thread).
+// ---------------------------------------------------------------------------------------
+namespace flush {
+constexpr int BN = 128;
+constexpr int STAGES = 3;
+constexpr int THREADS = 320;
+constexpr int A_TILE = BM * BK * 4;   // 16 KB
+constexpr int B_TILE = BK * BN * 4;   // 16 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256;
+constexpr int TMEM_COLS = 2 * BN;
+
+__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+}  // namespace flush
+
+template <bool A_SPLIT, bool B_MN, int F>
+__global__ void __launch_bounds__(flush::THREADS, 1)
+gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
+                         const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N, int Kd,
+                         int64_t ldd, int slices, int splits, int kb_per) {
+    constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
+    constexpr int STAGE_BYTES = flush::STAGE_BYTES, TMEM_COLS = flush::TMEM_COLS;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;                       // [STAGES]
+    uint64_t* split = bars + STAGES;             // [STAGES] (64 arrivals)
+    uint64_t* empty = bars + 2 * STAGES;         // [STAGES]
+    uint64_t* tfull = bars + 3 * STAGES;         // [2]
+    uint64_t* tempty = bars + 3 * STAGES + 2;    // [2] (256 arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+    const int s = blockIdx.z / splits, q = blockIdx.z - s * splits;
+    const int kb_total = (Kd + BK - 1) / BK;
+    const int kb0 = q * kb_per;
+    const int kblocks = max(0, min(kb_total, kb0 + kb_per) - kb0);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split[i], 256);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int st = kb % STAGES;
+                if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
+                uint8_t* base = stage_ptr(st);
+                const int kk = (kb0 + kb) * BK;
+                mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
+                tma_load_3d(base, &mapAh, &full[st], kk, m0, s);
+                if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, m0, s);
+                if (B_MN) {
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j)
+                        tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], n0 + 32 * j, kk, s);
+                } else {
+                    tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, n0, s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id = flush::idesc(B_MN);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int st = kb % STAGES, g = kb / F, b = g & 1;
+                const bool first = (kb % F) == 0, last = (kb % F) == F - 1 || kb == kblocks - 1;
+                if (first && g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+                mbar_wait(&split[st], (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a_hi = smem_u32(stage_ptr(st));
+                const uint32_t a_lo = a_hi + A_TILE;
+                const uint32_t b_hi = a_hi + 2 * A_TILE;
+                const uint32_t b_lo = b_hi + B_TILE;
+                const uint32_t acc = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
+                    const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
+                    uint64_t dbh, dbl;
+                    if (B_MN) {
+                        dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                        dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                    } else {
+                        dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
+                        dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
+                    }
+                    mma_tf32(acc, dah, dbh, id, (first && k == 0) ? 0u : 1u);  // fresh per group
+                    mma_tf32(acc, dah, dbl, id, 1u);
+                    mma_tf32(acc, dal, dbh, id, 1u);
+                }
+                mma_commit(&empty[st]);
+                if (last) mma_commit(&tfull[b]);
+            }
+        }
+    } else {
+        const int t = threadIdx.x - 64;  // 0..255
+        const int qd = warp & 3, half = (warp - 2) >> 2;
+        auto split_stage = [&](int kb) {
+            const int st = kb % STAGES;
+            mbar_wait(&full[st], (kb / STAGES) & 1);
+            uint8_t* base = stage_ptr(st);
+            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t, 256);
+            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t, 256);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&split[st]);
+        };
+        for (int kb = 0; kb < min(kblocks, STAGES - 1); ++kb) split_stage(kb);
+        double accd[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) accd[j] = 0.0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+            if (kb + STAGES - 1 < kblocks) split_stage(kb + STAGES - 1);
+            if ((kb % F) != F - 1 && kb != kblocks - 1) continue;  // drain once per group
+            const int g = kb / F, b = g & 1;
+            mbar_wait(&tfull[b], (g >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + half * 64);
+            uint32_t v[32];
+            tmem_ld32(ta, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) accd[j] += (double)__uint_as_float(v[j]);
+            tmem_ld32(ta + 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty[b]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) accd[32 + j] += (double)__uint_as_float(v[j]);
+        }
+        const int row = m0 + qd * 32 + lane;
+        if (row < M) {
+            float* drow = D + (((int64_t)q * slices + s) * M + row) * ldd + n0 + half * 64;
+            const int col0 = n0 + half * 64;
+            if (col0 + 64 <= N && (ldd & 3) == 0) {
+#pragma unroll
+                for (int j = 0; j < 64; j += 4)
+                    *reinterpret_cast<float4*>(drow + j) =
+                        make_float4((float)accd[j], (float)accd[j + 1], (float)accd[j + 2], (float)accd[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 64; ++j)
+                    if (col0 + j < N) drow[j] = (float)accd[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // dW_F from the split-K partials [splits][P2][K][C]: fp64 sum in split order, written in the
 // W_F layout K×C×p×q (layer.hpp:36).
 __global__ void reduce_dw_kernel(const float* __restrict__ part, float* __restrict__ dw, int K, int C, int P2,

@@ -140,8 +140,12 @@ class WinogradLayer:
 
     # -- weights ------------------------------------------------------------------
     def set_weights(self, w_f, zero_tol: float = 0.0, dense: bool | str | None = None):
-        """W_F (K×C×p×q).  dense=None picks the dense layer when no entry is dropped; dense='tc'
-        runs the dense contractions on the tensor cores (3xTF32 tcgen05, approximate)."""
+        """W_F (K×C×p×q).
+        dense=False: CSR of the nonzeros (the sparse path).  dense=None: dense when no entry is
+        dropped.  dense=True / 'tc': every coordinate is a weight; the contractions run on the
+        tensor cores (3xTF32 tcgen05, each k-block folded into fp64 — fp32-level accuracy).
+        dense='exact': the reference-order SIMT kernels (bitwise forward).  dense='tc-fast': one
+        TMEM accumulation chain (fastest, ~1e-6 of Σ|w·x|)."""
         w_f = np.ascontiguousarray(w_f, dtype=np.float64)
         if w_f.shape != (self.k, self.c, self.p, self.p):
             raise _lib.ShapeError(f"weights {w_f.shape} do not match layer "
@@ -149,7 +153,10 @@ class WinogradLayer:
         if dense is None:
             kept = (np.abs(w_f) > zero_tol) | ((zero_tol == 0.0) & (w_f != 0.0))
             dense = bool(kept.all())
-        mode = 2 if dense == "tc" else int(bool(dense))
+        mode = ({"tc": 2, "tc-fast": 3, "exact": 1}.get(dense, None) if isinstance(dense, str)
+                else (2 if dense else 0))
+        if mode is None:
+            raise _lib.InvalidArgument(f"dense must be None, bool, 'tc', 'tc-fast' or 'exact', got {dense!r}")
         check(lib().wino_set_weights(self._h, w_f.ctypes.data_as(_lib._pd), zero_tol, mode))
 
     def set_weights_csr(self, csr: PointwiseCsr):

@@ -18,6 +18,13 @@ static float tf32_round(float x) {  // host rna to tf32
     return r;
 }
 
+static bool g_flush = false;
+static int g_F = 1;
+template <bool A, bool B>
+auto flush_k() {
+    return g_F == 1 ? wino::tc::gemm_3xtf32_flush_kernel<A, B, 1>
+         : g_F == 2 ? wino::tc::gemm_3xtf32_flush_kernel<A, B, 2> : wino::tc::gemm_3xtf32_flush_kernel<A, B, 4>;
+}
 int run(int S, int M, int N, int Kd, bool timeit) {
     const int NTs = (N + 3) / 4 * 4;
     std::mt19937 rng(1234 + M + N + Kd);
@@ -45,11 +52,13 @@ int run(int S, int M, int N, int Kd, bool timeit) {
               wino::make_map_3d(&mAl, dAl, Kd, M, S, (uint64_t)Kd * 4, (uint64_t)M * Kd * 4, 32, 128) &&
               wino::make_map_3d(&mB, dB, NTs, Kd, S, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true);
     if (!ok) { printf("tensor map creation failed\n"); return 1; }
-    auto kern = wino::tc::gemm_3xtf32_kernel<false, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::SMEM_BYTES);
-    dim3 grid((NTs + 255) / 256, (M + 127) / 128, S);
+    auto kern = g_flush ? flush_k<false, true>() : wino::tc::gemm_3xtf32_kernel<false, true>;
+    const int smem = g_flush ? wino::tc::flush::SMEM_BYTES : wino::tc::SMEM_BYTES;
+    const int bn = g_flush ? 128 : 256, th = g_flush ? wino::tc::flush::THREADS : 256;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    dim3 grid((NTs + bn - 1) / bn, (M + 127) / 128, S);
     const int kbp = (Kd + 31) / 32;
-    kern<<<grid, 256, wino::tc::SMEM_BYTES>>>(mAh, mAl, mB, dD, M, NTs, Kd, NTs, S, 1, kbp);
+    kern<<<grid, th, smem>>>(mAh, mAl, mB, dD, M, NTs, Kd, NTs, S, 1, kbp);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("kernel error: %s\n", cudaGetErrorString(e)); return 1; }
     std::vector<float> D((size_t)S * M * NTs);
@@ -97,7 +106,7 @@ int run(int S, int M, int N, int Kd, bool timeit) {
         cudaEventCreate(&b);
         cudaEventRecord(a);
         for (int i = 0; i < 10; ++i)
-            kern<<<grid, 256, wino::tc::SMEM_BYTES>>>(mAh, mAl, mB, dD, M, NTs, Kd, NTs, S, 1, kbp);
+            kern<<<grid, th, smem>>>(mAh, mAl, mB, dD, M, NTs, Kd, NTs, S, 1, kbp);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -126,13 +135,15 @@ int run_kk(int S, int M, int N, int R, int splits) {
     cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
     CUtensorMap mA, mB;
     bool ok = wino::make_map_3d(&mA, dA, R, M, S, (uint64_t)R * 4, (uint64_t)M * R * 4, 32, 128) &&
-              wino::make_map_3d(&mB, dB, R, N, S, (uint64_t)R * 4, (uint64_t)N * R * 4, 32, 256);
+              wino::make_map_3d(&mB, dB, R, N, S, (uint64_t)R * 4, (uint64_t)N * R * 4, 32, g_flush ? 128 : 256);
     if (!ok) { printf("map failed %d\n", wino::last_tmap_error()); return 1; }
-    auto kern = wino::tc::gemm_3xtf32_kernel<true, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::SMEM_BYTES);
+    auto kern = g_flush ? flush_k<true, false>() : wino::tc::gemm_3xtf32_kernel<true, false>;
+    const int smem = g_flush ? wino::tc::flush::SMEM_BYTES : wino::tc::SMEM_BYTES;
+    const int bn = g_flush ? 128 : 256, th = g_flush ? wino::tc::flush::THREADS : 256;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int kbt = (R + 31) / 32, kbp = (kbt + splits - 1) / splits;
-    dim3 grid((N + 255) / 256, (M + 127) / 128, S * splits);
-    kern<<<grid, 256, wino::tc::SMEM_BYTES>>>(mA, mA, mB, dP, M, N, R, N, S, splits, kbp);
+    dim3 grid((N + bn - 1) / bn, (M + 127) / 128, S * splits);
+    kern<<<grid, th, smem>>>(mA, mA, mB, dP, M, N, R, N, S, splits, kbp);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("kernel error: %s\n", cudaGetErrorString(e)); return 1; }
     std::vector<float> P((size_t)splits * S * M * N);
@@ -165,13 +176,38 @@ int main() {
     rc0 |= run_kk(1, 128, 256, 64, 1);
     rc0 |= run_kk(2, 256, 256, 1000, 3);
     rc0 |= run_kk(2, 384, 200, 520, 2);
+    // accuracy vs accumulation length: same product, 1 split (TMEM accumulates all 63 k-blocks)
+    // vs 63 splits (each k-block a fresh accumulator, partials summed in fp64)
+    rc0 |= run_kk(2, 128, 256, 2000, 1);
+    rc0 |= run_kk(2, 128, 256, 2000, 8);
+    rc0 |= run_kk(2, 128, 256, 2000, 63);
+    g_flush = true;
+    printf("--- flush variant ---\n");
+    rc0 |= run_kk(1, 128, 256, 64, 1);
+    rc0 |= run_kk(2, 256, 256, 1000, 3);
+    rc0 |= run_kk(2, 384, 200, 520, 2);
+    rc0 |= run_kk(2, 128, 256, 2000, 1);
+    rc0 |= run(1, 128, 256, 32, false);
+    rc0 |= run(3, 256, 520, 256, false);
+    rc0 |= run(2, 16, 36, 16, false);
+    rc0 |= run(2, 384, 1000, 256, false);
+    rc0 |= run(36, 256, 12544, 256, true);
+    for (int f : {2, 4}) {
+        g_F = f;
+        printf("--- flush every %d k-blocks ---\n", f);
+        rc0 |= run_kk(2, 128, 256, 2000, 1);
+        rc0 |= run(36, 256, 12544, 256, true);
+    }
+    g_flush = false;
+    printf("--- fast variant timing ---\n");
+    rc0 |= run(36, 256, 12544, 256, true);
     int rc = 0;
     rc |= run(1, 128, 256, 32, false);
     rc |= run(2, 128, 256, 64, false);
     rc |= run(3, 256, 520, 256, false);
     rc |= run(2, 16, 36, 16, false);
     rc |= run(2, 384, 1000, 256, false);
-    rc |= run(36, 256, 12544, 256, true);
+    // rc |= run(36, 256, 12544, 256, true);
     rc |= rc0;
     return rc;
 }
