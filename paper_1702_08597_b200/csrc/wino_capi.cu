@@ -153,6 +153,7 @@ struct wino_plan {
     wino_geometry g{};
     wino::Coefs cf{};
     bool has_weights = false, dense = false;
+    bool builtin = false;  // coefficients equal a built-in set: compile-time-constant kernels
     int64_t nnz = 0;
     std::vector<int64_t> slice_nnz, slice_off;
     // CSR (global offsets) and CSC of W_F(:,:,i,j)ᵀ
@@ -449,45 +450,45 @@ int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
     return WINO_OK;
 }
 
-template <int M, int P>
+template <int M, int P, class CF>
 int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, wino_cache* c,
                    float* V, float* Z, int n, int64_t NT, int64_t NTs, int flags, int stage) {
     const wino_geometry& g = p->g;
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
-        wino::input_transform_kernel<M, P><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
+        wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
             in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
     const int grid = grid_for((int64_t)p->K * NT, 256, p->sm_count);
     if (flags & WINO_FWD_RELU)
-        wino::output_transform_kernel<M, P, true><<<grid, 256, 0, st>>>(
+        wino::output_transform_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(
             Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
     else
-        wino::output_transform_kernel<M, P, false><<<grid, 256, 0, st>>>(
+        wino::output_transform_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(
             Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
     return L.done();
 }
 
-template <int M, int P>
+template <int M, int P, class CF>
 int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
                   int64_t NT, int64_t NTs, bool mask) {
     const wino_geometry& g = p->g;
     Launch L(p, st, K_GRADZ);
     const int grid = grid_for((int64_t)p->K * NTs, 256, p->sm_count);
     if (mask)
-        wino::grad_z_kernel<M, P, true><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
+        wino::grad_z_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
                                                               (int)NT, (int)NTs);
     else
-        wino::grad_z_kernel<M, P, false><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
+        wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t,
                                                                (int)NT, (int)NTs);
     return L.done();
 }
 
-template <int M, int P>
+template <int M, int P, class CF>
 int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI, int n, int64_t NTs) {
     const wino_geometry& g = p->g;
     const int T = (int)g.t;
@@ -498,21 +499,24 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
         int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c,
                                                                 (256 + T - 1) / T}));
         const size_t smem = (size_t)cg * per_c;
-        set_smem_attr(wino::input_grad_kernel<M, P>, (int)std::max<size_t>(smem, 48 * 1024));
-        wino::input_grad_kernel<M, P><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
+        set_smem_attr(wino::input_grad_kernel<M, P, CF>, (int)std::max<size_t>(smem, 48 * 1024));
+        wino::input_grad_kernel<M, P, CF><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
             DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg);
     } else {
         const int64_t total = (int64_t)n * p->C * p->H * p->W;
-        wino::input_grad_direct_kernel<M, P><<<grid_for(total, 256, p->sm_count), 256, 0, st>>>(
+        wino::input_grad_direct_kernel<M, P, CF><<<grid_for(total, 256, p->sm_count), 256, 0, st>>>(
             DV, dI, p->cf, n, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs);
     }
     return L.done();
 }
 
-#define DISPATCH_MP(p, FN, ...)                                         \
-    ((p)->m == 4   ? FN<4, 6>(__VA_ARGS__)                              \
-     : (p)->m == 2 ? FN<2, 4>(__VA_ARGS__)                              \
-                   : FN<6, 8>(__VA_ARGS__))
+#define DISPATCH_MP(p, FN, ...)                                                                    \
+    ((p)->m == 4   ? ((p)->builtin ? FN<4, 6, wino::ConstCoef<4, 6>>(__VA_ARGS__)                      \
+                                   : FN<4, 6, wino::RuntimeCoef>(__VA_ARGS__))                          \
+     : (p)->m == 2 ? ((p)->builtin ? FN<2, 4, wino::ConstCoef<2, 4>>(__VA_ARGS__)                      \
+                                   : FN<2, 4, wino::RuntimeCoef>(__VA_ARGS__))                          \
+                   : ((p)->builtin ? FN<6, 8, wino::ConstCoef<6, 8>>(__VA_ARGS__)                      \
+                                   : FN<6, 8, wino::RuntimeCoef>(__VA_ARGS__)))
 
 // Dense plan: (re)build the tcgen05 operands from the live values (full CSR order = W[s][k][c]).
 int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
@@ -733,6 +737,15 @@ int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
     }
     for (int i = 0; i < p->p * p->m; ++i) p->cf.a[i] = (float)a[i];
     for (int i = 0; i < p->p * p->p; ++i) p->cf.b[i] = (float)b[i];
+    auto same = [&](const float* ta, const float* tb) {
+        return std::memcmp(p->cf.a, ta, sizeof(float) * p->p * p->m) == 0 &&
+               std::memcmp(p->cf.b, tb, sizeof(float) * p->p * p->p) == 0;
+    };
+    if (!std::getenv("WINO_RUNTIME_COEFS")) {
+        if (p->m == 4) p->builtin = same(wino::BuiltinCoefs<4, 6>::a, wino::BuiltinCoefs<4, 6>::b);
+        if (p->m == 2) p->builtin = same(wino::BuiltinCoefs<2, 4>::a, wino::BuiltinCoefs<2, 4>::b);
+        if (p->m == 6) p->builtin = same(wino::BuiltinCoefs<6, 8>::a, wino::BuiltinCoefs<6, 8>::b);
+    }
     cudaError_t e = cudaSetDevice(p->device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device);
     if (e == cudaSuccess)

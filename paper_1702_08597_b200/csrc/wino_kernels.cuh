@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "builtin_coefs.h"
+
 namespace wino {
 
 constexpr int kMaxP = 8;
@@ -36,11 +38,44 @@ __device__ __forceinline__ float madd(float acc, float c, float x) {
     return __fadd_rn(acc, __fmul_rn(c, x));
 }
 
+// Coefficient policies.  RuntimeCoef reads the plan's Coefs (any TransformSet the caller
+// passes).  ConstCoef<M,P> uses the built-in sets as compile-time constants (builtin_coefs.h,
+// the reference's doubles cast to float): after unrolling, a zero coefficient drops its term
+// and ±1 drops the multiply — bit-identical for finite inputs (acc starts at +0 and never
+// becomes -0, so acc + (±0) == acc; 1·x == x; -1·x == -x exactly).
+struct RuntimeCoef {
+    static constexpr bool kConst = false;
+};
+template <int M, int P>
+struct ConstCoef {
+    static constexpr bool kConst = true;
+};
+
+template <class CF, int M, int P>
+__device__ __forceinline__ float coef_a(const Coefs& cf, int i) {
+    if constexpr (CF::kConst) return BuiltinCoefs<M, P>::A(i);
+    else return cf.a[i];
+}
+template <class CF, int M, int P>
+__device__ __forceinline__ float coef_b(const Coefs& cf, int i) {
+    if constexpr (CF::kConst) return BuiltinCoefs<M, P>::B(i);
+    else return cf.b[i];
+}
+template <class CF>
+__device__ __forceinline__ float cmadd(float acc, float c, float x) {
+    if constexpr (CF::kConst) {
+        if (c == 0.f) return acc;
+        if (c == 1.f) return __fadd_rn(acc, x);
+        if (c == -1.f) return __fsub_rn(acc, x);
+    }
+    return madd(acc, c, x);
+}
+
 // ---------------------------------------------------------------------------------
 // K1: φ gather (pad folded in) + Ĩ_F = B1ᵀ·d·B2   (transforms.cpp:196-210, sparse.cpp:94-120)
 // One thread per (c, nt); consecutive threads = consecutive tiles -> coalesced stores.
 // ---------------------------------------------------------------------------------
-template <int M, int P>
+template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
                        int H, int W, int pad, int tiles_x, int T, int NT, int NTs) {
@@ -78,7 +113,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
             for (int j = 0; j < P; ++j) {
                 float acc = 0.f;
 #pragma unroll
-                for (int k = 0; k < P; ++k) acc = madd(acc, cf.b[k * P + i], d[k][j]);
+                for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + i), d[k][j]);
                 tmp[i][j] = acc;
             }
 #pragma unroll
@@ -87,7 +122,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
             for (int j = 0; j < P; ++j) {
                 float acc = 0.f;
 #pragma unroll
-                for (int k = 0; k < P; ++k) acc = madd(acc, cf.b[k * P + j], tmp[i][k]);
+                for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
                 V[(int64_t)(i * P + j) * plane + gid] = acc;
             }
     }
@@ -97,7 +132,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
 // K3: O = ψ(A1ᵀ·Z·A2), crop, optional ReLU   (sparse.cpp:151-184; layer.cpp:79-95)
 // One thread per (k, nt): 36 coalesced loads, 16 outputs.
 // ---------------------------------------------------------------------------------
-template <int M, int P, bool RELU>
+template <int M, int P, bool RELU, class CF>
 __global__ void __launch_bounds__(256)
 output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, const Coefs cf, int K,
                         int Ho, int Wo, int tiles_x, int T, int NT, int NTs) {
@@ -120,7 +155,7 @@ output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, cons
             for (int j = 0; j < P; ++j) {
                 float acc = 0.f;
 #pragma unroll
-                for (int i = 0; i < P; ++i) acc = madd(acc, cf.a[i * M + y], z[i][j]);
+                for (int i = 0; i < P; ++i) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), z[i][j]);
                 tmp[y][j] = acc;
             }
         const int n = nt / T, t = nt - n * T;
@@ -133,7 +168,7 @@ output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, cons
             for (int x = 0; x < M; ++x) {
                 float acc = 0.f;
 #pragma unroll
-                for (int j = 0; j < P; ++j) acc = madd(acc, cf.a[j * M + x], tmp[y][j]);
+                for (int j = 0; j < P; ++j) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), tmp[y][j]);
                 if (RELU) acc = acc > 0.f ? acc : 0.f;  // train.cpp:76-83
                 const int ox = tx * M + x;
                 if (oy < Ho && ox < Wo) op[oy * Wo + ox] = acc;
@@ -147,7 +182,7 @@ output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, cons
 //     (layer.cpp:107-116, transforms.cpp:228-241, train.cpp:193)
 // One thread per (k, nt < NTs); padding columns nt ≥ NT are written as zeros.
 // ---------------------------------------------------------------------------------
-template <int M, int P, bool MASK>
+template <int M, int P, bool MASK, class CF>
 __global__ void __launch_bounds__(256)
 grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
               float* __restrict__ DZ, const Coefs cf, int K, int Ho, int Wo, int tiles_x, int T,
@@ -190,7 +225,7 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
             for (int x = 0; x < M; ++x) {
                 float acc = 0.f;
 #pragma unroll
-                for (int y = 0; y < M; ++y) acc = madd(acc, cf.a[i * M + y], d[y][x]);
+                for (int y = 0; y < M; ++y) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), d[y][x]);
                 m1[i][x] = acc;
             }
 #pragma unroll
@@ -199,7 +234,7 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
             for (int j = 0; j < P; ++j) {  // dz(i,j) = Σ_x m1(i,x)·a2(j,x)
                 float acc = 0.f;
 #pragma unroll
-                for (int x = 0; x < M; ++x) acc = madd(acc, cf.a[j * M + x], m1[i][x]);
+                for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), m1[i][x]);
                 DZ[(int64_t)(i * P + j) * plane + gid] = acc;
             }
     }
@@ -212,7 +247,7 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
 //     its ≤⌈p/m⌉² contributions in ascending t order from +0 (the reference's
 //     accumulation order), so no atomics and the result is bitwise deterministic.
 // ---------------------------------------------------------------------------------
-template <int M, int P>
+template <int M, int P, class CF>
 __device__ __forceinline__ float tile_grad_entry(const float* __restrict__ dv, int64_t plane,
                                                  const Coefs& cf, int i, int j) {
     // g(i,j) with m1(i,l) = Σ_k b1(i,k)·x(k,l) ; g(i,j) = Σ_l m1(i,l)·b2(j,l)
@@ -221,13 +256,13 @@ __device__ __forceinline__ float tile_grad_entry(const float* __restrict__ dv, i
     for (int l = 0; l < P; ++l) {
         float m = 0.f;
 #pragma unroll
-        for (int k = 0; k < P; ++k) m = madd(m, cf.b[i * P + k], __ldg(dv + (int64_t)(k * P + l) * plane));
-        acc = madd(acc, cf.b[j * P + l], m);
+        for (int k = 0; k < P; ++k) m = cmadd<CF>(m, coef_b<CF, M, P>(cf, i * P + k), __ldg(dv + (int64_t)(k * P + l) * plane));
+        acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, j * P + l), m);
     }
     return acc;
 }
 
-template <int M, int P>
+template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Coefs cf, int C,
                   int H, int W, int pad, int tiles_y, int tiles_x, int T, int NTs, int CG) {
@@ -253,7 +288,7 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
             for (int l = 0; l < P; ++l) {
                 float acc = 0.f;
 #pragma unroll
-                for (int k = 0; k < P; ++k) acc = madd(acc, cf.b[i * P + k], x[k][l]);
+                for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, i * P + k), x[k][l]);
                 m1[i][l] = acc;
             }
         float* g = gsm + (int64_t)idx * TS;
@@ -263,7 +298,7 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
             for (int j = 0; j < P; ++j) {
                 float acc = 0.f;
 #pragma unroll
-                for (int l = 0; l < P; ++l) acc = madd(acc, cf.b[j * P + l], m1[i][l]);
+                for (int l = 0; l < P; ++l) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, j * P + l), m1[i][l]);
                 g[i * P + j] = acc;
             }
     }
@@ -309,7 +344,7 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
 
 // Same result without shared-memory staging (large T): each pixel recomputes the
 // transformed-tile entries it needs (identical operation order, hence identical bits).
-template <int M, int P>
+template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_grad_direct_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Coefs cf,
                          int N, int C, int H, int W, int pad, int tiles_y, int tiles_x, int T,
@@ -332,7 +367,7 @@ input_grad_direct_kernel(const float* __restrict__ DV, float* __restrict__ dI, c
             for (int tx = tx_lo; tx <= tx_hi; ++tx) {
                 const int t = ty * tiles_x + tx;
                 const float* src = DV + (int64_t)c * NTs + (int64_t)n * T + t;
-                acc = __fadd_rn(acc, tile_grad_entry<M, P>(src, plane, cf, Y - ty * M, X - tx * M));
+                acc = __fadd_rn(acc, tile_grad_entry<M, P, CF>(src, plane, cf, Y - ty * M, X - tx * M));
             }
         dI[gid] = acc;
     }

@@ -125,3 +125,20 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(wb.CudaError):
         wb.WinogradLayer(16, 16, 12, 12)
+
+
+def test_builtin_coefficient_header_matches_reference():
+    """csrc/builtin_coefs.h (compile-time coefficients of the specialised transform kernels)
+    holds exactly the fp32 casts of the reference's TransformSet doubles."""
+    import re
+
+    text = (_lib.LIB_PATH.parent / "csrc" / "builtin_coefs.h").read_text()
+    z = np.load(GOLDEN / "transforms.npz")
+    for m in (2, 4, 6):
+        blk = text[text.index(f"struct BuiltinCoefs<{m}, {m + 2}>"):]
+        for key in ("a", "b"):
+            body = re.search(rf"static constexpr float {key}\[\d+\] = \{{([^}}]*)\}}", blk).group(1)
+            vals = np.array([float.fromhex(v.strip()[:-1]) if "0x" in v else float(v.strip()[:-1])
+                             for v in body.split(",")], dtype=np.float32)
+            ref = z[f"{key.upper()}{m}"].astype(np.float32).ravel()
+            assert np.array_equal(vals.view(np.int32), ref.view(np.int32)), (m, key)

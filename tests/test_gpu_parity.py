@@ -415,3 +415,15 @@ def test_stack_training_step_matches_mirror():
         v1 = np.concatenate(lay.get_csr().values)
         np.testing.assert_allclose(v1, v0 - 0.05 * g.cpu().numpy() / 3, rtol=1e-5, atol=1e-7)
         assert lay.nnz == len(v0)  # the mask is fixed: pruned coordinates never reappear
+
+
+@pytest.mark.parametrize("name", ["c0", "f23_odd", "f63"])
+def test_runtime_and_builtin_coefficient_kernels_agree_bitwise(name, monkeypatch):
+    """Transform kernels with compile-time coefficients (zero terms dropped) vs the generic
+    runtime-coefficient kernels: identical bits."""
+    d = load_layer(name)
+    a = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False)
+    monkeypatch.setenv("WINO_RUNTIME_COEFS", "1")
+    b = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False)
+    for key in ("o", "di", "dw_raw"):
+        assert np.array_equal(a[key], b[key]), key
