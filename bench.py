@@ -227,6 +227,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
     dense = cfg.sparsity == 0.0
     layer.set_weights(w_f, dense=(args.dense or "tc") if dense else False)
+    if args.dw == "tc" and not dense:
+        layer.set_dw_mode("tc")
     cache = layer.new_cache(n)
     x = torch.from_numpy(img).to(dev)
     g_o = torch.from_numpy(go).to(dev)
@@ -364,6 +366,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
                    "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
                              "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else "csr",
+                   "dw": "masked-sddmm-exact" if args.dw == "sddmm" else "tcgen05-3xtf32-fp64fold+mask-gather",
                    "l2_flush": "256 MB write between timed steps",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
@@ -514,6 +517,8 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
+    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc"],
+                    help="sparse dW_F: exact masked SDDMM (default) or tensor-core GEMM + mask gather")
     ap.add_argument("--dense", default=None, choices=["tc", "tc-fast", "exact"],
                     help="dense path at 0%% sparsity: 'tc' (default: 3xTF32 tcgen05, per-k-block fp64 "
                          "folding), 'tc-fast' (one TMEM chain), 'exact' (reference-order SIMT)")

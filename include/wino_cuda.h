@@ -148,6 +148,15 @@ WINO_API int wino_backward_input(wino_plan* plan, const wino_cache* cache, float
 WINO_API int wino_sgd_step(wino_plan* plan, const float* grad_w, float lr, float scale, float l2,
                   void* stream);
 
+/* Plan options.
+ *   WINO_OPT_DW_MODE: how the sparse plan computes dW_F on the mask (layer.cpp:118-128):
+ *     0 (default) masked SDDMM — exact fp64 products and accumulation of the fp32 operands;
+ *     1 tensor cores — the accurate 3xTF32 tcgen05 GEMM over all K×C (per-k-block fp64
+ *       folding, ~2e-7 of Σ|dz·x|), then the surviving entries gathered in CSR order.
+ *       Faster whenever the density is above a few percent; requires C, K multiples of 4. */
+#define WINO_OPT_DW_MODE 1
+WINO_API int wino_set_option(wino_plan* plan, int option, int value);
+
 /* ---------------------------------------------------------------------------- */
 /* Instrumentation                                                               */
 /* ---------------------------------------------------------------------------- */

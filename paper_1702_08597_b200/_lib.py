@@ -98,6 +98,7 @@ SIGNATURES = {
     "wino_backward_weights": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_input": (C.c_int, [_vp, _vp, _vp, _vp]),
     "wino_sgd_step": (C.c_int, [_vp, _vp, C.c_float, C.c_float, C.c_float, _vp]),
+    "wino_set_option": (C.c_int, [_vp, C.c_int, C.c_int]),
     "wino_launch_count": (C.c_int64, [_vp]),
     "wino_reset_launch_count": (None, [_vp]),
     "wino_profile_enable": (C.c_int, [_vp, C.c_int]),
@@ -106,6 +107,7 @@ SIGNATURES = {
     "wino_version": (C.c_char_p, []),
 }
 
+WINO_OPT_DW_MODE = 1
 WINO_FWD_RELU = 1
 WINO_BWD_RELU_MASK = 1
 

@@ -181,6 +181,8 @@ struct wino_plan {
     CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
     bool tc_ready = false;
     bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
+    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather
+    int64_t* d_slice_off = nullptr;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
     // scratch
@@ -213,11 +215,17 @@ struct wino_cache {
 namespace {
 
 void free_weights(wino_plan* p) {
+    const char* names[] = {"rowptr", "colidx", "rowof", "vals", "colptr", "rowidx", "perm", "cv", "cvT",
+                           "wdense", "wh", "wl", "wth", "wtl"};
+    int i = 0;
     for (void* ptr : {(void*)p->d_rowptr, (void*)p->d_colidx, (void*)p->d_rowof, (void*)p->d_vals,
                       (void*)p->d_colptr, (void*)p->d_rowidx, (void*)p->d_perm, (void*)p->d_cv,
                       (void*)p->d_cvT, (void*)p->d_wdense, (void*)p->d_wh, (void*)p->d_wl, (void*)p->d_wth,
-                      (void*)p->d_wtl})
-        if (ptr) cudaFree(ptr);
+                      (void*)p->d_wtl}) {
+        if (ptr && cudaFree(ptr) != cudaSuccess)
+            std::fprintf(stderr, "wino: cudaFree(%s) failed\n", names[i]);
+        ++i;
+    }
     p->d_wh = p->d_wl = p->d_wth = p->d_wtl = nullptr;
     p->tc_ready = false;
     p->d_rowptr = p->d_colidx = p->d_rowof = p->d_colptr = p->d_rowidx = p->d_perm = nullptr;
@@ -579,7 +587,8 @@ int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& a
 }
 
 // dW_F = dZ·Ĩ_Fᵀ on the tensor cores, split over NT, partials summed in fp64 -> K×C×p×q.
-int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs) {
+int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs,
+                 bool masked = false) {
     CUtensorMap ma, mb;
     const uint32_t bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
     if (!wino::make_map_3d(&ma, DZ, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128) ||
@@ -595,10 +604,15 @@ int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
     int rc = ensure(&p->d_dwc, &p->dwc_cap, need);
     if (rc) return rc;
     part = p->d_dwc;
-    if ((rc = launch_tc<true, false>(p, st, K_DENSE_DW, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits))) return rc;
-    Launch L(p, st, K_DENSE_DW);
-    wino::tc::reduce_dw_kernel<<<grid_for((int64_t)p->P2 * p->K * p->C, 256, p->sm_count), 256, 0, st>>>(
-        part, dW, p->K, p->C, p->P2, splits);
+    const int kind = masked ? K_SDDMM : K_DENSE_DW;
+    if ((rc = launch_tc<true, false>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits))) return rc;
+    Launch L(p, st, kind);
+    if (masked)
+        wino::tc::reduce_dw_masked_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
+            part, dW, p->d_rowof, p->d_colidx, p->d_slice_off, p->K, p->C, p->P2, splits, p->nnz);
+    else
+        wino::tc::reduce_dw_kernel<<<grid_for((int64_t)p->P2 * p->K * p->C, 256, p->sm_count), 256, 0, st>>>(
+            part, dW, p->K, p->C, p->P2, splits);
     return L.done();
 }
 
@@ -656,6 +670,14 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
         return rc;
     p->h_rowptr = rowptr;
     p->h_colptr = colptr;
+    if (p->d_slice_off) {
+        cudaFree(p->d_slice_off);
+        p->d_slice_off = nullptr;
+    }
+    if (p->slice_off.size() == (size_t)P2) {
+        CUDA_TRY(cudaMalloc(&p->d_slice_off, P2 * sizeof(int64_t)));
+        CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
@@ -761,18 +783,26 @@ int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
 
 int wino_plan_destroy(wino_plan* p) {
     if (!p) return WINO_OK;
+    std::string bad;
+    auto chk = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && bad.empty()) bad = std::string(what) + ": " + cudaGetErrorString(e);
+    };
+    chk(cudaGetLastError(), "pending error before destroy");
     free_weights(p);
-    if (p->d_dwc) cudaFree(p->d_dwc);
-    if (p->d_z) cudaFree(p->d_z);
-    if (p->d_dv) cudaFree(p->d_dv);
-    if (p->d_scalar) cudaFree(p->d_scalar);
-    if (p->d_partial) cudaFree(p->d_partial);
+    chk(cudaGetLastError(), "free_weights");
+    if (p->d_dwc) chk(cudaFree(p->d_dwc), "d_dwc");
+    if (p->d_z) chk(cudaFree(p->d_z), "d_z");
+    if (p->d_dv) chk(cudaFree(p->d_dv), "d_dv");
+    if (p->d_scalar) chk(cudaFree(p->d_scalar), "d_scalar");
+    if (p->d_partial) chk(cudaFree(p->d_partial), "d_partial");
+    if (p->d_slice_off) chk(cudaFree(p->d_slice_off), "d_slice_off");
     for (auto& r : p->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     delete p;
-    return WINO_OK;
+    cudaGetLastError();  // never leave a stale error behind for the caller's next CUDA call
+    return bad.empty() ? WINO_OK : set_err(WINO_CUDA_ERROR, "plan_destroy: " + bad);
 }
 
 int wino_plan_info(const wino_plan* p, wino_geometry* geom, int64_t* nnz_total, int* is_dense) {
@@ -1011,7 +1041,11 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
         float* dwc = grad_w;
         if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
         if (p->dense) dwc = p->d_dwc;
-        if ((rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs))) return rc;
+        if (!p->dense && p->dw_mode == 1 && p->nnz > 0)
+            rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
+        else
+            rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs);
+        if (rc) return rc;
         if (p->dense) {  // [s][k][c] -> K×C×p×q
             Launch L(p, st, K_MISC);
             wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
@@ -1067,6 +1101,22 @@ int wino_sgd_step(wino_plan* p, const float* grad_w, float lr, float scale, floa
         if ((rc = L.done())) return rc;
     }
     return wino_values_updated(p, stream);
+}
+
+int wino_set_option(wino_plan* p, int option, int value) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    if (option != WINO_OPT_DW_MODE || value < 0 || value > 1)
+        return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
+    if (value == 1) {
+        if (p->C % 4 || p->K % 4)
+            return set_err(WINO_CAPABILITY_ERROR, "tensor-core dW needs C and K multiples of 4 (TMA strides)");
+        if (!p->d_slice_off && p->has_weights) {
+            CUDA_TRY(cudaMalloc(&p->d_slice_off, p->P2 * sizeof(int64_t)));
+            CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), p->P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
+        }
+    }
+    p->dw_mode = value;
+    return WINO_OK;
 }
 
 int64_t wino_launch_count(const wino_plan* p) { return p ? p->launches : -1; }

@@ -494,5 +494,23 @@ __global__ void reduce_dw_kernel(const float* __restrict__ part, float* __restri
     }
 }
 
+// Sparse plan, dW on the tensor cores: sum the split-K partials [splits][P2][K][C] in fp64 at the
+// surviving coordinates only, written in CSR order (e -> (slice, row, col)).
+__global__ void reduce_dw_masked_kernel(const float* __restrict__ part, float* __restrict__ dwc,
+                                        const int* __restrict__ rowof, const int* __restrict__ colidx,
+                                        const int64_t* __restrict__ slice_off, int K, int C, int P2,
+                                        int splits, int64_t nnz) {
+    const int64_t plane = (int64_t)P2 * K * C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;  // slice of e: P2 ≤ 64 offsets, linear scan
+        while (s + 1 < P2 && slice_off[s + 1] <= e) ++s;
+        const int64_t idx = ((int64_t)s * K + rowof[e]) * C + colidx[e];
+        double a = 0.0;
+        for (int q = 0; q < splits; ++q) a += (double)part[(int64_t)q * plane + idx];
+        dwc[e] = (float)a;
+    }
+}
+
 }  // namespace tc
 }  // namespace wino

@@ -200,6 +200,10 @@ class WinogradLayer:
                             [col[offs[s]:offs[s + 1]].copy() for s in range(n)],
                             [val[offs[s]:offs[s + 1]].copy() for s in range(n)])
 
+    def set_dw_mode(self, mode: str):
+        """'sddmm' (default: exact masked SDDMM) or 'tc' (tensor-core GEMM + mask gather)."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE, {"sddmm": 0, "tc": 1}[mode]))
+
     def weight_values(self):
         """Device pointer (int) of the live CSR values (nnz floats)."""
         ptr = C.c_void_p()
@@ -283,8 +287,8 @@ class WinogradLayer:
 
     def close(self):
         if self._h:
-            lib().wino_plan_destroy(self._h)
-            self._h = C.c_void_p()
+            h, self._h = self._h, C.c_void_p()
+            check(lib().wino_plan_destroy(h))
 
     def __del__(self):
         try:
