@@ -418,6 +418,9 @@ gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid
                     mma_tf32(acc, dah, dbh, id, (first && k == 0) ? 0u : 1u);  // fresh per group
                     mma_tf32(acc, dah, dbl, id, 1u);
                     mma_tf32(acc, dal, dbh, id, 1u);
+#ifdef WINO_TC_FOUR_PRODUCTS  // lo·lo measured no accuracy gain (the MMA's internal sum dominates)
+                    mma_tf32(acc, dal, dbl, id, 1u);
+#endif
                 }
                 mma_commit(&empty[st]);
                 if (last) mma_commit(&tfull[b]);
