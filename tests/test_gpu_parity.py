@@ -453,3 +453,31 @@ def test_c1_tensor_core_dw_mode():
     # 3xTF32 products (~2e-7 of Σ|dz·x|) miss the strict bound on a few times more near-zero
     # entries than the exact-product SDDMM (measured 3.4e-4 vs 5.4e-5): an opt-in trade-off
     assert miss_tc < 1e-3
+
+
+def test_host_step_pipeline_matches_device_path():
+    """HostStep (pinned host buffers, overlapped copies, graphed passes) returns exactly what
+    the device-resident calls return."""
+    from paper_1702_08597_b200.pipeline import HostStep
+
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg, n=8)
+    ref = run_layer(img, w_f, go, 4, 1, dense=False)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    cache = layer.new_cache(8)
+    x, g = dev(np.zeros_like(img)), dev(np.zeros_like(go))
+    o = torch.empty((8, cfg.k, layer.ho, layer.wo), device="cuda")
+    dw = torch.empty((layer.nnz,), device="cuda")
+    di = torch.empty((8, cfg.c, cfg.h, cfg.w), device="cuda")
+    layer.forward(x, cache, out=o)
+    layer.backward_weights(g, cache, out=dw)
+    hs = HostStep(layer, cache, x, g, o, dw, di)
+    h = [torch.from_numpy(a).pin_memory() for a in (img, go)]
+    outs = [torch.empty(t.shape).pin_memory() for t in (o, dw, di)]
+    for _ in range(3):
+        hs(h[0], h[1], *outs)
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0].numpy(), ref["o"])
+    assert np.array_equal(outs[1].numpy(), ref["dw_raw"])
+    assert np.array_equal(outs[2].numpy(), ref["di"])
