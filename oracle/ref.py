@@ -198,3 +198,27 @@ def layer_fwd_bwd_batch(batch, w_f, grad_o, m=4, threads=None, n=None, want_outp
     _check(lib().wref_layer_fwd_bwd_batch(m, n, c, h_i, w_i, k, _ptr(batch), _ptr(w_f), _ptr(grad_o),
                                           C.c_uint(threads), _ptr(o), _ptr(gi), _ptr(gw)))
     return o, gi, gw
+
+
+def write_wgt1(path, arr, dtype="f64"):
+    arr = _c64(arr)
+    shape = np.array(arr.shape, dtype=np.int64)
+    _check(lib().wref_write_wgt1(str(path).encode(), _ptr(shape, _l), arr.ndim, _ptr(arr),
+                                 2 if dtype == "f32" else 1))
+
+
+def uniform_stream(seed, name, n):
+    out = np.zeros(n)
+    _check(lib().wref_uniform_stream(C.c_ulonglong(seed), name.encode(), C.c_long(n), _ptr(out)))
+    return out
+
+
+def threshold_to_density(w, density):
+    w = _c64(w).ravel().copy()
+    _check(lib().wref_threshold_to_density(_ptr(w), C.c_long(w.size), C.c_double(density)))
+    return w
+
+
+def checkpoint_roundtrip(dir_in, dir_out):
+    """The reference loads dir_in and saves what it loaded to dir_out."""
+    _check(lib().wref_checkpoint_roundtrip(str(dir_in).encode(), str(dir_out).encode()))

@@ -24,9 +24,14 @@
 #include <thread>
 #include <vector>
 
+#include <random>
+
+#include "wino/harness.hpp"
 #include "wino/layer.hpp"
 #include "wino/reference.hpp"
 #include "wino/sparse.hpp"
+#include "wino/tensor.hpp"
+#include "wino/train.hpp"
 #include "wino/transforms.hpp"
 
 using namespace wino;
@@ -284,6 +289,42 @@ int wref_layer_fwd_bwd_batch(int m, int n, int c, int h_i, int w_i, int k, const
                 for (std::size_t e = 0; e < wf_sz; ++e) grad_wf_sum[e] += partial[w][e];
         }
     })
+}
+
+// WGT1 I/O (tensor.cpp:166-216): dtype 1 = f64, 2 = f32
+int wref_write_wgt1(const char* path, const long* shape, int ndim, const double* data, int dtype) {
+    GUARD({
+        std::vector<std::size_t> sh(shape, shape + ndim);
+        std::size_t n = 1;
+        for (auto e : sh) n *= e;
+        Tensor t(sh, std::vector<double>(data, data + n));
+        write_wgt1(path, t, dtype == 2 ? Dtype::f32 : Dtype::f64);
+    })
+}
+
+// The reference's seeded inputs of infer-bench (tools/wino.cpp:338-343): mt19937_64 seeded with
+// train::stream_seed(seed, name), uniform_real_distribution<double>(-1, 1), n draws.
+int wref_uniform_stream(unsigned long long seed, const char* name, long n, double* out) {
+    GUARD({
+        std::mt19937_64 rng(train::stream_seed(seed, name));
+        std::uniform_real_distribution<double> dist(-1.0, 1.0);
+        for (long i = 0; i < n; ++i) out[i] = dist(rng);
+    })
+}
+
+// magnitude_threshold_to_density (train.cpp:419-429), in place on a flat f64 array
+int wref_threshold_to_density(double* w, long n, double density) {
+    GUARD({
+        Tensor t({(std::size_t)n}, std::vector<double>(w, w + n));
+        train::magnitude_threshold_to_density(t, density);
+        std::memcpy(w, t.data().data(), n * sizeof(double));
+    })
+}
+
+// harness::load_checkpoint then harness::save_checkpoint (harness.cpp:152-212): what the
+// reference makes of a checkpoint directory, written back out in its own format.
+int wref_checkpoint_roundtrip(const char* dir_in, const char* dir_out) {
+    GUARD({ harness::save_checkpoint(dir_out, harness::load_checkpoint(dir_in)); })
 }
 
 }  // extern "C"

@@ -69,7 +69,43 @@ def layer_case(name, m, n, c, k, h, w, pad, sparsity, seed):
         csr_nnz=np.array([len(x) for x in cols], dtype=np.int64))
 
 
+# infer-bench layers (name, c, k, h, m); the first two are the reference's own CLI test config
+# (tests/cli_smoke.cpp:127-128), the third exercises F(4x4,3x3)
+BENCH_LAYERS = [("convA", 8, 8, 16, 2), ("convB", 4, 4, 12, 2), ("convC", 8, 16, 10, 4)]
+BENCH_BATCH, BENCH_SEED, BENCH_DENSITIES = 2, 1, (0.25, 1.0)
+STREAM_CASES = [(1, "bench/convA", 700), (0, "", 5), ((1 << 63) + 5, "init/conv1", 320)]
+
+
+def io_and_bench():
+    """WGT1 files written by the reference writer, its seeded uniform streams, its magnitude
+    threshold, and infer-bench checksums of its f32 sparse_forward on its own inputs."""
+    ref.write_wgt1(OUT / "ref_f64.wgt", np.array([[1.0, -2.5, 0.0], [1e300, -1e-300, 3.14159]]))
+    ref.write_wgt1(OUT / "ref_f32.wgt", np.arange(8, dtype=np.float64).reshape(4, 1, 2) * 0.5 - 1.0,
+                   dtype="f32")
+    g = {}
+    for seed, name, n in STREAM_CASES:
+        g[f"stream_{seed}_{name.replace('/', '_')}"] = ref.uniform_stream(seed, name, n)
+    tw = np.round(ref.uniform_stream(3, "ties", 60) * 4) / 4  # many equal magnitudes
+    g["thr_in"] = tw
+    for x in (0.0, 0.3, 0.5, 0.99, 1.0):
+        g[f"thr_{x}"] = ref.threshold_to_density(tw, x)
+    for name, c, k, h, m in BENCH_LAYERS:
+        hi, p = h + 2, m + 2
+        nb = BENCH_BATCH * c * hi * hi
+        v = ref.uniform_stream(BENCH_SEED, "bench/" + name, nb + k * c * p * p)
+        batch, w_f = v[:nb].reshape(BENCH_BATCH, c, hi, hi), v[nb:].reshape(k, c, p, p)
+        for x in BENCH_DENSITIES:
+            w = ref.threshold_to_density(w_f, x).reshape(w_f.shape)
+            out = ref.sparse_forward(batch, w, m=m, workers=1, precision=32)
+            cs = 0.0
+            for val in out.ravel():  # the reference CLI's checksum loop
+                cs += float(val)
+            g[f"bench_{name}_{x}"] = np.float64(cs)
+    np.savez_compressed(OUT / "io_bench.npz", **g)
+
+
 def main():
+    io_and_bench()
     tr = {}
     for m in (2, 3, 4, 6):
         a, b, g = ref.transforms(m)
