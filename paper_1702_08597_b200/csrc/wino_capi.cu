@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/wino_cuda.h"
+#include "wino_compress.cuh"
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
 #include "wino_tmap.h"
@@ -166,6 +167,14 @@ struct wino_plan {
     int* d_perm = nullptr;
     int2* d_cv = nullptr;   // CSR (col, value bits) interleaved, the SpMM operand stream
     int2* d_cvT = nullptr;  // CSC (row, value bits) interleaved
+    // capacities (elements) of the buffers above, in declaration order: reused across weight sets
+    size_t cap_rowptr = 0, cap_colidx = 0, cap_rowof = 0, cap_vals = 0, cap_colptr = 0, cap_rowidx = 0,
+           cap_perm = 0, cap_cv = 0, cap_cvT = 0;
+    // device compress scratch: the f64 weights, line counts, CSR position map
+    double* d_wsrc = nullptr;
+    int* d_cnt = nullptr;
+    int* d_pos = nullptr;
+    size_t cap_wsrc = 0, cap_cnt = 0, cap_pos = 0;
     std::vector<int> h_rowptr, h_colptr;  // kept for launch partitioning
     int sddmm_rows = 0, sddmm_r = 0, sddmm_stages = 1, sddmm_maxb = 8;
     int64_t sddmm_max_nb = 0;
@@ -231,7 +240,17 @@ void free_weights(wino_plan* p) {
     p->d_rowptr = p->d_colidx = p->d_rowof = p->d_colptr = p->d_rowidx = p->d_perm = nullptr;
     p->d_vals = p->d_wdense = nullptr;
     p->d_cv = p->d_cvT = nullptr;
+    p->cap_rowptr = p->cap_colidx = p->cap_rowof = p->cap_vals = p->cap_colptr = p->cap_rowidx = p->cap_perm =
+        p->cap_cv = p->cap_cvT = 0;
     p->has_weights = false;
+}
+
+void free_compress_scratch(wino_plan* p) {
+    for (void* ptr : {(void*)p->d_wsrc, (void*)p->d_cnt, (void*)p->d_pos})
+        if (ptr) cudaFree(ptr);
+    p->d_wsrc = nullptr;
+    p->d_cnt = p->d_pos = nullptr;
+    p->cap_wsrc = p->cap_cnt = p->cap_pos = 0;
 }
 
 // Launch bracket: counts launches and, when profiling, records events on the stream.
@@ -284,6 +303,19 @@ void set_smem_attr(K kernel, int bytes) {
 int grid_for(int64_t work, int threads, int sm_count) {
     int64_t b = (work + threads - 1) / threads;
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sm_count * 16));
+}
+
+// typed capacity-based (re)allocation: keeps a buffer while it is large enough
+template <typename T>
+int grow(T** buf, size_t* cap, size_t need) {
+    need = std::max<size_t>(need, 1);
+    if (*buf && *cap >= need) return WINO_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(buf), need * sizeof(T)));
+    *cap = need;
+    return WINO_OK;
 }
 
 int ensure(float** buf, size_t* cap, size_t need) {
@@ -685,6 +717,91 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     return WINO_OK;
 }
 
+// compress<float> on the device (wino_compress.cuh): W_F f64 is copied to HBM once, CSR + CSC +
+// position map are built there; only the two pointer arrays come back (launch partitioning).
+// keep_all = 1 keeps every coordinate (the dense plan's full CSR).
+int device_compress(wino_plan* p, const double* w_host, double tol, int keep_all) {
+    const int K = p->K, C = p->C, P2 = p->P2;
+    const int64_t total = (int64_t)P2 * K * C;
+    if (total >= ((int64_t)1 << 31)) return set_err(WINO_CAPABILITY_ERROR, "more than 2^31 weight coordinates");
+    // buffers are reused in place: nothing still in flight may read the previous weights
+    CUDA_TRY(cudaDeviceSynchronize());
+    p->has_weights = false;
+    p->tc_ready = false;
+    int rc;
+    if ((rc = grow(&p->d_wsrc, &p->cap_wsrc, (size_t)total)) ||
+        (rc = grow(&p->d_cnt, &p->cap_cnt, (size_t)P2 * std::max(K, C))) ||
+        (rc = grow(&p->d_rowptr, &p->cap_rowptr, (size_t)P2 * (K + 1))) ||
+        (rc = grow(&p->d_colptr, &p->cap_colptr, (size_t)P2 * (C + 1))) ||
+        (rc = grow(&p->d_pos, &p->cap_pos, (size_t)total)))
+        return rc;
+    CUDA_TRY(cudaMemcpy(p->d_wsrc, w_host, (size_t)total * sizeof(double), cudaMemcpyHostToDevice));
+    const cudaStream_t st = 0;
+    constexpr int TH = 128;
+    auto blocks = [](int64_t n) { return (int)std::max<int64_t>(1, (n + TH - 1) / TH); };
+    {
+        Launch L(p, st, K_MISC);
+        wino::compress_count_kernel<false><<<blocks((int64_t)K * P2), TH, 0, st>>>(p->d_wsrc, K, C, P2, tol, keep_all,
+                                                                                  p->d_cnt);
+        if ((rc = L.done())) return rc;
+    }
+    {
+        Launch L(p, st, K_MISC);
+        wino::compress_scan_kernel<<<1, 1024, 0, st>>>(p->d_cnt, P2, K, p->d_rowptr);
+        if ((rc = L.done())) return rc;
+    }
+    {
+        Launch L(p, st, K_MISC);
+        wino::compress_count_kernel<true><<<blocks((int64_t)C * P2), TH, 0, st>>>(p->d_wsrc, K, C, P2, tol, keep_all,
+                                                                                 p->d_cnt);
+        if ((rc = L.done())) return rc;
+    }
+    {
+        Launch L(p, st, K_MISC);
+        wino::compress_scan_kernel<<<1, 1024, 0, st>>>(p->d_cnt, P2, C, p->d_colptr);
+        if ((rc = L.done())) return rc;
+    }
+    std::vector<int> rowptr((size_t)P2 * (K + 1)), colptr((size_t)P2 * (C + 1));
+    CUDA_TRY(cudaMemcpy(rowptr.data(), p->d_rowptr, rowptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(colptr.data(), p->d_colptr, colptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    const int64_t nnz = rowptr.back();
+    if ((rc = grow(&p->d_colidx, &p->cap_colidx, (size_t)nnz)) || (rc = grow(&p->d_vals, &p->cap_vals, (size_t)nnz)) ||
+        (rc = grow(&p->d_rowof, &p->cap_rowof, (size_t)nnz)) || (rc = grow(&p->d_cv, &p->cap_cv, (size_t)nnz)) ||
+        (rc = grow(&p->d_rowidx, &p->cap_rowidx, (size_t)nnz)) || (rc = grow(&p->d_perm, &p->cap_perm, (size_t)nnz)) ||
+        (rc = grow(&p->d_cvT, &p->cap_cvT, (size_t)nnz)))
+        return rc;
+    if (nnz > 0) {
+        {
+            Launch L(p, st, K_MISC);
+            wino::compress_fill_rows_kernel<<<blocks((int64_t)K * P2), TH, 0, st>>>(
+                p->d_wsrc, K, C, P2, tol, keep_all, p->d_rowptr, p->d_colidx, p->d_vals, p->d_rowof, p->d_cv, p->d_pos);
+            if ((rc = L.done())) return rc;
+        }
+        {
+            Launch L(p, st, K_MISC);
+            wino::compress_fill_cols_kernel<<<blocks((int64_t)C * P2), TH, 0, st>>>(
+                p->d_wsrc, K, C, P2, tol, keep_all, p->d_colptr, p->d_pos, p->d_rowidx, p->d_perm, p->d_cvT);
+            if ((rc = L.done())) return rc;
+        }
+    }
+    p->slice_nnz.resize(P2);
+    p->slice_off.resize(P2);
+    for (int s = 0; s < P2; ++s) {
+        p->slice_off[s] = rowptr[(size_t)s * (K + 1)];
+        p->slice_nnz[s] = rowptr[(size_t)s * (K + 1) + K] - p->slice_off[s];
+    }
+    if (!p->d_slice_off) CUDA_TRY(cudaMalloc(&p->d_slice_off, P2 * sizeof(int64_t)));
+    CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaDeviceSynchronize());
+    p->h_rowptr = std::move(rowptr);
+    p->h_colptr = std::move(colptr);
+    p->nnz = nnz;
+    p->has_weights = true;
+    p->dense = false;
+    plan_sddmm(p);
+    return WINO_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -789,6 +906,7 @@ int wino_plan_destroy(wino_plan* p) {
     };
     chk(cudaGetLastError(), "pending error before destroy");
     free_weights(p);
+    free_compress_scratch(p);
     chk(cudaGetLastError(), "free_weights");
     if (p->d_dwc) chk(cudaFree(p->d_dwc), "d_dwc");
     if (p->d_z) chk(cudaFree(p->d_z), "d_z");
@@ -860,61 +978,18 @@ int wino_set_weights_csr(wino_plan* p, const uint64_t* const* row_ptr, const uin
 
 int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense) {
     if (!p || !w_f) return set_err(WINO_INVALID_ARGUMENT, "null argument");
-    const int K = p->K, C = p->C, P = p->p, P2 = p->P2;
+    if (dense < 0 || dense > 3) return set_err(WINO_INVALID_ARGUMENT, "dense must be 0..3");
     CUDA_TRY(cudaSetDevice(p->device));
-    if (dense) {  // every coordinate is a weight (zeros included): full CSR
-        std::vector<int> rowptr((size_t)P2 * (K + 1)), col((size_t)P2 * K * C);
-        std::vector<float> val((size_t)P2 * K * C);
-        for (int s = 0; s < P2; ++s) {
-            for (int k = 0; k <= K; ++k) rowptr[(size_t)s * (K + 1) + k] = (int)((int64_t)s * K * C + (int64_t)k * C);
-            for (int k = 0; k < K; ++k)
-                for (int c = 0; c < C; ++c) {
-                    const size_t e = ((size_t)s * K + k) * C + c;
-                    col[e] = c;
-                    val[e] = (float)w_f[((size_t)k * C + c) * P2 + s];
-                }
-        }
-        free_weights(p);
-        p->slice_nnz.assign(P2, (int64_t)K * C);
-        p->slice_off.resize(P2);
-        for (int s = 0; s < P2; ++s) p->slice_off[s] = (int64_t)s * K * C;
-        int rc = upload_csr(p, rowptr, col, val);
-        p->dense = true;
-        p->tc_fast = dense == 3;
-        if (rc == WINO_OK && dense >= 2) {
-            rc = refresh_tc_operands(p, nullptr);
-            if (rc == WINO_OK) CUDA_TRY(cudaDeviceSynchronize());
-        }
-        return rc;
+    // dense != 0: every coordinate is a weight (zeros included): the full CSR
+    int rc = device_compress(p, w_f, zero_tol, dense ? 1 : 0);
+    if (rc != WINO_OK || !dense) return rc;
+    p->dense = true;
+    p->tc_fast = dense == 3;
+    if (dense >= 2) {
+        rc = refresh_tc_operands(p, nullptr);
+        if (rc == WINO_OK) CUDA_TRY(cudaDeviceSynchronize());
     }
-    // compress<float> (sparse.cpp:9-36): slices (i,j) row-major, rows k, columns c ascending
-    std::vector<std::vector<uint64_t>> rps(P2), cols(P2);
-    std::vector<std::vector<float>> vals(P2);
-    std::vector<uint64_t> nnz(P2);
-    for (int i = 0; i < P; ++i)
-        for (int j = 0; j < P; ++j) {
-            const int s = i * P + j;
-            rps[s].assign(K + 1, 0);
-            for (int k = 0; k < K; ++k) {
-                for (int c = 0; c < C; ++c) {
-                    const double v = w_f[((size_t)k * C + c) * P2 + s];
-                    if (std::abs(v) > zero_tol || (zero_tol == 0.0 && v != 0.0)) {
-                        cols[s].push_back((uint64_t)c);
-                        vals[s].push_back((float)v);
-                    }
-                }
-                rps[s][k + 1] = vals[s].size();
-            }
-            nnz[s] = vals[s].size();
-        }
-    std::vector<const uint64_t*> prp(P2), pcol(P2);
-    std::vector<const float*> pval(P2);
-    for (int s = 0; s < P2; ++s) {
-        prp[s] = rps[s].data();
-        pcol[s] = cols[s].data();
-        pval[s] = vals[s].data();
-    }
-    return wino_set_weights_csr(p, prp.data(), pcol.data(), pval.data(), nnz.data());
+    return rc;
 }
 
 int wino_get_csr(const wino_plan* p, uint64_t* nnz, uint64_t* row_ptr, uint64_t* col_idx, float* values) {
