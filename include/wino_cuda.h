@@ -141,12 +141,35 @@ WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, co
  * WINO_CONSISTENCY_ERROR if backward_weights has not run on this cache. */
 WINO_API int wino_backward_input(wino_plan* plan, const wino_cache* cache, float* grad_input, void* stream);
 
-/* Masked SGD on the live CSR values (train.cpp:281-290 with a fixed mask: only surviving
- * coordinates exist in the CSR, so masked ones are never touched):
- *   v -= lr · (scale·g + l2·v/‖v‖₂)   (l2 = 0 skips the norm, train.cpp:219-229),
- * then refreshes the CSC copy. grad is nnz-compact (device). */
+/* The weight update of train_step (train.cpp:210-290), on the live weights, in fp64 on the
+ * fp32 values.  Per coordinate of the plan (a sparse plan holds only unmasked coordinates, so
+ * frozen zeros are never touched — train.cpp:280):
+ *   g = scale·grad;  reg = λ·sign(w) (norm 1) | λ·w/‖w‖₂ (norm 2, 0 when ‖w‖ = 0)
+ *   v = w − lr·(g + reg);  prune && λ > 0: v = 0 when |v|·(|g| + β) < ε  (train.cpp:108-110)
+ * grad is in the layout backward_weights wrote (nnz-compact, or K×C×p×q for a dense plan).
+ * Non-finite results are counted on the device (wino_update_status).  Asynchronous on
+ * `stream`, capturable in a CUDA graph; refreshes the CSC copy and tensor-core operands. */
+typedef struct wino_update {
+    double lr;     /* the layer's learning rate (lr · wino_lr_mult for Winograd layers) */
+    double scale;  /* gradient scale: 1/B for a Σ over B images (train.cpp:166) */
+    double lambda; /* regularisation factor; 0 = none */
+    double eps;    /* gradient-threshold ε (PruneConfig::eps) */
+    double beta;   /* gradient-threshold β (PruneConfig::beta) */
+    int norm;      /* 1 or 2 (fine-tuning uses 2, train.cpp:262) */
+    int prune;     /* apply the threshold (StepMode::prune) */
+} wino_update;
+WINO_API int wino_update_weights(wino_plan* plan, const float* grad_w, const wino_update* update,
+                                 void* stream);
+/* Masked SGD (the fine-tune step): wino_update_weights with norm 2, λ = l2, no threshold. */
 WINO_API int wino_sgd_step(wino_plan* plan, const float* grad_w, float lr, float scale, float l2,
                   void* stream);
+/* Synchronizes; *nonfinite = non-finite updated weights since the last call (then reset).
+ * A nonzero count is the reference's TrainingError "divergence" (train.cpp:288). */
+WINO_API int wino_update_status(wino_plan* plan, int64_t* nonfinite);
+/* Re-derive the CSR from the plan's current weights on the device, exactly as compress
+ * (sparse.cpp:9-36) of those weights would: a dense plan after pruning steps becomes the sparse
+ * plan of its surviving coordinates (set_masks_from_zeros + fine-tune, train.cpp:322-338). */
+WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
 
 /* Plan options.
  *   WINO_OPT_DW_MODE: how the sparse plan computes dW_F on the mask (layer.cpp:118-128):

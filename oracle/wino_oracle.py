@@ -477,6 +477,30 @@ def layer_f32(batch, csr: Csr, grad_o=None, m=4, pad=0):
     return res
 
 
+def train_update_f64(w, g, lr, scale=1.0, lmbda=0.0, norm=1, prune=False, eps=0.0, beta=0.0):
+    """The per-coordinate update of train_step (train.cpp:255-290) on the coordinates given
+    (a sparse plan's values, or all of a dense layer's), in the reference's f64 expression order:
+    reg_grad (train.cpp:213-218; λ·w/‖w‖₂ with ‖w‖ over the given values, l2_norm
+    train.cpp:220-224), v = w − lr·(g + reg) (train.cpp:284), threshold_value
+    (train.cpp:108-110, applied in prune mode when λ > 0, train.cpp:285-286).
+    Returns (new values rounded to f32, number of non-finite results)."""
+    w = np.asarray(w, dtype=np.float64)
+    g = scale * np.asarray(g, dtype=np.float64)
+    if lmbda == 0.0:
+        reg = np.zeros_like(w)
+    elif norm == 1:
+        reg = np.where(w > 0, lmbda, np.where(w < 0, -lmbda, 0.0))
+    else:
+        nrm = np.sqrt(np.sum(w * w))
+        reg = (lmbda * w) / nrm if nrm > 0 else np.zeros_like(w)
+    with np.errstate(over="ignore", invalid="ignore"):
+        v = w - lr * (g + reg)
+        if prune and lmbda > 0:
+            v = np.where(np.abs(v) * (np.abs(g) + beta) < eps, 0.0, v)
+        f = v.astype(np.float32)
+    return f, int(np.count_nonzero(~np.isfinite(f)))
+
+
 def flops_baseline(c, k, h, r=3):
     """perfmodel.cpp:6-9: 2·C·K·H²·r² per image and pass (the 'effective FLOP' numerator)."""
     return 2.0 * c * k * h * h * r * r

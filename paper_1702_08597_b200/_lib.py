@@ -51,6 +51,10 @@ class InvalidArgument(WinoError, ValueError):
     code = 6
 
 
+class TrainingError(RuntimeError):
+    """wino::train::TrainingError (train.hpp) — a non-finite update ("divergence")."""
+
+
 _BY_CODE = {cls.code: cls for cls in (ShapeError, ConsistencyError, CorruptFormatError,
                                       CapabilityError, CudaError, InvalidArgument)}
 
@@ -63,6 +67,13 @@ class Geometry(C.Structure):
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class Update(C.Structure):
+    """wino_update (include/wino_cuda.h)."""
+
+    _fields_ = [("lr", C.c_double), ("scale", C.c_double), ("lmbda", C.c_double), ("eps", C.c_double),
+                ("beta", C.c_double), ("norm", C.c_int), ("prune", C.c_int)]
 
 
 class LayerDesc(C.Structure):
@@ -97,7 +108,10 @@ SIGNATURES = {
     "wino_forward": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_weights": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_input": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "wino_update_weights": (C.c_int, [_vp, _vp, C.POINTER(Update), _vp]),
     "wino_sgd_step": (C.c_int, [_vp, _vp, C.c_float, C.c_float, C.c_float, _vp]),
+    "wino_update_status": (C.c_int, [_vp, _pi64]),
+    "wino_recompress": (C.c_int, [_vp, C.c_double]),
     "wino_set_option": (C.c_int, [_vp, C.c_int, C.c_int]),
     "wino_launch_count": (C.c_int64, [_vp]),
     "wino_reset_launch_count": (None, [_vp]),

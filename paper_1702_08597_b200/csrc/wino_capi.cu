@@ -16,6 +16,7 @@
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
 #include "wino_tmap.h"
+#include "wino_update.cuh"
 
 namespace {
 
@@ -175,6 +176,10 @@ struct wino_plan {
     int* d_cnt = nullptr;
     int* d_pos = nullptr;
     size_t cap_wsrc = 0, cap_cnt = 0, cap_pos = 0;
+    // weight update: Σw² partials, non-finite counter
+    double* d_sumsq_part = nullptr;
+    size_t cap_sumsq_part = 0;
+    unsigned long long* d_nonfinite = nullptr;
     std::vector<int> h_rowptr, h_colptr;  // kept for launch partitioning
     int sddmm_rows = 0, sddmm_r = 0, sddmm_stages = 1, sddmm_maxb = 8;
     int64_t sddmm_max_nb = 0;
@@ -246,11 +251,14 @@ void free_weights(wino_plan* p) {
 }
 
 void free_compress_scratch(wino_plan* p) {
-    for (void* ptr : {(void*)p->d_wsrc, (void*)p->d_cnt, (void*)p->d_pos})
+    for (void* ptr : {(void*)p->d_wsrc, (void*)p->d_cnt, (void*)p->d_pos, (void*)p->d_sumsq_part,
+                      (void*)p->d_nonfinite})
         if (ptr) cudaFree(ptr);
     p->d_wsrc = nullptr;
     p->d_cnt = p->d_pos = nullptr;
-    p->cap_wsrc = p->cap_cnt = p->cap_pos = 0;
+    p->d_sumsq_part = nullptr;
+    p->d_nonfinite = nullptr;
+    p->cap_wsrc = p->cap_cnt = p->cap_pos = p->cap_sumsq_part = 0;
 }
 
 // Launch bracket: counts launches and, when profiling, records events on the stream.
@@ -720,22 +728,31 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
 // compress<float> on the device (wino_compress.cuh): W_F f64 is copied to HBM once, CSR + CSC +
 // position map are built there; only the two pointer arrays come back (launch partitioning).
 // keep_all = 1 keeps every coordinate (the dense plan's full CSR).
+int compress_from_wsrc(wino_plan* p, double tol, int keep_all);
+
 int device_compress(wino_plan* p, const double* w_host, double tol, int keep_all) {
-    const int K = p->K, C = p->C, P2 = p->P2;
-    const int64_t total = (int64_t)P2 * K * C;
+    const int64_t total = (int64_t)p->P2 * p->K * p->C;
     if (total >= ((int64_t)1 << 31)) return set_err(WINO_CAPABILITY_ERROR, "more than 2^31 weight coordinates");
     // buffers are reused in place: nothing still in flight may read the previous weights
     CUDA_TRY(cudaDeviceSynchronize());
+    int rc = grow(&p->d_wsrc, &p->cap_wsrc, (size_t)total);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(p->d_wsrc, w_host, (size_t)total * sizeof(double), cudaMemcpyHostToDevice));
+    return compress_from_wsrc(p, tol, keep_all);
+}
+
+// compress of the K×C×p×q f64 weights already in p->d_wsrc (device-synchronous)
+int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
+    const int K = p->K, C = p->C, P2 = p->P2;
+    const int64_t total = (int64_t)P2 * K * C;
     p->has_weights = false;
     p->tc_ready = false;
     int rc;
-    if ((rc = grow(&p->d_wsrc, &p->cap_wsrc, (size_t)total)) ||
-        (rc = grow(&p->d_cnt, &p->cap_cnt, (size_t)P2 * std::max(K, C))) ||
+    if ((rc = grow(&p->d_cnt, &p->cap_cnt, (size_t)P2 * std::max(K, C))) ||
         (rc = grow(&p->d_rowptr, &p->cap_rowptr, (size_t)P2 * (K + 1))) ||
         (rc = grow(&p->d_colptr, &p->cap_colptr, (size_t)P2 * (C + 1))) ||
         (rc = grow(&p->d_pos, &p->cap_pos, (size_t)total)))
         return rc;
-    CUDA_TRY(cudaMemcpy(p->d_wsrc, w_host, (size_t)total * sizeof(double), cudaMemcpyHostToDevice));
     const cudaStream_t st = 0;
     constexpr int TH = 128;
     auto blocks = [](int64_t n) { return (int)std::max<int64_t>(1, (n + TH - 1) / TH); };
@@ -890,6 +907,8 @@ int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
     if (e == cudaSuccess)
         e = cudaDeviceGetAttribute(&p->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_scalar, sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_nonfinite, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(p->d_nonfinite, 0, sizeof(unsigned long long));
     if (e != cudaSuccess) {
         delete p;
         return set_err(WINO_CUDA_ERROR, std::string("plan_create: ") + cudaGetErrorString(e));
@@ -1152,30 +1171,63 @@ int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, vo
     return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
 }
 
-int wino_sgd_step(wino_plan* p, const float* grad_w, float lr, float scale, float l2, void* stream) {
+int wino_update_weights(wino_plan* p, const float* grad_w, const wino_update* u, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
-    if (!grad_w) return set_err(WINO_INVALID_ARGUMENT, "null gradient");
+    if (!grad_w || !u) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (u->norm != 1 && u->norm != 2) return set_err(WINO_INVALID_ARGUMENT, "norm must be 1 or 2");
+    if (p->nnz == 0) return WINO_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    float* vals = p->d_vals;
-    float l2n = 0.f;
-    if (l2 != 0.f) {
-        {
-            Launch L(p, st, K_SGD);
-            wino::sumsq_kernel<<<1, 1024, 0, st>>>(vals, p->nnz, p->d_scalar);
-            if ((rc = L.done())) return rc;
-        }
-        double ss = 0.0;
-        CUDA_TRY(cudaMemcpyAsync(&ss, p->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        l2n = ss > 0.0 ? (float)(l2 / std::sqrt(ss)) : 0.f;
+    wino::UpdateParams up{u->lr, u->scale, u->lambda, u->eps, u->beta, u->norm, u->prune};
+    if (u->norm == 2 && u->lambda != 0.0) {  // ‖w‖₂ of the layer before the step (train.cpp:264)
+        const int parts = std::min<int64_t>(4 * p->sm_count, (p->nnz + 1023) / 1024);
+        if ((rc = grow(&p->d_sumsq_part, &p->cap_sumsq_part, (size_t)parts))) return rc;
+        Launch L(p, st, K_SGD);
+        wino::sumsq_partial_kernel<<<parts, 1024, 0, st>>>(p->d_vals, p->nnz, p->d_sumsq_part);
+        wino::sumsq_final_kernel<<<1, 1024, 0, st>>>(p->d_sumsq_part, parts, p->d_scalar);
+        ++p->launches;
+        if ((rc = L.done())) return rc;
     }
     {
         Launch L(p, st, K_SGD);
-        wino::sgd_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(vals, grad_w, p->nnz, lr, scale, l2n);
+        wino::update_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
+            p->d_vals, grad_w, p->nnz, p->dense ? 1 : 0, p->K, p->C, p->P2, up, p->d_scalar, p->d_nonfinite);
         if ((rc = L.done())) return rc;
     }
     return wino_values_updated(p, stream);
+}
+
+int wino_sgd_step(wino_plan* p, const float* grad_w, float lr, float scale, float l2, void* stream) {
+    const wino_update u{lr, scale, l2, 0.0, 0.0, 2, 0};
+    return wino_update_weights(p, grad_w, &u, stream);
+}
+
+int wino_update_status(wino_plan* p, int64_t* nonfinite) {
+    if (!p || !nonfinite) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    unsigned long long n = 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(&n, p->d_nonfinite, sizeof(n), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemset(p->d_nonfinite, 0, sizeof(n)));
+    *nonfinite = (int64_t)n;
+    return WINO_OK;
+}
+
+int wino_recompress(wino_plan* p, double zero_tol) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    const int K = p->K, C = p->C, P2 = p->P2;
+    const int64_t total = (int64_t)P2 * K * C;
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    if ((rc = grow(&p->d_wsrc, &p->cap_wsrc, (size_t)total))) return rc;
+    CUDA_TRY(cudaMemset(p->d_wsrc, 0, (size_t)total * sizeof(double)));
+    if (p->nnz > 0) {
+        Launch L(p, 0, K_MISC);
+        wino::csr_to_kcpq_f64_kernel<<<grid_for((int64_t)K * P2, 128, p->sm_count), 128>>>(
+            p->d_rowptr, p->d_colidx, p->d_vals, K, C, P2, p->d_wsrc);
+        if ((rc = L.done())) return rc;
+    }
+    return compress_from_wsrc(p, zero_tol, 0);
 }
 
 int wino_set_option(wino_plan* p, int option, int value) {

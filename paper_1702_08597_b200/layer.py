@@ -263,7 +263,32 @@ class WinogradLayer:
         return out
 
     def sgd_step(self, grad_w, lr: float, scale: float = 1.0, l2: float = 0.0, stream=None):
+        """Masked SGD (fine-tune): update(norm=2, lmbda=l2)."""
         check(lib().wino_sgd_step(self._h, _dptr(grad_w), lr, scale, l2, _stream_ptr(stream)))
+
+    def update(self, grad_w, lr: float, scale: float = 1.0, lmbda: float = 0.0, norm: int = 1,
+               prune: bool = False, eps: float = 0.0, beta: float = 0.0, stream=None):
+        """train_step's per-layer update (train.cpp:255-290): regulariser λ‖w‖_norm, SGD, and in
+        prune mode the gradient threshold |v|·(|g|+β) < ε → 0.  Asynchronous; divergence is
+        reported by check_finite()."""
+        u = _lib.Update(lr, scale, lmbda, eps, beta, norm, int(bool(prune)))
+        check(lib().wino_update_weights(self._h, _dptr(grad_w), C.byref(u), _stream_ptr(stream)))
+
+    def check_finite(self, name: str = "winograd layer"):
+        """Raise TrainingError if an update since the last check produced a non-finite weight."""
+        n = C.c_int64()
+        check(lib().wino_update_status(self._h, C.byref(n)))
+        if n.value:
+            raise _lib.TrainingError(f"train_step: divergence in {name} ({n.value} non-finite weights)")
+
+    def recompress(self, zero_tol: float = 0.0):
+        """Re-derive the CSR from the live weights (compress of them, on the device): after
+        pruning steps the plan keeps only the surviving coordinates (set_masks_from_zeros)."""
+        check(lib().wino_recompress(self._h, zero_tol))
+
+    def weights(self) -> np.ndarray:
+        """The live weights as K×C×p×q f64 (zeros off the CSR)."""
+        return reconstruct(self.get_csr())
 
     # -- instrumentation ------------------------------------------------------------
     def launch_count(self) -> int:

@@ -18,8 +18,10 @@ from .layer import WinogradLayer
 
 
 class WinogradStack:
-    def __init__(self, weights, c, h, w, pad=1, m=4, device=0, n_max=1):
-        """weights: list of K×C×p×p W_F arrays (exact zeros = pruned)."""
+    def __init__(self, weights, c, h, w, pad=1, m=4, device=0, n_max=1, dense=False):
+        """weights: list of K×C×p×p W_F arrays.  dense=False: exact zeros are pruned (masked)
+        coordinates — the fine-tune network.  dense=True: every coordinate is trainable — the
+        pruning phase (StepMode::prune); prune_to_sparse() then keeps the survivors."""
         import torch
 
         self.device = device
@@ -29,15 +31,19 @@ class WinogradStack:
         for w_f in weights:
             w_f = np.asarray(w_f)
             lay = WinogradLayer(cin, w_f.shape[0], h, w, pad=pad, m=m, device=device)
-            lay.set_weights(w_f, dense=False)
+            lay.set_weights(w_f, dense=dense if isinstance(dense, str) else bool(dense))
             self.layers.append(lay)
             self.caches.append(lay.new_cache(n_max))
             cin = w_f.shape[0]
             h, w = lay.ho, lay.wo
-        self.bucket = GradBucket.allocate([lay.nnz for lay in self.layers], device=f"cuda:{device}")
+        self._alloc_bucket()
         self.n_max = n_max
         self.outs = [None] * len(self.layers)
         self._torch = torch
+
+    def _alloc_bucket(self):
+        self.bucket = GradBucket.allocate([lay.nnz for lay in self.layers], device=f"cuda:{self.device}")
+        self.grads = [v.view(lay.grad_w_shape()) for v, lay in zip(self.bucket.views, self.layers)]
 
     def forward(self, x):
         """run_forward (train.cpp:66-87): conv -> ReLU for every layer; returns the last output."""
@@ -54,19 +60,46 @@ class WinogradStack:
         g = grad_out
         for i in range(len(self.layers) - 1, -1, -1):
             lay, cache = self.layers[i], self.caches[i]
-            lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.bucket.views[i])
+            lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.grads[i])
             if i > 0:
                 g = lay.backward_input(cache)
         return self.bucket
 
-    def step(self, x, grad_out, lr, n_global, l2=0.0, group=None):
+    def step(self, x, grad_out, lr, n_global, l2=0.0, group=None, mode=None, lmbda=0.0, norm=1,
+             eps=0.0, beta=0.0):
         """One data-parallel training step: forward, backward, ONE all-reduce of the bucket,
-        masked SGD with the 1/B scaling of train.cpp:166,200."""
+        then the update of train_step (train.cpp:255-290) with the 1/B scaling of
+        train.cpp:166,200.  mode=None: masked SGD with L2 factor l2 (the fine-tune step).
+        'prune': λ‖w‖_norm regulariser + the gradient threshold (ε, β).  'finetune': λ‖w‖₂.
+        'train': λ‖w‖_norm without threshold."""
         self.forward(x)
         self.backward(grad_out)
         self.bucket.allreduce(group)
-        for lay, g in zip(self.layers, self.bucket.views):
-            lay.sgd_step(g, lr=lr, scale=1.0 / float(n_global), l2=l2)
+        scale = 1.0 / float(n_global)
+        for lay, g in zip(self.layers, self.grads):
+            if mode is None:
+                lay.sgd_step(g, lr=lr, scale=scale, l2=l2)
+            elif mode in ("prune", "finetune", "train"):
+                lay.update(g, lr=lr, scale=scale, lmbda=lmbda, norm=2 if mode == "finetune" else norm,
+                           prune=mode == "prune", eps=eps, beta=beta)
+            else:
+                raise ValueError(f"unknown mode {mode!r}")
+
+    def check_finite(self):
+        """TrainingError if any layer's update diverged since the last check (synchronizes)."""
+        for i, lay in enumerate(self.layers):
+            lay.check_finite(f"conv{i + 1}")
+
+    def prune_to_sparse(self, zero_tol=0.0):
+        """After the pruning phase: every layer keeps only its nonzero coordinates (the masks of
+        set_masks_from_zeros, train.cpp:322-330), re-derived on the device; the gradient
+        bucket shrinks to the new nnz."""
+        for lay in self.layers:
+            lay.recompress(zero_tol)
+        self._alloc_bucket()
+
+    def densities(self):
+        return [lay.nnz / float(lay.k * lay.c * lay.p * lay.p) for lay in self.layers]
 
     def launch_count(self):
         return sum(lay.launch_count() for lay in self.layers)

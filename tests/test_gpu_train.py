@@ -1,0 +1,157 @@
+"""The batched training step's weight update on the GPU, through the C-ABI:
+prune-mode steps (L1 regulariser + gradient threshold) on dense plans, the on-device
+re-derivation of the CSR (bit-exact with the reference's compress), fine-tune steps (L2) on
+the sparse plans, and divergence detection — each checked against oracle.train_update_f64,
+the restatement of train.cpp:255-290, applied to the same fp32 weights and gradients."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ref
+from oracle import wino_oracle as wo
+import paper_1702_08597_b200 as wb
+from paper_1702_08597_b200.stack import WinogradStack
+from paper_1702_08597_b200.synth import CONFIGS, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def _weights(stack):
+    return [lay.weights() for lay in stack.layers]
+
+
+def _grads(stack):
+    out = []
+    for lay, g in zip(stack.layers, stack.grads):
+        g = g.cpu().numpy().astype(np.float64)
+        out.append(g if lay.is_dense else lay.compact_to_dense(g))
+    return out
+
+
+def _stack(dense):
+    cfg = CONFIGS["c0"]
+    img, w1, go = make_inputs(cfg, n=3)
+    rng = np.random.default_rng(5)
+    w1 = (rng.standard_normal(w1.shape) * 0.2).astype(np.float32).astype(np.float64)
+    w2 = (rng.standard_normal(w1.shape) * 0.2).astype(np.float32).astype(np.float64)
+    st = WinogradStack([w1, w2], cfg.c, cfg.h, cfg.w, pad=1, m=4, n_max=3, dense=dense)
+    return st, dev(img), dev(go * 1e-3)  # small gradients: |g| << β, so the threshold bites
+
+
+@pytest.mark.parametrize("dense", [True, "exact"])
+def test_prune_steps_then_recompress_then_finetune(dense):
+    st, x, go = _stack(dense)
+    lam, eps, beta, lr = 0.02, 2e-3, 0.05, 0.05
+    for step in range(3):
+        w0 = _weights(st)
+        st.step(x, go, lr=lr, n_global=3, mode="prune", lmbda=lam, norm=1, eps=eps, beta=beta)
+        torch.cuda.synchronize()
+        g = _grads(st)
+        for lay, w_before, gr, w_after in zip(st.layers, w0, g, _weights(st)):
+            want, bad = wo.train_update_f64(w_before.ravel(), gr.ravel(), lr, 1.0 / 3, lam, 1, True, eps, beta)
+            assert bad == 0
+            # norm 1 involves no reduction: the update is bit-exact
+            assert np.array_equal(w_after.ravel().astype(np.float32), want), f"step {step}"
+    st.check_finite()
+    dens = [np.count_nonzero(w) / w.size for w in _weights(st)]
+    assert all(0.0 < d < 1.0 for d in dens), dens  # the threshold pruned something
+    assert st.densities() == [1.0, 1.0]  # ... but a dense plan still holds every coordinate
+    # set_masks_from_zeros + compress, on the device: equal to the reference's compress<float>
+    wts = _weights(st)
+    st.prune_to_sparse()
+    assert st.densities() == pytest.approx(dens)
+    for lay, w in zip(st.layers, wts):
+        assert not lay.is_dense
+        rp, cols, vals = ref.compress_f32(w)
+        csr = lay.get_csr()
+        for s in range(lay.p * lay.p):
+            assert np.array_equal(csr.row_ptr[s].astype(np.int64), rp[s])
+            assert np.array_equal(csr.col_idx[s].astype(np.int64), cols[s])
+            assert np.array_equal(csr.values[s], vals[s])
+    # fine-tune: L2 regulariser on the survivors, masked coordinates stay exactly zero
+    w0 = _weights(st)
+    st.step(x, go, lr=lr, n_global=3, mode="finetune", lmbda=0.01)
+    torch.cuda.synchronize()
+    for lay, w_before, g in zip(st.layers, w0, st.grads):
+        vals0 = np.concatenate(wb.compress(w_before).values)
+        want, _ = wo.train_update_f64(vals0, g.cpu().numpy(), lr, 1.0 / 3, 0.01, 2)
+        got = np.concatenate(lay.get_csr().values)
+        # ‖w‖₂ is reduced in a different order than numpy's: at most one fp32 ulp apart
+        assert np.max(np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))) <= 1
+        assert np.all(lay.weights()[w_before == 0] == 0)
+
+
+def test_update_matches_oracle_sparse_l2_and_plain():
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=2)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f)
+    cache = layer.new_cache(2)
+    layer.forward(dev(img), cache)
+    g = layer.backward_weights(dev(go), cache)
+    gh = g.cpu().numpy()
+    for kw in ({"lmbda": 0.0}, {"lmbda": 0.3, "norm": 1}, {"lmbda": 0.3, "norm": 2},
+               {"lmbda": 0.3, "norm": 1, "prune": True, "eps": 1e-3, "beta": 0.2}):
+        v0 = np.concatenate(layer.get_csr().values)
+        layer.update(g, lr=0.01, scale=0.5, **kw)
+        torch.cuda.synchronize()
+        want, _ = wo.train_update_f64(v0, gh, 0.01, 0.5, kw.get("lmbda", 0.0), kw.get("norm", 1),
+                                      kw.get("prune", False), kw.get("eps", 0.0), kw.get("beta", 0.0))
+        got = np.concatenate(layer.get_csr().values)
+        ulp = np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
+        assert ulp.max() <= (1 if kw.get("norm") == 2 else 0), kw
+    layer.check_finite()
+
+
+def test_divergence_raises_training_error():
+    cfg = CONFIGS["c0"]
+    _, w_f, _ = make_inputs(cfg, n=1)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f)
+    g = torch.full((layer.nnz,), float("nan"), device="cuda")
+    layer.update(g, lr=0.1)
+    with pytest.raises(wb._lib.TrainingError):
+        layer.check_finite()
+    layer.check_finite()  # the counter was reset
+    layer.set_weights(w_f)
+    big = torch.full((layer.nnz,), 3e38, device="cuda")
+    layer.update(big, lr=10.0)  # finite in f64, beyond fp32
+    with pytest.raises(wb._lib.TrainingError):
+        layer.check_finite()
+
+
+def test_dense_plan_sgd_uses_kcpq_gradient_layout():
+    """A dense plan's gradient is K×C×p×q (what backward_weights returns); the update must pair
+    it with the right coordinates."""
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=1)
+    rng = np.random.default_rng(1)
+    w_f = rng.standard_normal(w_f.shape).astype(np.float32).astype(np.float64)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense="exact")
+    g = rng.standard_normal(w_f.shape).astype(np.float32)
+    layer.sgd_step(dev(g), lr=0.1)
+    torch.cuda.synchronize()
+    lr = float(np.float32(0.1))  # wino_sgd_step takes fp32 scalars
+    np.testing.assert_array_equal(layer.weights().astype(np.float32),
+                                  (w_f - lr * g.astype(np.float64)).astype(np.float32))
+
+
+def test_recompress_with_tolerance_matches_compress():
+    cfg = CONFIGS["c0"]
+    _, w_f, _ = make_inputs(cfg, n=1)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=True)
+    layer.recompress(zero_tol=0.05)
+    rp, cols, vals = ref.compress_f32(w_f.astype(np.float32).astype(np.float64), zero_tol=0.05)
+    csr = layer.get_csr()
+    assert layer.nnz == sum(len(c) for c in cols)
+    for s in range(layer.p * layer.p):
+        assert np.array_equal(csr.col_idx[s].astype(np.int64), cols[s])
+        assert np.array_equal(csr.values[s], vals[s])
