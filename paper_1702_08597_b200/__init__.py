@@ -7,6 +7,8 @@ the reference's interfaces:
     compress / reconstruct / PointwiseCsr -- sparse.hpp:19-49
     gen_transforms, lift, conv_winograd, conv_winograd_grad, sparse_conv, density
                                    -- python/bindings.cpp:55-204
+    autograd.WinogradConv2d        -- the same layer as a differentiable torch module
+    io, infer_bench                -- WGT1 / checkpoints, the infer-bench CSV driver
 """
 from ._lib import (CapabilityError, ConsistencyError, CorruptFormatError, CudaError, ShapeError,
                    WinoError)

@@ -210,6 +210,11 @@ class WinogradLayer:
         check(lib().wino_weight_values(self._h, C.byref(ptr)))
         return ptr.value
 
+    def values_updated(self, stream=None):
+        """The values behind weight_values() were modified in place: refresh the derived
+        operands (CSC copy, tensor-core splits)."""
+        check(lib().wino_values_updated(self._h, _stream_ptr(stream)))
+
     # -- passes ---------------------------------------------------------------------
     def new_cache(self, n_max: int) -> ForwardCache:
         return ForwardCache(self, n_max)

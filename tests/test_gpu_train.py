@@ -155,3 +155,71 @@ def test_recompress_with_tolerance_matches_compress():
     for s in range(layer.p * layer.p):
         assert np.array_equal(csr.col_idx[s].astype(np.int64), cols[s])
         assert np.array_equal(csr.values[s], vals[s])
+
+
+# -- the torch operator surface ---------------------------------------------
+@pytest.mark.parametrize("dense", [False, "exact", True])
+def test_winograd_conv2d_module_matches_torch_conv2d(dense):
+    """W_F = lift(w): the module is conv2d(x, w, padding=1); its gradients chain back to the
+    spatial kernel as dL/dw = Gᵀ·dL/dW_F·G (f64 torch reference, fp32 tolerance)."""
+    from paper_1702_08597_b200.autograd import WinogradConv2d
+
+    rng = np.random.default_rng(7)
+    n, c, k, h = 2, 8, 12, 10
+    w = rng.standard_normal((k, c, 3, 3)) * 0.3
+    w_f = wb.lift(w, m=4).astype(np.float32).astype(np.float64)
+    if dense is False:
+        w_f[np.abs(w_f) < 0.15] = 0.0  # a pruned W_F is no longer a lifted kernel: compare to itself
+    mod = WinogradConv2d(w_f, h, h, pad=1, m=4, dense=dense)
+    x = torch.tensor(rng.standard_normal((n, c, h, h)), dtype=torch.float32, device="cuda", requires_grad=True)
+    out = mod(x)
+    go = torch.tensor(rng.standard_normal(out.shape), dtype=torch.float32, device="cuda")
+    out.backward(go)
+    _, _, g = wb.transforms(4)
+    if dense is not False:
+        xr = x.detach().double().cpu().requires_grad_(True)
+        wr = torch.tensor(w, requires_grad=True)
+        ref_out = torch.nn.functional.conv2d(xr, wr, padding=1)
+        ref_out.backward(go.double().cpu())
+        np.testing.assert_allclose(out.detach().cpu().numpy(), ref_out.detach().numpy(), rtol=1e-4, atol=1e-4)
+        np.testing.assert_allclose(x.grad.cpu().numpy(), xr.grad.numpy(), rtol=1e-4, atol=1e-4)
+        dwf = mod.values.grad.double().cpu().numpy().reshape(6, 6, k, c).transpose(2, 3, 0, 1)
+        dw = np.einsum("iu,kcij,jv->kcuv", g, dwf, g)
+        np.testing.assert_allclose(dw, wr.grad.numpy(), rtol=1e-4, atol=1e-3)
+    else:
+        lay = wb.WinogradLayer(c, k, h, h, pad=1, m=4)
+        lay.set_weights(w_f)
+        cache = lay.new_cache(n)
+        o2 = lay.forward(x.detach(), cache)
+        assert torch.equal(out, o2)
+        dw2 = lay.backward_weights(go, cache)
+        dx2 = lay.backward_input(cache)
+        assert torch.equal(mod.values.grad, dw2) and torch.equal(x.grad, dx2)
+
+
+def test_winograd_conv2d_optimizer_updates_live_weights():
+    from paper_1702_08597_b200.autograd import WinogradConv2d
+
+    rng = np.random.default_rng(3)
+    w_f = rng.standard_normal((8, 4, 6, 6)).astype(np.float32).astype(np.float64)
+    w_f[np.abs(w_f) < 0.7] = 0.0
+    mod = WinogradConv2d(w_f, 9, 9, pad=1, m=4, relu=True)
+    opt = torch.optim.SGD(mod.parameters(), lr=0.05)
+    x = torch.tensor(rng.standard_normal((3, 4, 9, 9)), dtype=torch.float32, device="cuda")
+    before = mod.weight()
+    loss = mod(x).square().sum()
+    loss.backward()
+    g = mod.values.grad.clone()
+    opt.step()
+    after = mod.weight()
+    assert np.all(after[w_f == 0] == 0)  # pruned coordinates do not exist in the parameter
+    v0 = np.concatenate(wb.compress(before).values)
+    want = (v0.astype(np.float64) - np.float64(np.float32(0.05)) * g.cpu().numpy()).astype(np.float32)
+    got = np.concatenate(wb.compress(after).values)
+    # torch's fp32 add_(alpha) may fuse: within one fp32 ulp of the exact update
+    assert np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64)).max() <= 1
+    # the next forward sees the update (CSC / operands refreshed): compare with a fresh layer
+    out = mod(x)
+    lay = wb.WinogradLayer(4, 8, 9, 9, pad=1, m=4)
+    lay.set_weights(after)
+    assert torch.equal(out, lay.forward(x, relu=True))
