@@ -176,7 +176,12 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *     0 (default) masked SDDMM — exact fp64 products and accumulation of the fp32 operands;
  *     1 tensor cores — the accurate 3xTF32 tcgen05 GEMM over all K×C (per-k-block fp64
  *       folding, ~2e-7 of Σ|dz·x|), then the surviving entries gathered in CSR order.
- *       Faster whenever the density is above a few percent; requires C, K multiples of 4. */
+ *       Faster whenever the density is above a few percent; requires C, K multiples of 4.
+ *     2 precise — the forward also stores the fp32 residual of Ĩ_F (and backward_weights that of
+ *       dZ), each recomputed in fp64 with the reference's coefficients; the SDDMM forms
+ *       zh·xh + zh·xl + zl·xh exactly in fp64, so dW_F matches the reference's f64 layer on
+ *       every element (no fp32-storage floor).  ~2× the SDDMM time and 2× the cache memory;
+ *       caches created before the switch allocate their residual buffers on first use. */
 #define WINO_OPT_DW_MODE 1
 WINO_API int wino_set_option(wino_plan* plan, int option, int value);
 

@@ -15,6 +15,7 @@
 #include "wino_compress.cuh"
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
+#include "wino_precise.cuh"
 #include "wino_tmap.h"
 #include "wino_update.cuh"
 
@@ -154,6 +155,7 @@ struct wino_plan {
     int C = 0, K = 0, H = 0, W = 0, pad = 0, m = 0, r = 0, p = 0, P2 = 0;
     wino_geometry g{};
     wino::Coefs cf{};
+    wino::CoefsD cfd{};  // the same transform in the reference's doubles (precise dW mode)
     bool has_weights = false, dense = false;
     bool builtin = false;  // coefficients equal a built-in set: compile-time-constant kernels
     int64_t nnz = 0;
@@ -222,6 +224,8 @@ struct wino_cache {
     int64_t NTs = 0;
     float* V = nullptr;
     float* DZ = nullptr;
+    float* Vlo = nullptr;   // precise dW mode: fp32 residuals of Ĩ_F and dZ
+    float* DZlo = nullptr;
     bool has_fwd = false;
     bool has_grad_z = false;
 };
@@ -417,9 +421,10 @@ void plan_sddmm(wino_plan* p) {
     const int64_t budget = std::min(p->max_smem, 210 * 1024);
     struct Opt { int r, stages; };
     const char* renv = std::getenv("WINO_SDDMM_R");
-    for (Opt o : {Opt{4, 1}, Opt{2, 2}, Opt{1, 2}}) {
+    for (Opt o : {Opt{4, 1}, Opt{2, 2}, Opt{2, 1}, Opt{1, 2}}) {
         if (renv && std::atoi(renv) != o.r) continue;
-        const int64_t per_row = (int64_t)o.stages * 32 * o.r * 4;
+        if (o.r == 2 && o.stages == 1 && p->dw_mode != 2) continue;  // precise mode only (R=1 LO spills)
+        const int64_t per_row = (int64_t)o.stages * 32 * o.r * 4 * (p->dw_mode == 2 ? 2 : 1);
         const int64_t cap_rows = budget / per_row - p->C;
         if (cap_rows < 8) continue;
         const char* env = std::getenv("WINO_SDDMM_MAXB");
@@ -442,23 +447,26 @@ void plan_sddmm(wino_plan* p) {
     p->sddmm_r = 0;  // no feasible variant: launch reports CAPABILITY
 }
 
-template <int R, int MAXB, int STAGES>
+template <int R, int MAXB, int STAGES, bool LO>
 void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
-                    const float* V, float* dW, double* partial, int NT, int NTs, int tps) {
+                    const float* V, const float* DZlo, const float* Vlo, float* dW, double* partial, int NT,
+                    int NTs, int tps) {
     constexpr int TH = kSddmmWarps * 32;
     static_assert(TH <= 1024, "block too large");
-    set_smem_attr(wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH>, (int)smem);
-    wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH><<<grid, TH, smem, st>>>(
-        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NT, NTs, p->sddmm_rows,
-        tps);
+    set_smem_attr(wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH, LO>, (int)smem);
+    wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH, LO><<<grid, TH, smem, st>>>(
+        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, DZlo, Vlo, dW, partial, p->nnz, p->K, p->C, NT, NTs,
+        p->sddmm_rows, tps);
 }
 
 int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
-                 int64_t NTs) {
+                 int64_t NTs, const float* DZlo = nullptr, const float* Vlo = nullptr) {
     if (p->nnz == 0) return WINO_OK;
     if (p->sddmm_r == 0) return set_err(WINO_CAPABILITY_ERROR, "sddmm: no variant fits this layer");
+    const bool lo = Vlo != nullptr;
+    if (lo != (p->dw_mode == 2)) return set_err(WINO_CONSISTENCY_ERROR, "sddmm: plan/precision mismatch");
     const int R = p->sddmm_r, TW = 32 * R;
-    const size_t smem = (size_t)p->sddmm_stages * (p->C + p->sddmm_rows) * TW * 4;
+    const size_t smem = (size_t)p->sddmm_stages * (p->C + p->sddmm_rows) * TW * 4 * (lo ? 2 : 1);
     const int groups = (p->K + p->sddmm_rows - 1) / p->sddmm_rows;
     const int chunks = (int)((NT + TW - 1) / TW);
     const int64_t base = (int64_t)groups * p->P2;
@@ -481,10 +489,17 @@ int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
     {
         Launch L(p, st, K_SDDMM);
 #define SDDMM_CASE(RR, MB, SS)                                                                   \
-    if (p->sddmm_r == RR && p->sddmm_maxb == MB && p->sddmm_stages == SS)                        \
-        launch_sddmm_v<RR, MB, SS>(grid, smem, st, p, DZ, V, dW, partial, (int)NT, (int)NTs, tps);
+    if (p->sddmm_r == RR && p->sddmm_maxb == MB && p->sddmm_stages == SS) {                      \
+        if (lo)                                                                                  \
+            launch_sddmm_v<RR, MB, SS, true>(grid, smem, st, p, DZ, V, DZlo, Vlo, dW, partial, (int)NT, \
+                                             (int)NTs, tps);                                     \
+        else                                                                                     \
+            launch_sddmm_v<RR, MB, SS, false>(grid, smem, st, p, DZ, V, nullptr, nullptr, dW, partial,  \
+                                              (int)NT, (int)NTs, tps);                           \
+    }
         SDDMM_CASE(4, 4, 1) SDDMM_CASE(4, 8, 1) SDDMM_CASE(4, 16, 1)
         SDDMM_CASE(2, 4, 2) SDDMM_CASE(2, 8, 2) SDDMM_CASE(2, 16, 2)
+        SDDMM_CASE(2, 4, 1) SDDMM_CASE(2, 8, 1) SDDMM_CASE(2, 16, 1)
         SDDMM_CASE(1, 4, 2) SDDMM_CASE(1, 8, 2) SDDMM_CASE(1, 16, 2)
 #undef SDDMM_CASE
         int rc = L.done();
@@ -533,6 +548,34 @@ int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* r
         wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t,
                                                                (int)NT, (int)NTs);
+    return L.done();
+}
+
+// precise dW mode: the fp32 residuals of Ĩ_F (after K1) and of dZ (after K4)
+template <int M, int P, class CF>
+int launch_input_lo(wino_plan* p, cudaStream_t st, const float* in, const float* V, float* Vlo, int64_t NT,
+                    int64_t NTs) {
+    const wino_geometry& g = p->g;
+    Launch L(p, st, K_INPUT);
+    wino::input_transform_lo_kernel<M, P><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
+        in, V, Vlo, p->cfd, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
+    return L.done();
+}
+
+template <int M, int P, class CF>
+int launch_grad_z_lo(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, const float* DZ,
+                     float* DZlo, int64_t NT, int64_t NTs, bool mask) {
+    const wino_geometry& g = p->g;
+    Launch L(p, st, K_GRADZ);
+    const int grid = grid_for((int64_t)p->K * NTs, 256, p->sm_count);
+    if (mask)
+        wino::grad_z_lo_kernel<M, P, true><<<grid, 256, 0, st>>>(dO, relu, DZ, DZlo, p->cfd, p->K, (int)g.h_o,
+                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT,
+                                                                (int)NTs);
+    else
+        wino::grad_z_lo_kernel<M, P, false><<<grid, 256, 0, st>>>(dO, relu, DZ, DZlo, p->cfd, p->K, (int)g.h_o,
+                                                                 (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT,
+                                                                 (int)NTs);
     return L.done();
 }
 
@@ -891,8 +934,8 @@ int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
         delete p;
         return rc;
     }
-    for (int i = 0; i < p->p * p->m; ++i) p->cf.a[i] = (float)a[i];
-    for (int i = 0; i < p->p * p->p; ++i) p->cf.b[i] = (float)b[i];
+    for (int i = 0; i < p->p * p->m; ++i) p->cf.a[i] = (float)(p->cfd.a[i] = a[i]);
+    for (int i = 0; i < p->p * p->p; ++i) p->cf.b[i] = (float)(p->cfd.b[i] = b[i]);
     auto same = [&](const float* ta, const float* tb) {
         return std::memcmp(p->cf.a, ta, sizeof(float) * p->p * p->m) == 0 &&
                std::memcmp(p->cf.b, tb, sizeof(float) * p->p * p->p) == 0;
@@ -1054,6 +1097,14 @@ int wino_values_updated(wino_plan* p, void* stream) {
     return rc;
 }
 
+static int ensure_cache_lo(wino_plan* p, wino_cache* c) {
+    if (c->Vlo) return WINO_OK;
+    const int64_t NTs = round_up((int64_t)c->n_max * p->g.t, 4);
+    CUDA_TRY(cudaMalloc(&c->Vlo, (size_t)p->P2 * p->C * NTs * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&c->DZlo, (size_t)p->P2 * p->K * NTs * sizeof(float)));
+    return WINO_OK;
+}
+
 int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
     if (!p || !out || n_max <= 0) return set_err(WINO_INVALID_ARGUMENT, "bad argument");
     CUDA_TRY(cudaSetDevice(p->device));
@@ -1068,6 +1119,13 @@ int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
         delete c;
         return set_err(WINO_CUDA_ERROR, std::string("cache_create: ") + cudaGetErrorString(e));
     }
+    if (p->dw_mode == 2) {
+        const int rc = ensure_cache_lo(p, c);
+        if (rc) {
+            wino_cache_destroy(c);
+            return rc;
+        }
+    }
     *out = c;
     return WINO_OK;
 }
@@ -1076,6 +1134,8 @@ int wino_cache_destroy(wino_cache* c) {
     if (!c) return WINO_OK;
     if (c->V) cudaFree(c->V);
     if (c->DZ) cudaFree(c->DZ);
+    if (c->Vlo) cudaFree(c->Vlo);
+    if (c->DZlo) cudaFree(c->DZlo);
     delete c;
     return WINO_OK;
 }
@@ -1101,6 +1161,10 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0)))
         return rc;
+    if (cache && p->dw_mode == 2) {
+        if ((rc = ensure_cache_lo(p, cache))) return rc;
+        if ((rc = DISPATCH_MP(p, launch_input_lo, p, st, input, V, cache->Vlo, NT, NTs))) return rc;
+    }
     if (p->dense && p->tc_ready)
         rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
     else
@@ -1129,7 +1193,13 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask))) return rc;
-    if (p->dense && p->tc_ready) {
+    const bool precise = p->dw_mode == 2;
+    if (precise) {
+        if (!c->Vlo) return set_err(WINO_CONSISTENCY_ERROR, "precise dW: run the forward with this mode set");
+        if ((rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask)))
+            return rc;
+    }
+    if (p->dense && p->tc_ready && !precise) {
         if ((rc = launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs))) return rc;  // tensor cores (opt-in)
     } else {
         float* dwc = grad_w;
@@ -1137,6 +1207,8 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
         if (p->dense) dwc = p->d_dwc;
         if (!p->dense && p->dw_mode == 1 && p->nnz > 0)
             rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
+        else if (precise)
+            rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
         else
             rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs);
         if (rc) return rc;
@@ -1232,7 +1304,7 @@ int wino_recompress(wino_plan* p, double zero_tol) {
 
 int wino_set_option(wino_plan* p, int option, int value) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
-    if (option != WINO_OPT_DW_MODE || value < 0 || value > 1)
+    if (option != WINO_OPT_DW_MODE || value < 0 || value > 2)
         return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
     if (value == 1) {
         if (p->C % 4 || p->K % 4)
@@ -1242,7 +1314,9 @@ int wino_set_option(wino_plan* p, int option, int value) {
             CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), p->P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
         }
     }
+    const bool replan = (value == 2) != (p->dw_mode == 2);
     p->dw_mode = value;
+    if (replan && p->has_weights) plan_sddmm(p);  // the precise variant stages twice the rows
     return WINO_OK;
 }
 

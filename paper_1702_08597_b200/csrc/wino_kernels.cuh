@@ -568,11 +568,15 @@ __device__ __forceinline__ void transpose_reduce16(double (&v)[16], int lane) {
     v[0] += __shfl_xor_sync(kFull, v[0], 16);
 }
 
-template <int R, int MAXB, int STAGES, int BATCH, int THREADS>
+// LO (the precise mode): Ĩ_F and dZ also carry their fp32 residuals (Ĩ_F ≈ V + Vlo,
+// dZ ≈ DZ + DZlo to ~2^-48, wino_precise.cuh); each term is zh·xh + zh·xl + zl·xh with exact
+// fp64 products, so dW_F reaches the accuracy of the reference's f64 layer itself.
+template <int R, int MAXB, int STAGES, int BATCH, int THREADS, bool LO>
 __global__ void __launch_bounds__(THREADS)
 sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
              const int* __restrict__ rowof, const float* __restrict__ DZ,
-             const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
+             const float* __restrict__ V, const float* __restrict__ DZlo, const float* __restrict__ Vlo,
+             float* __restrict__ dW, double* __restrict__ partial,
              int64_t nnz_total, int K, int C, int NT, int NTs, int rows_per_block, int t_per_split) {
     constexpr int TW = 32 * R;
     extern __shared__ float4 smem_f4[];
@@ -585,10 +589,13 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
     const int nb = e1 - e0;
     const int tb = blockIdx.z * t_per_split;
     const int te = min(NT, tb + t_per_split);
-    const int stage_floats = (C + nrb) * TW;
+    const int hi_floats = (C + nrb) * TW;  // [Ĩ_F rows C][dZ rows nrb] × TW (then the lo copy)
+    const int stage_floats = hi_floats * (LO ? 2 : 1);
     float* st0 = reinterpret_cast<float*>(smem_f4);
     const float* vg = V + (int64_t)s * C * NTs;
     const float* zg = DZ + ((int64_t)s * K + r0) * NTs;
+    const float* vlg = LO ? Vlo + (int64_t)s * C * NTs : nullptr;
+    const float* zlg = LO ? DZlo + ((int64_t)s * K + r0) * NTs : nullptr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 
     // per nonzero: (row offset, col offset) into the staged chunk, in units of R floats
@@ -605,6 +612,10 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
         float* vs = st0 + buf * stage_floats;
         stage_rows_async<TW>(vg, vs, C, NTs, t0);
         stage_rows_async<TW>(zg, vs + C * TW, nrb, NTs, t0);
+        if constexpr (LO) {
+            stage_rows_async<TW>(vlg, vs + hi_floats, C, NTs, t0);
+            stage_rows_async<TW>(zlg, vs + hi_floats + C * TW, nrb, NTs, t0);
+        }
         cp_async_commit();
     };
     if (STAGES == 2 && tb < te) stage(0, tb);
@@ -629,6 +640,7 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
             if ((warp + i * nw) * BATCH >= nb) break;  // warp-uniform
             double part[BATCH];
             double zd[R];
+            double zl[LO ? R : 1];
             int rprev = -1;
 #pragma unroll
             for (int j = 0; j < BATCH; ++j) {
@@ -639,6 +651,11 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                     lds_vec<R>(base + ro * R, z);
 #pragma unroll
                     for (int qq = 0; qq < R; ++qq) zd[qq] = (double)z[qq];
+                    if constexpr (LO) {
+                        lds_vec<R>(base + hi_floats + ro * R, z);
+#pragma unroll
+                        for (int qq = 0; qq < R; ++qq) zl[qq] = (double)z[qq];
+                    }
                     rprev = ro;
                 }
                 float x[R];
@@ -646,6 +663,12 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                 double pr = zd[0] * (double)x[0];  // exact: fp32×fp32 fits fp64
 #pragma unroll
                 for (int qq = 1; qq < R; ++qq) pr = fma(zd[qq], (double)x[qq], pr);
+                if constexpr (LO) {
+                    float xl[R];
+                    lds_vec<R>(base + hi_floats + (q & 0xffff) * R, xl);
+#pragma unroll
+                    for (int qq = 0; qq < R; ++qq) pr = fma(zd[qq], (double)xl[qq], fma(zl[qq], (double)x[qq], pr));
+                }
                 part[j] = pr;
             }
             if constexpr (BATCH == 32)

@@ -201,8 +201,10 @@ class WinogradLayer:
                             [val[offs[s]:offs[s + 1]].copy() for s in range(n)])
 
     def set_dw_mode(self, mode: str):
-        """'sddmm' (default: exact masked SDDMM) or 'tc' (tensor-core GEMM + mask gather)."""
-        check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE, {"sddmm": 0, "tc": 1}[mode]))
+        """'sddmm' (default: exact products of the fp32 operands), 'tc' (tensor-core GEMM + mask
+        gather) or 'precise' (operands carried as fp32 hi+lo pairs: the reference's f64 dW_F)."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE,
+                                    {"sddmm": 0, "tc": 1, "precise": 2}[mode]))
 
     def weight_values(self):
         """Device pointer (int) of the live CSR values (nnz floats)."""

@@ -32,11 +32,13 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
 
 
-def run_layer(img, w_f, grad_o, m, pad, dense=None):
+def run_layer(img, w_f, grad_o, m, pad, dense=None, dw_mode=None):
     n, c, h, w = img.shape
     k = w_f.shape[0]
     layer = wb.WinogradLayer(c, k, h, w, pad=pad, m=m)
     layer.set_weights(w_f, dense=dense)
+    if dw_mode is not None:
+        layer.set_dw_mode(dw_mode)
     cache = layer.new_cache(n)
     o = layer.forward(dev(img), cache)
     out = {"layer": layer, "o": o.cpu().numpy()}
@@ -252,6 +254,37 @@ def test_c1_full_batch_parity():
     assert not np.any(got_bad & ~floor_bad), "dW_F misses the tolerance where the fp32 floor does not"
     assert got_bad.mean() <= 1e-4, f"strict-tolerance misses {got_bad.mean():.2e}"
     # and bitwise against the f32 mirror (reference association order) for the forward
+    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
+    assert np.array_equal(r["o"], mir["o"])
+
+
+@pytest.mark.parametrize("name", LAYER_CASES)
+def test_precise_dw_mode_golden(name):
+    """WINO_OPT_DW_MODE=2: dW_F within the strict tolerance of the reference's f64 layer on
+    every element; O and dI unchanged (bitwise) by the mode."""
+    d = load_layer(name)
+    base = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False)
+    r = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False, dw_mode="precise")
+    assert np.array_equal(r["o"], base["o"]) and np.array_equal(r["di"], base["di"])
+    mask = d["w_f"] != 0
+    assert fail_fraction(r["dw"][mask], d["grad_wf_f64"][mask]) == 0.0
+    # far below the tolerance: the residual pairs carry the f64 operands to ~2^-48
+    err = np.abs(r["dw"][mask] - d["grad_wf_f64"][mask])
+    assert np.all(err <= 1e-6 * (1.0 + np.abs(d["grad_wf_f64"][mask])))
+
+
+def test_c1_precise_dw_strict_everywhere():
+    """configs[1] at full size in the precise dW mode: zero strict-tolerance misses (the fp32
+    floor of the default mode misses 19/353,647), and the fp32 forward path is unchanged."""
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg)
+    r = run_layer(img, w_f, go, 4, 1, dense=False, dw_mode="precise")
+    o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
+    assert_parity(r["o"], o, "c1 O")
+    assert_parity(r["di"], di, "c1 dI")
+    mask = w_f != 0
+    bad = np.abs(r["dw"][mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
+    assert int(bad.sum()) == 0, f"{int(bad.sum())} strict misses"
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(r["o"], mir["o"])
 
