@@ -34,6 +34,7 @@ sys.path.insert(0, str(ROOT))
 
 from paper_1702_08597_b200.synth import CONFIGS, make_inputs, with_sparsity  # noqa: E402
 
+METRIC_FWD = "Winograd layer fwd effective GFLOP/s"
 METRIC = "Winograd layer fwd+bwd effective GFLOP/s"
 
 
@@ -229,6 +230,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     layer.set_weights(w_f, dense=(args.dense or "tc") if dense else False)
     if args.dw == "tc" and not dense:
         layer.set_dw_mode("tc")
+    elif args.dw == "precise":
+        layer.set_dw_mode("precise")
+    if args.contraction == "tc" and not dense:
+        layer.set_contraction("tc")
     cache = layer.new_cache(n)
     x = torch.from_numpy(img).to(dev)
     g_o = torch.from_numpy(go).to(dev)
@@ -237,8 +242,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     di = torch.empty((n, cfg.c, cfg.h, cfg.w), device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
 
+    fwd_only = not cfg.backward  # c2: the reference's sparse inference pass
+
     def step():
         layer.forward(x, cache, out=out)
+        if fwd_only:
+            return
         layer.backward_weights(g_o, cache, out=dw)
         if world > 1:
             dist.all_reduce(dw)
@@ -284,7 +293,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    flops_step = 3 * flops_per_image(cfg) * n
+    passes = 1 if fwd_only else 3
+    flops_step = passes * flops_per_image(cfg) * n
     value = world * flops_step / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers (pinned) ----
@@ -294,7 +304,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
     h_dw = torch.empty(dw.shape, dtype=torch.float32).pin_memory()
     h_di = torch.empty(di.shape, dtype=torch.float32).pin_memory()
 
-    if world == 1 and not args.no_graph:
+    if fwd_only:
+        def e2e_step():
+            x.copy_(h_img, non_blocking=True)
+            run()
+            h_out.copy_(out, non_blocking=True)
+        e2e_mode = "serial copies + forward"
+    elif world == 1 and not args.no_graph:
         # public API: HostStep overlaps dO upload with the forward and the O / dW downloads
         # with the backward (paper_1702_08597_b200/pipeline.py)
         from paper_1702_08597_b200.pipeline import HostStep
@@ -330,8 +346,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = world * flops_step / (float(t2.item()) * 1e-3) / 1e9
-    h2d = h_img.numel() * 4 + h_go.numel() * 4
-    d2h = (h_out.numel() + h_dw.numel() + h_di.numel()) * 4
+    h2d = h_img.numel() * 4 + (0 if fwd_only else h_go.numel() * 4)
+    d2h = (h_out.numel() + (0 if fwd_only else h_dw.numel() + h_di.numel())) * 4
 
     if rank != 0:
         return
@@ -371,14 +387,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
                     "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
                              "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
     line = {
-        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC_FWD if fwd_only else METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
-        "config": {"workload": workload_name(cfg, "fwd+bwd"), "global_batch": n * world,
+        "config": {"workload": workload_name(cfg, "fwd" if fwd_only else "fwd+bwd"), "global_batch": n * world,
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
                    "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
-                             "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else "csr",
-                   "dw": "masked-sddmm-exact" if args.dw == "sddmm" else "tcgen05-3xtf32-fp64fold+mask-gather",
+                             "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else
+                           ("csr" if args.contraction == "csr" else "tcgen05-3xtf32-fp64fold on zero-filled W_F"),
+                   "dw": {"sddmm": "masked-sddmm-exact", "tc": "tcgen05-3xtf32-fp64fold+mask-gather",
+                          "precise": "masked-sddmm-exact on fp32 hi+lo operands"}[args.dw],
                    "l2_flush": "256 MB write between timed steps",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
@@ -390,7 +409,25 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "launch_mode": graph_note,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and fwd_only:
+        # the reference's sparse inference (compress + sparse_forward<float>, all host cores),
+        # best of 3 after a warm-up call (acceptance.cpp:313-320 style), on a sample of images
+        from oracle import ref
+
+        threads = os.cpu_count() or 1
+        n_img = min(n, 8)
+        imgp = np.pad(img[:n_img].astype(np.float64), ((0, 0), (0, 0), (cfg.pad, cfg.pad), (cfg.pad, cfg.pad)))
+        ref.sparse_forward(imgp[:1], w_f, m=cfg.m, workers=threads, precision=32)
+        best = float("inf")
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref.sparse_forward(imgp, w_f, m=cfg.m, workers=threads, precision=32)
+            best = min(best, time.perf_counter() - t0)
+        line["cpu_baseline"] = {"value": flops_per_image(cfg) * n_img / best / 1e9, "unit": "GFLOP/s",
+                                "cores": threads, "kind": "reference",
+                                "sample": f"{n_img} of {cfg.n} images through the reference's "
+                                          "compress + sparse_forward<float>, best of 3"}
+    elif world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n_img = cpu_sample_size(cfg, threads)
         t, kind = cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads)
@@ -529,7 +566,9 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
-    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc"],
+    ap.add_argument("--contraction", default="csr", choices=["csr", "tc"],
+                    help="sparse plan: CSR kernels (bitwise reference order) or tcgen05 on zero-filled W_F")
+    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise"],
                     help="sparse dW_F: exact masked SDDMM (default) or tensor-core GEMM + mask gather")
     ap.add_argument("--dense", default=None, choices=["tc", "tc-fast", "exact"],
                     help="dense path at 0%% sparsity: 'tc' (default: 3xTF32 tcgen05, per-k-block fp64 "

@@ -183,6 +183,15 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *       every element (no fp32-storage floor).  ~2× the SDDMM time and 2× the cache memory;
  *       caches created before the switch allocate their residual buffers on first use. */
 #define WINO_OPT_DW_MODE 1
+/*   WINO_OPT_CONTRACTION: how a sparse plan runs Z = W_F·Ĩ_F and dĨ_F = W_Fᵀ·dZ:
+ *     0 (default) the CSR kernels — the reference's association order, forward bitwise equal
+ *       to sparse_forward<float>;
+ *     1 tensor cores — the 3xTF32 tcgen05 GEMM (per-k-block fp64 folding) over the zero-filled
+ *       W_F slices; fp32-level accuracy (within the north_star tolerance, not bitwise), faster
+ *       than the SIMT CSR kernels above ~5-10% density.  Masked coordinates stay exactly zero
+ *       (the operands are re-scattered from the CSR values on every update).
+ *       Requires C, K multiples of 4.  dW_F still follows WINO_OPT_DW_MODE. */
+#define WINO_OPT_CONTRACTION 2
 WINO_API int wino_set_option(wino_plan* plan, int option, int value);
 
 /* ---------------------------------------------------------------------------- */

@@ -197,7 +197,8 @@ struct wino_plan {
     CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
     bool tc_ready = false;
     bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
-    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather
+    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather, 2 = precise
+    int contraction = 0;   // sparse plan: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
     int64_t* d_slice_off = nullptr;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
@@ -630,7 +631,18 @@ int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
             return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the weight operands (CUresult " +
                                                 std::to_string(wino::last_tmap_error()) + ")");
     }
-    wino::split_tf32_kernel<<<grid_for(n, 256, p->sm_count), 256, 0, st>>>(p->d_vals, p->d_wh, p->d_wl, p->d_wth,
+    const float* src = p->d_vals;  // dense plan: the full CSR is W[s][k][c]
+    if (!p->dense) {               // sparse plan: scatter the CSR into a zero-filled W[s][k][c]
+        if (!p->d_wdense) CUDA_TRY(cudaMalloc(&p->d_wdense, n * 4));
+        CUDA_TRY(cudaMemsetAsync(p->d_wdense, 0, n * 4, st));
+        if (p->nnz > 0) {
+            wino::csr_scatter_dense_kernel<<<grid_for((int64_t)p->K * p->P2, 128, p->sm_count), 128, 0, st>>>(
+                p->d_rowptr, p->d_colidx, p->d_vals, p->K, p->C, p->P2, p->d_wdense);
+            ++p->launches;
+        }
+        src = p->d_wdense;
+    }
+    wino::split_tf32_kernel<<<grid_for(n, 256, p->sm_count), 256, 0, st>>>(src, p->d_wh, p->d_wl, p->d_wth,
                                                                            p->d_wtl, p->K, p->C, p->P2);
     ++p->launches;
     CUDA_TRY(cudaGetLastError());
@@ -765,6 +777,11 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     p->has_weights = true;
     p->dense = false;
     plan_sddmm(p);
+    if (p->contraction == 1) {
+        const int rc2 = refresh_tc_operands(p, nullptr);
+        if (rc2) return rc2;
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
     return WINO_OK;
 }
 
@@ -859,6 +876,11 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     p->has_weights = true;
     p->dense = false;
     plan_sddmm(p);
+    if (p->contraction == 1) {
+        const int rc2 = refresh_tc_operands(p, nullptr);
+        if (rc2) return rc2;
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
     return WINO_OK;
 }
 
@@ -1093,7 +1115,7 @@ int wino_values_updated(wino_plan* p, void* stream) {
     wino::refresh_values_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_cv, p->d_cvT, p->d_vals,
                                                                                    p->d_perm, p->nnz);
     rc = L.done();
-    if (rc == WINO_OK && p->dense && p->tc_ready) rc = refresh_tc_operands(p, st);
+    if (rc == WINO_OK && p->tc_ready) rc = refresh_tc_operands(p, st);
     return rc;
 }
 
@@ -1165,7 +1187,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         if ((rc = ensure_cache_lo(p, cache))) return rc;
         if ((rc = DISPATCH_MP(p, launch_input_lo, p, st, input, V, cache->Vlo, NT, NTs))) return rc;
     }
-    if (p->dense && p->tc_ready)
+    if (p->tc_ready && (p->dense || p->contraction == 1))
         rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
@@ -1235,7 +1257,7 @@ int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, vo
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
-    if (p->dense && p->tc_ready)
+    if (p->tc_ready && (p->dense || p->contraction == 1))
         rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
     else
         rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
@@ -1304,6 +1326,22 @@ int wino_recompress(wino_plan* p, double zero_tol) {
 
 int wino_set_option(wino_plan* p, int option, int value) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    if (option == WINO_OPT_CONTRACTION) {
+        if (value < 0 || value > 1) return set_err(WINO_INVALID_ARGUMENT, "contraction must be 0 or 1");
+        if (value == 1 && (p->C % 4 || p->K % 4))
+            return set_err(WINO_CAPABILITY_ERROR, "tensor-core contraction needs C and K multiples of 4 (TMA strides)");
+        p->contraction = value;
+        if (p->has_weights && !p->dense) {
+            if (value == 1) {
+                const int rc = refresh_tc_operands(p, nullptr);
+                if (rc) return rc;
+                CUDA_TRY(cudaDeviceSynchronize());
+            } else {
+                p->tc_ready = false;
+            }
+        }
+        return WINO_OK;
+    }
     if (option != WINO_OPT_DW_MODE || value < 0 || value > 2)
         return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
     if (value == 1) {

@@ -99,4 +99,18 @@ __global__ void csr_to_kcpq_f64_kernel(const int* __restrict__ rowptr, const int
     }
 }
 
+// CSR values -> zero-filled slice-major W[s][k][c] fp32 (the tensor-core operand source of a
+// sparse plan).  One thread per (row k, slice s).
+__global__ void csr_scatter_dense_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
+                                         const float* __restrict__ vals, int K, int C, int P2,
+                                         float* __restrict__ dst) {
+    const int64_t total = (int64_t)K * P2;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(t % P2), k = (int)(t / P2);
+        const int b = rowptr[(int64_t)s * (K + 1) + k], e = rowptr[(int64_t)s * (K + 1) + k + 1];
+        float* row = dst + ((int64_t)s * K + k) * C;
+        for (int i = b; i < e; ++i) row[colidx[i]] = vals[i];
+    }
+}
+
 }  // namespace wino

@@ -206,6 +206,11 @@ class WinogradLayer:
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE,
                                     {"sddmm": 0, "tc": 1, "precise": 2}[mode]))
 
+    def set_contraction(self, mode: str):
+        """Sparse plan contractions: 'csr' (default; the reference's order, forward bitwise equal
+        to sparse_forward<float>) or 'tc' (3xTF32 tcgen05 GEMM over the zero-filled W_F slices)."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1}[mode]))
+
     def weight_values(self):
         """Device pointer (int) of the live CSR values (nnz floats)."""
         ptr = C.c_void_p()

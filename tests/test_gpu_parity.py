@@ -32,13 +32,15 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
 
 
-def run_layer(img, w_f, grad_o, m, pad, dense=None, dw_mode=None):
+def run_layer(img, w_f, grad_o, m, pad, dense=None, dw_mode=None, contraction=None):
     n, c, h, w = img.shape
     k = w_f.shape[0]
     layer = wb.WinogradLayer(c, k, h, w, pad=pad, m=m)
     layer.set_weights(w_f, dense=dense)
     if dw_mode is not None:
         layer.set_dw_mode(dw_mode)
+    if contraction is not None:
+        layer.set_contraction(contraction)
     cache = layer.new_cache(n)
     o = layer.forward(dev(img), cache)
     out = {"layer": layer, "o": o.cpu().numpy()}
@@ -287,6 +289,52 @@ def test_c1_precise_dw_strict_everywhere():
     assert int(bad.sum()) == 0, f"{int(bad.sum())} strict misses"
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(r["o"], mir["o"])
+
+
+def test_c1_tensor_core_contraction():
+    """WINO_OPT_CONTRACTION=1 on the sparse plan (zero-filled W_F on tcgen05): O and dI within the
+    strict tolerance of the f64 reference on every element at configs[1]; dW_F unchanged (it
+    stays on the exact SDDMM)."""
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg)
+    r = run_layer(img, w_f, go, 4, 1, dense=False, contraction="tc")
+    base = run_layer(img, w_f, go, 4, 1, dense=False)
+    o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
+    assert_parity(r["o"], o, "c1 O (tc contraction)")
+    assert_parity(r["di"], di, "c1 dI (tc contraction)")
+    # dZ does not depend on the contraction, so neither does the SDDMM's dW
+    assert np.array_equal(r["dw_raw"], base["dw_raw"])
+
+
+@pytest.mark.parametrize("name", ["c0", "f43_dense", "f63"])
+def test_tensor_core_contraction_golden(name):
+    d = load_layer(name)
+    if d["c"] % 4 or d["k"] % 4:
+        pytest.skip("TMA strides need C, K multiples of 4")
+    r = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False, contraction="tc")
+    assert_parity(r["o"], d["o_f64"], "O vs f64 reference")
+    assert_parity(r["di"], d["grad_in_f64"], "dI vs f64 reference")
+
+
+def test_tensor_core_contraction_follows_updates():
+    """After an update the zero-filled operands are rebuilt: the forward equals a fresh plan of
+    the updated weights, and masked coordinates stay zero."""
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=2)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f)
+    layer.set_contraction("tc")
+    cache = layer.new_cache(2)
+    layer.forward(dev(img), cache)
+    g = layer.backward_weights(dev(go), cache)
+    layer.sgd_step(g, lr=0.05)
+    out = layer.forward(dev(img)).cpu().numpy()
+    w1 = layer.weights()
+    assert np.all(w1[w_f == 0] == 0)
+    fresh = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    fresh.set_weights(w1, dense=False)
+    fresh.set_contraction("tc")
+    assert np.array_equal(out, fresh.forward(dev(img)).cpu().numpy())
 
 
 def test_determinism_and_repeatability():
