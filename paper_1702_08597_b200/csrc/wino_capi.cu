@@ -184,6 +184,8 @@ struct wino_plan {
     unsigned long long* d_nonfinite = nullptr;
     std::vector<int> h_rowptr, h_colptr;  // kept for launch partitioning
     int sddmm_rows = 0, sddmm_r = 0, sddmm_stages = 1, sddmm_maxb = 8;
+    int sddmm_impl = 1;               // 0 = warp/transpose kernel (also the precise mode), 1 = chunk form
+    int lane_rows = 0, lane_tw = 0;   // chunk-form plan (0 rows: infeasible)
     int64_t sddmm_max_nb = 0;
     double* d_partial = nullptr;
     size_t partial_cap = 0;
@@ -431,7 +433,9 @@ void plan_sddmm(wino_plan* p) {
         const char* env = std::getenv("WINO_SDDMM_MAXB");
         const int first = env ? std::atoi(env) : 4;
         for (int lim : {first, 8, 16}) {
-            for (int rows = (int)std::min<int64_t>(round_up(K, 8), cap_rows / 8 * 8); rows >= 8; rows -= 8) {
+            int rows_cap = (int)std::min<int64_t>(round_up(K, 8), cap_rows / 8 * 8);
+            if (const char* e = std::getenv("WINO_SDDMM_ROWS")) rows_cap = std::min(rows_cap, std::max(8, std::atoi(e)));
+            for (int rows = rows_cap; rows >= 8; rows -= 8) {
                 const int64_t nb = max_group_nnz(p, rows);
                 if (nb <= (int64_t)kSddmmWarps * kSddmmBatch * lim) {
                     p->sddmm_r = o.r;
@@ -448,6 +452,44 @@ void plan_sddmm(wino_plan* p) {
     p->sddmm_r = 0;  // no feasible variant: launch reports CAPABILITY
 }
 
+void plan_sddmm_chunk(wino_plan* p);
+void plan_sddmm_all(wino_plan* p) {
+    plan_sddmm(p);
+    plan_sddmm_chunk(p);
+    p->sddmm_impl = p->lane_rows > 0 ? 1 : 0;
+    if (const char* e = std::getenv("WINO_SDDMM_IMPL")) p->sddmm_impl = (std::atoi(e) == 1 && p->lane_rows > 0) ? 1 : 0;
+}
+
+constexpr int kChunkThreads = 1024;
+
+// Chunk-form SDDMM plan: TW = 128 when Ĩ_F(:, chunk) plus a useful row group fits, else 64; the
+// row group is as large as shared memory allows (fewest re-stagings of the Ĩ_F chunk).
+void plan_sddmm_chunk(wino_plan* p) {
+    p->lane_rows = 0;
+    const int64_t budget = std::min(p->max_smem, 220 * 1024);
+    for (int tw : {128, 64}) {
+        const int64_t cap_rows = budget / (tw * 4) - p->C;
+        if (cap_rows < 8) continue;
+        const int64_t need = round_up(p->K, 8);
+        int rows = (int)std::min<int64_t>(need, cap_rows / 8 * 8);
+        // balance the groups: same number of groups, rows spread evenly
+        const int groups = (p->K + rows - 1) / rows;
+        rows = (int)round_up((p->K + groups - 1) / groups, 8);
+        if (const char* e = std::getenv("WINO_SDDMM_ROWS")) rows = std::max(8, std::min(rows, std::atoi(e)));
+        p->lane_rows = rows;
+        p->lane_tw = tw;
+        return;
+    }
+}
+
+template <int TW>
+void launch_sddmm_chunk_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
+                          const float* V, float* dW, double* partial, int NTs) {
+    set_smem_attr(wino::sddmm_chunk_kernel<TW, kChunkThreads>, (int)smem);
+    wino::sddmm_chunk_kernel<TW, kChunkThreads><<<grid, kChunkThreads, smem, st>>>(
+        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NTs, p->lane_rows);
+}
+
 template <int R, int MAXB, int STAGES, bool LO>
 void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
                     const float* V, const float* DZlo, const float* Vlo, float* dW, double* partial, int NT,
@@ -460,18 +502,62 @@ void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p,
         p->sddmm_rows, tps);
 }
 
+double* ensure_partial(wino_plan* p, size_t need, int* rc) {
+    *rc = WINO_OK;
+    if (p->partial_cap < need) {
+        if (p->d_partial) cudaFree(p->d_partial);
+        p->d_partial = nullptr;
+        p->partial_cap = 0;
+        const cudaError_t e = cudaMalloc(&p->d_partial, need * sizeof(double));
+        if (e != cudaSuccess) {
+            *rc = set_err(WINO_CUDA_ERROR, std::string("sddmm partials: ") + cudaGetErrorString(e));
+            return nullptr;
+        }
+        p->partial_cap = need;
+    }
+    return p->d_partial;
+}
+
+int launch_sddmm_chunk(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
+                       int64_t NTs) {
+    const int TW = p->lane_tw;
+    const size_t smem = (size_t)(p->C + p->lane_rows) * TW * 4;
+    const int groups = (p->K + p->lane_rows - 1) / p->lane_rows;
+    const int chunks = (int)((NT + TW - 1) / TW);
+    int rc = WINO_OK;
+    double* partial = chunks > 1 ? ensure_partial(p, (size_t)chunks * p->nnz, &rc) : nullptr;
+    if (rc) return rc;
+    const dim3 grid(groups, p->P2, chunks);
+    {
+        Launch L(p, st, K_SDDMM);
+        if (TW == 128)
+            launch_sddmm_chunk_v<128>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs);
+        else
+            launch_sddmm_chunk_v<64>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs);
+        if ((rc = L.done())) return rc;
+    }
+    if (chunks > 1) {
+        Launch L(p, st, K_SDDMM);
+        wino::split_sum_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(partial, dW, p->nnz, chunks);
+        return L.done();
+    }
+    return WINO_OK;
+}
+
 int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
                  int64_t NTs, const float* DZlo = nullptr, const float* Vlo = nullptr) {
     if (p->nnz == 0) return WINO_OK;
-    if (p->sddmm_r == 0) return set_err(WINO_CAPABILITY_ERROR, "sddmm: no variant fits this layer");
     const bool lo = Vlo != nullptr;
     if (lo != (p->dw_mode == 2)) return set_err(WINO_CONSISTENCY_ERROR, "sddmm: plan/precision mismatch");
+    if (p->sddmm_impl == 1 && !lo) return launch_sddmm_chunk(p, st, DZ, V, dW, NT, NTs);
+    if (p->sddmm_r == 0) return set_err(WINO_CAPABILITY_ERROR, "sddmm: no variant fits this layer");
     const int R = p->sddmm_r, TW = 32 * R;
     const size_t smem = (size_t)p->sddmm_stages * (p->C + p->sddmm_rows) * TW * 4 * (lo ? 2 : 1);
     const int groups = (p->K + p->sddmm_rows - 1) / p->sddmm_rows;
     const int chunks = (int)((NT + TW - 1) / TW);
     const int64_t base = (int64_t)groups * p->P2;
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>((3LL * p->sm_count + base - 1) / base, chunks / 2));
+    if (const char* e = std::getenv("WINO_SDDMM_SPLITS")) splits = std::max(1, std::min(chunks, std::atoi(e)));
     const int tps = ((chunks + splits - 1) / splits) * TW;
     splits = (int)((NT + tps - 1) / tps);
     double* partial = nullptr;
@@ -776,7 +862,7 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
-    plan_sddmm(p);
+    plan_sddmm_all(p);
     if (p->contraction == 1) {
         const int rc2 = refresh_tc_operands(p, nullptr);
         if (rc2) return rc2;
@@ -875,7 +961,7 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
-    plan_sddmm(p);
+    plan_sddmm_all(p);
     if (p->contraction == 1) {
         const int rc2 = refresh_tc_operands(p, nullptr);
         if (rc2) return rc2;
@@ -1354,7 +1440,7 @@ int wino_set_option(wino_plan* p, int option, int value) {
     }
     const bool replan = (value == 2) != (p->dw_mode == 2);
     p->dw_mode = value;
-    if (replan && p->has_weights) plan_sddmm(p);  // the precise variant stages twice the rows
+    if (replan && p->has_weights) plan_sddmm_all(p);  // the precise variant stages twice the rows
     return WINO_OK;
 }
 

@@ -637,16 +637,21 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
         const float* base = st0 + buf * stage_floats + lane * R;
 #pragma unroll
         for (int i = 0; i < MAXB; ++i) {
-            if ((warp + i * nw) * BATCH >= nb) break;  // warp-uniform
+            // warp-uniform conditions are evaluated through votes, so the compiler knows the
+            // shuffles below run converged (no collective fallback code around them)
+            if (!__any_sync(kFull, (warp + i * nw) * BATCH < nb)) break;
             double part[BATCH];
             double zd[R];
             double zl[LO ? R : 1];
+            int qv[BATCH];
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) qv[j] = __shfl_sync(kFull, pk[i], j);
             int rprev = -1;
 #pragma unroll
             for (int j = 0; j < BATCH; ++j) {
-                const int q = __shfl_sync(kFull, pk[i], j);
+                const int q = qv[j];
                 const int ro = q >> 16;
-                if (ro != rprev) {
+                if (__any_sync(kFull, ro != rprev)) {
                     float z[R];
                     lds_vec<R>(base + ro * R, z);
 #pragma unroll
@@ -689,6 +694,86 @@ sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                 dW[e0 + b] = (float)acc[i];
             else
                 partial[(int64_t)blockIdx.z * nnz_total + e0 + b] = acc[i];
+        }
+    }
+}
+
+// K5, chunk form (the default SDDMM).  Block = (row group, slice, one TW-wide t chunk): Ĩ_F(:, chunk)
+// and dZ(rows, chunk) are staged once, then every nonzero of the row group is reduced over the
+// chunk by one quarter-warp: lane l of the quarter covers t = 4l + 32i (i < TW/32), so each
+// LDS.128 step of a quarter reads 128 contiguous bytes of the nonzero's Ĩ_F row (conflict-free).
+// A quarter walks a contiguous CSR segment, so its dZ row stays cached in registers as fp64 and
+// is reloaded only when the row changes.  Products are exact fp64 products of the fp32 operands
+// (one conversion per product), summed in two fp64 chains per lane, then across the quarter by
+// a 3-step xor butterfly.  The chunk sum goes to partial[chunk][e] (fp64; summed over chunks in
+// order by split_sum_kernel) or straight to dW when there is one chunk.  No per-chunk state
+// survives the block, so blocks never re-stage the same Ĩ_F chunk for the same nonzeros.
+// Deterministic: fixed per-lane t order, fixed butterfly, fixed chunk order.
+template <int TW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1)
+sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
+                   const int* __restrict__ rowof, const float* __restrict__ DZ,
+                   const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
+                   int64_t nnz_total, int K, int C, int NTs, int rows_per_block) {
+    constexpr int Q = TW / 32;  // LDS.128 steps per lane per nonzero
+    constexpr int NQ = THREADS / 8;
+    extern __shared__ float4 smem_f4[];
+    const int s = blockIdx.y;
+    const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(K, r0 + rows_per_block);
+    const int nrb = r1 - r0;
+    const int* rp = rowptr + (int64_t)s * (K + 1);
+    const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
+    const int t0 = blockIdx.z * TW;
+    float* vs = reinterpret_cast<float*>(smem_f4);
+    float* zs = vs + C * TW;
+    stage_rows_async<TW>(V + (int64_t)s * C * NTs, vs, C, NTs, t0);
+    stage_rows_async<TW>(DZ + ((int64_t)s * K + r0) * NTs, zs, nrb, NTs, t0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int ql = threadIdx.x & 7;
+    const int quarter = threadIdx.x >> 3;
+    const unsigned qmask = 0xffu << (threadIdx.x & 24);
+    const int nb = e1 - e0;
+    const int per = (nb + NQ - 1) / NQ;
+    const int qb = e0 + quarter * per;
+    const int qe = min(e1, qb + per);
+    double zd[4 * Q];
+    int rcur = -1;
+    for (int e = qb; e < qe; ++e) {
+        const int r = __ldg(rowof + e), c = __ldg(colidx + e);
+        if (r != rcur) {
+            const float* zr = zs + (r - r0) * TW + 4 * ql;
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                const float4 z = *reinterpret_cast<const float4*>(zr + 32 * i);
+                zd[4 * i] = z.x;
+                zd[4 * i + 1] = z.y;
+                zd[4 * i + 2] = z.z;
+                zd[4 * i + 3] = z.w;
+            }
+            rcur = r;
+        }
+        const float* xr = vs + c * TW + 4 * ql;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const float4 x = *reinterpret_cast<const float4*>(xr + 32 * i);
+            a0 = fma(zd[4 * i], (double)x.x, a0);  // exact products: fp32×fp32 fits fp64
+            a1 = fma(zd[4 * i + 1], (double)x.y, a1);
+            a0 = fma(zd[4 * i + 2], (double)x.z, a0);
+            a1 = fma(zd[4 * i + 3], (double)x.w, a1);
+        }
+        double v = a0 + a1;
+        v += __shfl_xor_sync(qmask, v, 1);
+        v += __shfl_xor_sync(qmask, v, 2);
+        v += __shfl_xor_sync(qmask, v, 4);
+        if (ql == 0) {
+            if (partial == nullptr)
+                dW[e] = (float)v;
+            else
+                partial[(int64_t)blockIdx.z * nnz_total + e] = v;
         }
     }
 }
