@@ -373,23 +373,34 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
     const size_t xbytes = (size_t)ncols * TW * sizeof(float);
     const int chunks = (int)((NT + TW - 1) / TW);
     const int64_t base = (int64_t)chunks * p->P2;
-    const int64_t target = (int64_t)p->sm_count * 3;
+    // enough blocks to fill the GPU once; beyond that every extra row group re-stages the X chunk
+    const int64_t target = (int64_t)p->sm_count * 9 / 10;
     int groups = (int)std::max<int64_t>(1, std::min<int64_t>((target + base - 1) / base, nrows / 16));
+    if (const char* e = std::getenv("WINO_SPMM_GROUPS")) groups = std::max(1, std::atoi(e));
+    // prefer the staged CSR segment (measured faster than L1 reads, c2/c3), adding row groups
+    // until it fits; only a segment that never fits falls back to reading it through L1
     int rpb = 0;
-    size_t smem = 0;
+    size_t seg = 0;
     for (;; ++groups) {
         rpb = (int)round_up((nrows + groups - 1) / groups, 16);
-        smem = xbytes + (size_t)max_segment(hptr, p->P2, nrows, rpb) * sizeof(int2);
-        if ((int)smem <= p->max_smem || rpb <= 16) break;
+        seg = (size_t)max_segment(hptr, p->P2, nrows, rpb) * sizeof(int2);
+        if ((int)(xbytes + seg) <= p->max_smem || rpb <= 16) break;
     }
     groups = (nrows + rpb - 1) / rpb;
+    const bool staged = (int)(xbytes + seg) <= p->max_smem && !std::getenv("WINO_SPMM_UNSTAGED");
+    const size_t smem = staged ? xbytes + seg : xbytes;
     if ((int)smem > p->max_smem)
         return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
-    set_smem_attr(wino::spmm_kernel<R>, (int)smem);
     Launch L(p, st, kind);
     const int threads = std::getenv("WINO_SPMM_THREADS") ? std::atoi(std::getenv("WINO_SPMM_THREADS")) : 1024;
-    wino::spmm_kernel<R><<<dim3(chunks, groups, p->P2), threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols,
-                                                                        (int)NTs, rpb);
+    const dim3 grid(chunks, groups, p->P2);
+    if (staged) {
+        set_smem_attr(wino::spmm_kernel<R, true>, (int)smem);
+        wino::spmm_kernel<R, true><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb);
+    } else {
+        set_smem_attr(wino::spmm_kernel<R, false>, (int)smem);
+        wino::spmm_kernel<R, false><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb);
+    }
     return L.done();
 }
 

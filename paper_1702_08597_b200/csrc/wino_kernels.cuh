@@ -436,7 +436,22 @@ __device__ __forceinline__ int2 ld_uniform_int2(const int2* p) {
     return v;
 }
 
-template <int R>
+template <bool STAGED>
+__device__ __forceinline__ int4 load_pair(const int2* p) {
+    if constexpr (STAGED) return *reinterpret_cast<const int4*>(p);
+    else return __ldg(reinterpret_cast<const int4*>(p));
+}
+template <bool STAGED>
+__device__ __forceinline__ int2 load_one(const int2* p) {
+    if constexpr (STAGED) return *p;
+    else return __ldg(p);
+}
+
+// STAGED: the block's CSR segment is copied next to the X chunk (LDS.128 broadcasts); otherwise
+// the (col, value) pairs are read warp-uniformly from global memory through L1, which frees the
+// shared memory for the whole row range of a slice (one block per (chunk, slice): the X chunk is
+// staged once instead of once per row group).
+template <int R, bool STAGED>
 __global__ void __launch_bounds__(1024)
 spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs,
@@ -454,7 +469,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
     // the block's CSR segment (col byte offset, value) lands next to the X chunk
     int2* cvs = reinterpret_cast<int2*>(xs + ncols * TW);
     stage_rows_async<TW>(X + (int64_t)s * ncols * NTs, xs, ncols, NTs, t0);
-    {
+    if constexpr (STAGED) {
         const int a0 = e0 & ~1;  // 16-byte aligned start (pairs of int2)
         const int n2 = (e1 - a0 + 1) >> 1;
         const int4* src = reinterpret_cast<const int4*>(colval + a0);
@@ -464,7 +479,8 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    const int2* cvb = cvs - (e0 & ~1);  // index with global entry numbers
+    // index with global entry numbers
+    const int2* cvb = STAGED ? cvs - (e0 & ~1) : colval;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float* yg = Y + (int64_t)s * nrows * NTs;
     const int tl = t0 + lane * R;
@@ -476,7 +492,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
         int e = __ldg(rp + r);
         const int ee = __ldg(rp + r + 1);
         if ((e & 1) && e < ee) {  // peel to a 16-byte-aligned pair boundary
-            const int2 cv = cvb[e];
+            const int2 cv = load_one<STAGED>(cvb + e);
             float x[R];
             lds_vec<R>(reinterpret_cast<const float*>(xl + cv.x * (TW * 4)), x);
 #pragma unroll
@@ -487,7 +503,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             int2 cv[U];
 #pragma unroll
             for (int u = 0; u < U; u += 2) {  // one broadcast LDS.128 per two nonzeros
-                const int4 two = *reinterpret_cast<const int4*>(cvb + e + u);
+                const int4 two = load_pair<STAGED>(cvb + e + u);
                 cv[u] = make_int2(two.x, two.y);
                 cv[u + 1] = make_int2(two.z, two.w);
             }
@@ -503,7 +519,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             int2 cv[4];
 #pragma unroll
             for (int u = 0; u < 4; u += 2) {
-                const int4 two = *reinterpret_cast<const int4*>(cvb + e + u);
+                const int4 two = load_pair<STAGED>(cvb + e + u);
                 cv[u] = make_int2(two.x, two.y);
                 cv[u + 1] = make_int2(two.z, two.w);
             }
@@ -517,7 +533,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             e += 4;
         }
         for (; e < ee; ++e) {
-            const int2 cv = cvb[e];
+            const int2 cv = load_one<STAGED>(cvb + e);
             float x[R];
             lds_vec<R>(reinterpret_cast<const float*>(xl + cv.x * (TW * 4)), x);
 #pragma unroll
