@@ -248,10 +248,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
         layer.forward(x, cache, out=out)
         if fwd_only:
             return
-        layer.backward_weights(g_o, cache, out=dw)
+        if args.separate_bwd:
+            layer.backward_weights(g_o, cache, out=dw)
+            layer.backward_input(cache, out=di)
+        else:  # dW_F concurrently with dI (wino_backward)
+            layer.backward(g_o, cache, out_w=dw, out_i=di)
         if world > 1:
             dist.all_reduce(dw)
-        layer.backward_input(cache, out=di)
 
     for _ in range(args.warmup):
         step()
@@ -566,6 +569,8 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
+    ap.add_argument("--separate-bwd", action="store_true",
+                    help="backward_weights then backward_input instead of the concurrent wino_backward")
     ap.add_argument("--contraction", default="csr", choices=["csr", "tc"],
                     help="sparse plan: CSR kernels (bitwise reference order) or tcgen05 on zero-filled W_F")
     ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise"],

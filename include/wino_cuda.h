@@ -137,6 +137,11 @@ WINO_API int wino_forward(wino_plan* plan, int n, const float* input, float* out
 #define WINO_BWD_RELU_MASK 1
 WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, const float* relu_out,
                           wino_cache* cache, float* grad_w, int flags, void* stream);
+/* backward_weights + backward_input in one call: dZ first, then dW_F on an internal stream
+ * concurrently with dĨ_F -> dI on `stream` (they share only the read-only dZ and Ĩ_F); `stream`
+ * waits for both before the call's work is complete.  Same results as the two calls. */
+WINO_API int wino_backward(wino_plan* plan, const float* grad_output, const float* relu_out,
+                           wino_cache* cache, float* grad_w, float* grad_input, int flags, void* stream);
 /* winograd_backward_input (layer.cpp:134-171): dI (device, n×C×H×W).
  * WINO_CONSISTENCY_ERROR if backward_weights has not run on this cache. */
 WINO_API int wino_backward_input(wino_plan* plan, const wino_cache* cache, float* grad_input, void* stream);

@@ -210,6 +210,8 @@ struct wino_plan {
     float* d_dv = nullptr;
     size_t dv_cap = 0;
     double* d_scalar = nullptr;
+    cudaStream_t side = nullptr;  // wino_backward: dW runs here, concurrent with dĨ_F -> dI
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // instrumentation
     int64_t launches = 0;
     bool prof = false;
@@ -1093,6 +1095,9 @@ int wino_plan_destroy(wino_plan* p) {
     if (p->d_z) chk(cudaFree(p->d_z), "d_z");
     if (p->d_dv) chk(cudaFree(p->d_dv), "d_dv");
     if (p->d_scalar) chk(cudaFree(p->d_scalar), "d_scalar");
+    if (p->side) chk(cudaStreamDestroy(p->side), "side stream");
+    if (p->ev_fork) chk(cudaEventDestroy(p->ev_fork), "ev_fork");
+    if (p->ev_join) chk(cudaEventDestroy(p->ev_join), "ev_join");
     if (p->d_partial) chk(cudaFree(p->d_partial), "d_partial");
     if (p->d_slice_off) chk(cudaFree(p->d_slice_off), "d_slice_off");
     for (auto& r : p->recs) {
@@ -1300,45 +1305,101 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     return WINO_OK;
 }
 
-int wino_backward_weights(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c,
-                          float* grad_w, int flags, void* stream) {
+static int bwd_check(wino_plan* p, const float* grad_output, const float* relu_out, const wino_cache* c,
+                     const float* grad_w, int flags) {
     int rc = check_plan(p);
     if (rc) return rc;
     if (!c || !grad_output || (!grad_w && p->nnz > 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (c->plan != p || !c->has_fwd)
         return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
+    if ((flags & WINO_BWD_RELU_MASK) && !relu_out)
+        return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
+    if (p->dw_mode == 2 && !c->Vlo)
+        return set_err(WINO_CONSISTENCY_ERROR, "precise dW: run the forward with this mode set");
+    return WINO_OK;
+}
+
+// dZ = A1·dÕ·A2ᵀ (+ its fp32 residual in the precise mode) into the cache
+static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, int flags,
+                      cudaStream_t st) {
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
-    if (mask && !relu_out) return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
-    cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask))) return rc;
+    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask);
+    if (rc) return rc;
+    if (p->dw_mode == 2)
+        rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask);
+    return rc;
+}
+
+// dW_F from the cached dZ and Ĩ_F
+static int bwd_dw(wino_plan* p, const wino_cache* c, float* grad_w, cudaStream_t st) {
+    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     const bool precise = p->dw_mode == 2;
-    if (precise) {
-        if (!c->Vlo) return set_err(WINO_CONSISTENCY_ERROR, "precise dW: run the forward with this mode set");
-        if ((rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask)))
-            return rc;
+    int rc = WINO_OK;
+    if (p->dense && p->tc_ready && !precise) return launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs);
+    float* dwc = grad_w;
+    if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
+    if (p->dense) dwc = p->d_dwc;
+    if (!p->dense && p->dw_mode == 1 && p->nnz > 0)
+        rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
+    else if (precise)
+        rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
+    else
+        rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs);
+    if (rc) return rc;
+    if (p->dense) {  // [s][k][c] -> K×C×p×q
+        Launch L(p, st, K_MISC);
+        wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(dwc, grad_w, p->K,
+                                                                                            p->C, p->P2);
+        rc = L.done();
     }
-    if (p->dense && p->tc_ready && !precise) {
-        if ((rc = launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs))) return rc;  // tensor cores (opt-in)
-    } else {
-        float* dwc = grad_w;
-        if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
-        if (p->dense) dwc = p->d_dwc;
-        if (!p->dense && p->dw_mode == 1 && p->nnz > 0)
-            rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
-        else if (precise)
-            rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
-        else
-            rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs);
-        if (rc) return rc;
-        if (p->dense) {  // [s][k][c] -> K×C×p×q
-            Launch L(p, st, K_MISC);
-            wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
-                dwc, grad_w, p->K, p->C, p->P2);
-            if ((rc = L.done())) return rc;
-        }
-    }
+    return rc;
+}
+
+// dĨ_F = W_Fᵀ·dZ and dI = Σ_φ B1·dĨ_F·B2ᵀ
+static int bwd_input(wino_plan* p, const wino_cache* c, float* grad_input, cudaStream_t st) {
+    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
+    int rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs);
+    if (rc) return rc;
+    if (p->tc_ready && (p->dense || p->contraction == 1))
+        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
+    else
+        rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
+    if (rc) return rc;
+    return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
+}
+
+int wino_backward_weights(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c,
+                          float* grad_w, int flags, void* stream) {
+    int rc = bwd_check(p, grad_output, relu_out, c, grad_w, flags);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
+    if ((rc = bwd_dw(p, c, grad_w, st))) return rc;
     c->has_grad_z = true;
+    return WINO_OK;
+}
+
+int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, float* grad_w,
+                  float* grad_input, int flags, void* stream) {
+    int rc = bwd_check(p, grad_output, relu_out, c, grad_w, flags);
+    if (rc) return rc;
+    if (!grad_input) return set_err(WINO_INVALID_ARGUMENT, "null grad_input");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!p->side) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
+    c->has_grad_z = true;
+    // dW (side stream) and dĨ_F -> dI (caller's stream) only share the read-only dZ and Ĩ_F
+    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
+    if ((rc = bwd_input(p, c, grad_input, st))) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
     return WINO_OK;
 }
 
@@ -1351,15 +1412,7 @@ int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, vo
     if (!c->has_fwd || !c->has_grad_z)  // layer.cpp:137-138
         return set_err(WINO_CONSISTENCY_ERROR, "backward_input: dL/dZ missing; run backward_weights first");
     if (!grad_input) return set_err(WINO_INVALID_ARGUMENT, "null grad_input");
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
-    if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
-    else
-        rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
-    if (rc) return rc;
-    return DISPATCH_MP(p, launch_input_grad, p, st, p->d_dv, grad_input, c->n, NTs);
+    return bwd_input(p, c, grad_input, (cudaStream_t)stream);
 }
 
 int wino_update_weights(wino_plan* p, const float* grad_w, const wino_update* u, void* stream) {

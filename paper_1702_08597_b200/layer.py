@@ -265,6 +265,22 @@ class WinogradLayer:
                                           _stream_ptr(stream)))
         return out
 
+    def backward(self, grad_o, cache: ForwardCache, relu_out=None, out_w=None, out_i=None, stream=None):
+        """backward_weights + backward_input in one call, dW_F computed concurrently with dI."""
+        import torch
+
+        n = cache.n
+        self._check_dev(grad_o, (n, self.k, self.ho, self.wo), "grad_output")
+        if relu_out is not None:
+            self._check_dev(relu_out, (n, self.k, self.ho, self.wo), "relu_out")
+        if out_w is None:
+            out_w = torch.empty(self.grad_w_shape(), device=grad_o.device, dtype=torch.float32)
+        if out_i is None:
+            out_i = torch.empty((max(n, 1), self.c, self.h, self.w), device=grad_o.device, dtype=torch.float32)
+        check(lib().wino_backward(self._h, _dptr(grad_o), _dptr(relu_out), cache._h, _dptr(out_w), _dptr(out_i),
+                                  _lib.WINO_BWD_RELU_MASK if relu_out is not None else 0, _stream_ptr(stream)))
+        return out_w, out_i
+
     def backward_input(self, cache: ForwardCache, out=None, stream=None):
         import torch
 

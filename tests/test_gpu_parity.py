@@ -337,6 +337,27 @@ def test_tensor_core_contraction_follows_updates():
     assert np.array_equal(out, fresh.forward(dev(img)).cpu().numpy())
 
 
+@pytest.mark.parametrize("mode", ["sparse", "dense-tc", "precise"])
+def test_fused_backward_equals_separate_calls(mode):
+    """wino_backward (dW on a side stream, concurrent with dI) == backward_weights + backward_input."""
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=3)
+    if mode == "dense-tc":
+        w_f = np.where(w_f == 0, 0.01, w_f)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=True if mode == "dense-tc" else False)
+    if mode == "precise":
+        layer.set_dw_mode("precise")
+    cache = layer.new_cache(3)
+    x, g = dev(img), dev(go)
+    o = layer.forward(x, cache, relu=True)
+    dw1 = layer.backward_weights(g, cache, relu_out=o)
+    di1 = layer.backward_input(cache)
+    dw2, di2 = layer.backward(g, cache, relu_out=o)
+    torch.cuda.synchronize()
+    assert torch.equal(dw1, dw2) and torch.equal(di1, di2)
+
+
 def test_determinism_and_repeatability():
     cfg = CONFIGS["c1"]
     img, w_f, go = make_inputs(cfg, n=8)
