@@ -283,11 +283,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist.barrier()
     clocks = sampler.stop()
     launches = per_step_launches * args.steps
-    # per-kernel times for the roofline: eager steps with CUDA events around every launch
+    # per-kernel times for the roofline: eager steps with CUDA events around every launch, the
+    # backward serialised (in the timed step dW_F runs concurrently with dI, which would blur the
+    # attribution of time to kernels)
+    def step_serial():
+        layer.forward(x, cache, out=out)
+        if not fwd_only:
+            layer.backward_weights(g_o, cache, out=dw)
+            layer.backward_input(cache, out=di)
+
     layer.profile(True)
     for _ in range(3):
         flush.zero_()
-        step()
+        step_serial()
     torch.cuda.synchronize()
     prof = layer.profile_read()
     layer.profile(False)
@@ -389,6 +397,25 @@ def run_gpu(args, cfg, rank, world, local_rank):
                     "traffic": traffic, "peak_source": pk["source"],
                     "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
                              "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
+    # the on-chip pipe that bounds the CSR contraction kernels: the SDDMM converts
+    # one fp32 operand to fp64 per exact product on the XU pipe (16 lanes/clk/SM); the SpMMs read
+    # one 4-byte Ĩ_F/dZ operand per product from shared memory (128 B/clk/SM = 32 products/clk/SM)
+    pipe_roofline = None
+    g_ = layer.geometry
+    products = float(layer.nnz) * n * g_["t"]
+    clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    pipes = {"sddmm_dw": ("XU: F2F.F64.F32, one per exact product", 16.0),
+             "spmm_fwd": ("shared-memory pipe: 4 B per product", 32.0),
+             "spmm_bwd_data": ("shared-memory pipe: 4 B per product", 32.0)}
+    if dom in pipes and not dense:
+        name_, peak_ = pipes[dom]
+        # sddmm_dw's two launches per step (SDDMM + split_sum) are both counted: a lower bound
+        t_dom = prof[dom][0] / 3 * 1e-3
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ach = products / t_dom / sms / clk
+        pipe_roofline = {"kernel": dom, "pipe": name_, "unit": "products/clk/SM", "achieved": ach,
+                         "peak": peak_, "frac": ach / peak_,
+                         "note": "products = nnz·N·T per launch; time from the same CUDA events"}
     line = {
         "metric": METRIC_FWD if fwd_only else METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps,
@@ -405,6 +432,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
         "roofline": roofline,
+        "pipe_roofline": pipe_roofline,
         "kernels": kernels,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item()), "mode": e2e_mode},
