@@ -321,6 +321,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
             run()
             h_out.copy_(out, non_blocking=True)
         e2e_mode = "serial copies + forward"
+    elif world == 1 and not dense and args.contraction == "csr" and args.dw == "sddmm" and not args.no_pipeline:
+        # public API: image chunks so every copy overlaps compute (paper_1702_08597_b200/pipeline.py)
+        from paper_1702_08597_b200.pipeline import PipelinedHostStep
+
+        ps = PipelinedHostStep(layer, cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
+        from paper_1702_08597_b200.graph import GraphedStep
+
+        # the whole pipelined step (copies on 3 streams + range kernels) as one CUDA graph
+        e2e_step = GraphedStep(lambda: ps(h_img, h_go, h_out, h_dw, h_di)).replay
+        e2e_mode = (f"PipelinedHostStep in one CUDA graph: pinned host buffers, {len(ps.bounds)} image chunks, "
+                    "copies overlapped with the range kernels, dW_F once over the batch")
     elif world == 1 and not args.no_graph:
         # public API: HostStep overlaps dO upload with the forward and the O / dW downloads
         # with the backward (paper_1702_08597_b200/pipeline.py)
@@ -597,6 +608,8 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
+    ap.add_argument("--no-pipeline", action="store_true", help="e2e through HostStep (whole-batch calls)")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
     ap.add_argument("--separate-bwd", action="store_true",
                     help="backward_weights then backward_input instead of the concurrent wino_backward")
     ap.add_argument("--contraction", default="csr", choices=["csr", "tc"],

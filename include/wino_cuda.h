@@ -142,6 +142,18 @@ WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, co
  * waits for both before the call's work is complete.  Same results as the two calls. */
 WINO_API int wino_backward(wino_plan* plan, const float* grad_output, const float* relu_out,
                            wino_cache* cache, float* grad_w, float* grad_input, int flags, void* stream);
+/* Image ranges of one batch of n_total images, for overlapping host transfers with compute
+ * (the CSR kernels only).  forward_range computes images [n0, n1) into the batch's cache (input
+ * and output point at image n0); backward_range computes their dL/dZ, dĨ_F and dI (grad_output,
+ * relu_out, grad_input point at image n0); once every range has run, backward_weights_cached
+ * computes dW_F over the whole batch.  n0·T must be a multiple of 4.  Results are bitwise those of
+ * the whole-batch calls (every kernel is per column, and dW_F runs once over all columns). */
+WINO_API int wino_forward_range(wino_plan* plan, int n_total, int n0, int n1, const float* input,
+                                float* output, wino_cache* cache, int flags, void* stream);
+WINO_API int wino_backward_range(wino_plan* plan, int n0, int n1, const float* grad_output,
+                                 const float* relu_out, wino_cache* cache, float* grad_input, int flags,
+                                 void* stream);
+WINO_API int wino_backward_weights_cached(wino_plan* plan, wino_cache* cache, float* grad_w, void* stream);
 /* winograd_backward_input (layer.cpp:134-171): dI (device, n×C×H×W).
  * WINO_CONSISTENCY_ERROR if backward_weights has not run on this cache. */
 WINO_API int wino_backward_input(wino_plan* plan, const wino_cache* cache, float* grad_input, void* stream);

@@ -370,7 +370,7 @@ int64_t max_segment(const std::vector<int>& ptr, int P2, int nrows, int rpb) {
 template <int R>
 int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                   const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
-                  int64_t NTs) {
+                  int64_t NTs, int64_t NTr) {
     constexpr int TW = 32 * R;
     const size_t xbytes = (size_t)ncols * TW * sizeof(float);
     const int chunks = (int)((NT + TW - 1) / TW);
@@ -398,21 +398,27 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
     const dim3 grid(chunks, groups, p->P2);
     if (staged) {
         set_smem_attr(wino::spmm_kernel<R, true>, (int)smem);
-        wino::spmm_kernel<R, true><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb);
+        wino::spmm_kernel<R, true><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb,
+                                                                (int)NTr);
     } else {
         set_smem_attr(wino::spmm_kernel<R, false>, (int)smem);
-        wino::spmm_kernel<R, false><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb);
+        wino::spmm_kernel<R, false><<<grid, threads, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs, rpb,
+                                                                 (int)NTr);
     }
     return L.done();
 }
 
+// X, Y may point at column `a` of their rows (a column range of the batch): NT = valid columns
+// of the range, NTs = the row stride, NTr = columns the range owns (≥ NT on the batch's last range,
+// which also owns the zero padding).  The whole batch: NTr = NTs.
 int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
-                int64_t NTs) {
+                int64_t NTs, int64_t NTr = -1) {
+    if (NTr < 0) NTr = NTs;
     switch (spmm_r(ncols)) {
-        case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
-        case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
-        default: return launch_spmm_r<1>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs);
+        case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
+        case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
+        default: return launch_spmm_r<1>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
     }
 }
 
@@ -615,12 +621,12 @@ int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
 
 template <int M, int P, class CF>
 int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, wino_cache* c,
-                   float* V, float* Z, int n, int64_t NT, int64_t NTs, int flags, int stage) {
+                   float* V, float* Z, int n, int64_t NT, int64_t NTs, int flags, int stage, int64_t NTr) {
     const wino_geometry& g = p->g;
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
-        wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
-            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
+        wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTr, 256, p->sm_count), 256, 0, st>>>(
+            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr);
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
@@ -636,18 +642,18 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, w
 
 template <int M, int P, class CF>
 int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
-                  int64_t NT, int64_t NTs, bool mask) {
+                  int64_t NT, int64_t NTs, bool mask, int64_t NTr) {
     const wino_geometry& g = p->g;
     Launch L(p, st, K_GRADZ);
-    const int grid = grid_for((int64_t)p->K * NTs, 256, p->sm_count);
+    const int grid = grid_for((int64_t)p->K * NTr, 256, p->sm_count);
     if (mask)
         wino::grad_z_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                              (int)NT, (int)NTs);
+                                                              (int)NT, (int)NTs, (int)NTr);
     else
         wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                               (int)NT, (int)NTs);
+                                                               (int)NT, (int)NTs, (int)NTr);
     return L.done();
 }
 
@@ -1283,7 +1289,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         V = p->d_dv;  // inference: the backward scratch doubles as Ĩ_F
     }
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0, NTs)))
         return rc;
     if (cache && p->dw_mode == 2) {
         if ((rc = ensure_cache_lo(p, cache))) return rc;
@@ -1294,7 +1300,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1, NTs)))
         return rc;
     if (cache) {
         cache->n = n;
@@ -1324,7 +1330,7 @@ static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_
                       cudaStream_t st) {
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask);
+    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs);
     if (rc) return rc;
     if (p->dw_mode == 2)
         rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask);
@@ -1401,6 +1407,95 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
     if ((rc = bwd_input(p, c, grad_input, st))) return rc;
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
     return WINO_OK;
+}
+
+// ---- image ranges of one batch (pipelined host transfers) ----
+struct ColRange {
+    int64_t a, NT, NTs, NTr;  // first column, valid columns, row stride, owned columns
+};
+
+static int make_range(const wino_plan* p, int n_total, int n0, int n1, ColRange* r) {
+    if (n_total <= 0 || n0 < 0 || n1 <= n0 || n1 > n_total)
+        return set_err(WINO_SHAPE_ERROR, "image range [" + std::to_string(n0) + ", " + std::to_string(n1) +
+                                             ") outside the batch of " + std::to_string(n_total));
+    const int64_t T = p->g.t;
+    r->a = (int64_t)n0 * T;
+    if (r->a % 4) return set_err(WINO_SHAPE_ERROR, "range start n0·T must be a multiple of 4 (16-byte columns)");
+    r->NTs = round_up((int64_t)n_total * T, 4);
+    r->NT = (int64_t)(n1 - n0) * T;
+    r->NTr = n1 == n_total ? r->NTs - r->a : r->NT;
+    return WINO_OK;
+}
+
+static int range_capable(const wino_plan* p) {
+    if (p->tc_ready || p->dw_mode != 0)
+        return set_err(WINO_CAPABILITY_ERROR, "image-range calls run the CSR kernels only "
+                                              "(no tensor-core plan/contraction, dW mode 0)");
+    return WINO_OK;
+}
+
+int wino_forward_range(wino_plan* p, int n_total, int n0, int n1, const float* input, float* output,
+                       wino_cache* cache, int flags, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if ((rc = range_capable(p))) return rc;
+    if (!input || !output || !cache) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (cache->plan != p || n_total > cache->n_max)
+        return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
+    ColRange r{};
+    if ((rc = make_range(p, n_total, n0, n1, &r))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * r.NTs))) return rc;
+    float* V = cache->V + r.a;
+    float* Z = p->d_z + r.a;
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, Z, n1 - n0, r.NT, r.NTs, flags, 0,
+                          r.NTr)))
+        return rc;
+    if ((rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, Z, p->K, p->C, r.NT, r.NTs, r.NTr)))
+        return rc;
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, Z, n1 - n0, r.NT, r.NTs, flags, 1,
+                          r.NTr)))
+        return rc;
+    cache->n = n_total;
+    cache->NTs = r.NTs;
+    cache->has_fwd = true;
+    cache->has_grad_z = false;
+    return WINO_OK;
+}
+
+int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, const float* relu_out,
+                        wino_cache* c, float* grad_input, int flags, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if ((rc = range_capable(p))) return rc;
+    if (!c || !grad_output || !grad_input) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (c->plan != p || !c->has_fwd)
+        return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
+    const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
+    if (mask && !relu_out) return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
+    ColRange r{};
+    if ((rc = make_range(p, c->n, n0, n1, &r))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * r.NTs))) return rc;
+    float* DZ = c->DZ + r.a;
+    float* DV = p->d_dv + r.a;
+    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, DZ, r.NT, r.NTs, mask, r.NTr)))
+        return rc;
+    if ((rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, DZ, DV, p->C, p->K, r.NT, r.NTs,
+                          r.NTr)))
+        return rc;
+    if ((rc = DISPATCH_MP(p, launch_input_grad, p, st, DV, grad_input, n1 - n0, r.NTs))) return rc;
+    c->has_grad_z = true;
+    return WINO_OK;
+}
+
+int wino_backward_weights_cached(wino_plan* p, wino_cache* c, float* grad_w, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!c || (!grad_w && p->nnz > 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (c->plan != p || !c->has_fwd || !c->has_grad_z)
+        return set_err(WINO_CONSISTENCY_ERROR, "backward_weights_cached: dL/dZ missing; run backward_range first");
+    return bwd_dw(p, c, grad_w, (cudaStream_t)stream);
 }
 
 int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, void* stream) {

@@ -78,12 +78,15 @@ __device__ __forceinline__ float cmadd(float acc, float c, float x) {
 template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
-                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs) {
+                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr) {
+    // columns [0, NTr) of V rows with stride NTs (a column range of the batch when V and `in` are
+    // offset to its first image); columns ≥ NT are the zero padding
     const int64_t plane = (int64_t)C * NTs;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < plane;
+    const int64_t items = (int64_t)C * NTr;
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
          gid += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(gid / NTs);
-        const int nt = (int)(gid - (int64_t)c * NTs);
+        const int c = (int)(gid / NTr);
+        const int nt = (int)(gid - (int64_t)c * NTr);
         float d[P][P];
         if (nt < NT) {
             const int n = nt / T, t = nt - n * T;
@@ -123,7 +126,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                 float acc = 0.f;
 #pragma unroll
                 for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
-                V[(int64_t)(i * P + j) * plane + gid] = acc;
+                V[(int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt] = acc;
             }
     }
 }
@@ -186,12 +189,13 @@ template <int M, int P, bool MASK, class CF>
 __global__ void __launch_bounds__(256)
 grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
               float* __restrict__ DZ, const Coefs cf, int K, int Ho, int Wo, int tiles_x, int T,
-              int NT, int NTs) {
+              int NT, int NTs, int NTr) {
     const int64_t plane = (int64_t)K * NTs;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < plane;
+    const int64_t items = (int64_t)K * NTr;
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
          gid += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(gid / NTs);
-        const int nt = (int)(gid - (int64_t)k * NTs);
+        const int k = (int)(gid / NTr);
+        const int nt = (int)(gid - (int64_t)k * NTr);
         float d[M][M];
         if (nt < NT) {
             const int n = nt / T, t = nt - n * T;
@@ -235,7 +239,7 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
                 float acc = 0.f;
 #pragma unroll
                 for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), m1[i][x]);
-                DZ[(int64_t)(i * P + j) * plane + gid] = acc;
+                DZ[(int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt] = acc;
             }
     }
 }
@@ -420,12 +424,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Stage X[0..nrows_x)[t0 .. t0+TW) (row stride NTs, NTs % 4 == 0) into xs[nrows_x][TW].
 template <int TW>
 __device__ __forceinline__ void stage_rows_async(const float* __restrict__ X, float* xs, int nrows_x,
-                                                 int NTs, int t0) {
+                                                 int NTs, int t0, int tbound = -1) {
     constexpr int V4 = TW / 4;
+    const int tb = tbound < 0 ? NTs : tbound;  // columns ≥ tb are zero-filled, never read
     for (int idx = threadIdx.x; idx < nrows_x * V4; idx += blockDim.x) {
         const int row = idx / V4, q = idx - row * V4;
         const int t = t0 + q * 4;
-        const bool ok = t < NTs;
+        const bool ok = t < tb;
         cp_async16(xs + row * TW + q * 4, X + (int64_t)row * NTs + (ok ? t : 0), ok);
     }
 }
@@ -455,7 +460,7 @@ template <int R, bool STAGED>
 __global__ void __launch_bounds__(1024)
 spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
             const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs,
-            int rows_per_block) {
+            int rows_per_block, int NTr) {
     constexpr int TW = 32 * R;
     constexpr int U = 8;  // nonzeros in flight per warp
     extern __shared__ float4 smem_f4[];
@@ -468,7 +473,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
     const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
     // the block's CSR segment (col byte offset, value) lands next to the X chunk
     int2* cvs = reinterpret_cast<int2*>(xs + ncols * TW);
-    stage_rows_async<TW>(X + (int64_t)s * ncols * NTs, xs, ncols, NTs, t0);
+    stage_rows_async<TW>(X + (int64_t)s * ncols * NTs, xs, ncols, NTs, t0, NTr);
     if constexpr (STAGED) {
         const int a0 = e0 & ~1;  // 16-byte aligned start (pairs of int2)
         const int n2 = (e1 - a0 + 1) >> 1;
@@ -539,7 +544,7 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
 #pragma unroll
             for (int q = 0; q < R; ++q) acc[q] = madd(acc[q], __int_as_float(cv.y), x[q]);
         }
-        if (tl < NTs) st_vec<R>(yg + (int64_t)r * NTs + tl, acc);
+        if (tl < NTr) st_vec<R>(yg + (int64_t)r * NTs + tl, acc);
     }
 }
 

@@ -281,6 +281,39 @@ class WinogradLayer:
                                   _lib.WINO_BWD_RELU_MASK if relu_out is not None else 0, _stream_ptr(stream)))
         return out_w, out_i
 
+    # -- image ranges of one batch (pipelined host transfers, pipeline.PipelinedHostStep) --------
+    def forward_range(self, x_part, n_total: int, n0: int, cache: ForwardCache, out_part, relu=False,
+                      stream=None):
+        """Images [n0, n0 + len(x_part)) of an n_total batch into `cache` (CSR plans only)."""
+        n1 = n0 + x_part.shape[0]
+        self._check_dev(x_part, (n1 - n0, self.c, self.h, self.w), "input")
+        self._check_dev(out_part, (n1 - n0, self.k, self.ho, self.wo), "output")
+        check(lib().wino_forward_range(self._h, n_total, n0, n1, _dptr(x_part), _dptr(out_part), cache._h,
+                                       _lib.WINO_FWD_RELU if relu else 0, _stream_ptr(stream)))
+        cache.n = n_total
+        return out_part
+
+    def backward_range(self, g_part, n0: int, cache: ForwardCache, out_part, relu_part=None, stream=None):
+        """dL/dZ, dĨ_F and dI of images [n0, n0 + len(g_part)) (after their forward_range)."""
+        n1 = n0 + g_part.shape[0]
+        self._check_dev(g_part, (n1 - n0, self.k, self.ho, self.wo), "grad_output")
+        self._check_dev(out_part, (n1 - n0, self.c, self.h, self.w), "grad_input")
+        if relu_part is not None:
+            self._check_dev(relu_part, (n1 - n0, self.k, self.ho, self.wo), "relu_out")
+        check(lib().wino_backward_range(self._h, n0, n1, _dptr(g_part), _dptr(relu_part), cache._h,
+                                        _dptr(out_part), _lib.WINO_BWD_RELU_MASK if relu_part is not None else 0,
+                                        _stream_ptr(stream)))
+        return out_part
+
+    def backward_weights_cached(self, cache: ForwardCache, out=None, stream=None):
+        """dW_F over the whole batch once every backward_range has run."""
+        import torch
+
+        if out is None:
+            out = torch.empty(self.grad_w_shape(), device=f"cuda:{self.device}", dtype=torch.float32)
+        check(lib().wino_backward_weights_cached(self._h, cache._h, _dptr(out), _stream_ptr(stream)))
+        return out
+
     def backward_input(self, cache: ForwardCache, out=None, stream=None):
         import torch
 

@@ -79,3 +79,77 @@ class HostStep:
             ev["di"].record()
         main.wait_stream(self.s_out)  # the caller's stream sees the whole step (downloads included)
         return ev["di"]
+
+
+class PipelinedHostStep:
+    """HostStep with the batch cut into image chunks so every transfer overlaps compute:
+
+        copy-in : I0 dO0 I1 dO1 I2 dO2 ...
+        compute :    f0 b0   f1 b1   f2 b2 ...            dW (whole batch)
+        copy-out:       O0 dI0  O1 dI1  O2 dI2 ...              dW
+
+    forward_range / backward_range run the CSR kernels on each chunk's columns of the one batch
+    cache; dW_F runs once over the whole batch, so results are bitwise those of HostStep.
+    The step is PCIe-bound (H2D ≈ D2H ≈ 55 GB/s on the B200 box): chunking hides all compute but
+    the last chunk's behind the transfers."""
+
+    def __init__(self, layer, cache, x, grad_o, out, grad_w, grad_in, chunks: int = 4, relu: bool = False):
+        import torch
+
+        self.layer, self.cache = layer, cache
+        self.x, self.g, self.o, self.dw, self.di = x, grad_o, out, grad_w, grad_in
+        self.relu = relu
+        n = x.shape[0]
+        t = layer.geometry["t"]
+        # chunk boundaries: image counts with n0·T a multiple of 4 (16-byte column alignment)
+        step = 1
+        while (step * t) % 4:
+            step += 1
+        per = max(step, -(-n // chunks) // step * step or step)
+        self.bounds = [(a, min(n, a + per)) for a in range(0, n, per)]
+        self.s_in = torch.cuda.Stream()
+        self.s_out = torch.cuda.Stream()
+        nb = len(self.bounds)
+        E = torch.cuda.Event
+        self.ev_x = [E() for _ in range(nb)]
+        self.ev_g = [E() for _ in range(nb)]
+        self.ev_f = [E() for _ in range(nb)]
+        self.ev_b = [E() for _ in range(nb)]
+        self.ev_w = E()
+        self.ev_done = E()
+
+    def __call__(self, h_x, h_g, h_o, h_dw, h_di):
+        import torch
+
+        main = torch.cuda.current_stream()
+        lay, cache, n = self.layer, self.cache, self.x.shape[0]
+        self.s_in.wait_stream(main)
+        with torch.cuda.stream(self.s_in):
+            for i, (a, b) in enumerate(self.bounds):
+                self.x[a:b].copy_(h_x[a:b], non_blocking=True)
+                self.ev_x[i].record()
+                self.g[a:b].copy_(h_g[a:b], non_blocking=True)
+                self.ev_g[i].record()
+        self.s_out.wait_stream(main)
+        for i, (a, b) in enumerate(self.bounds):
+            main.wait_event(self.ev_x[i])
+            lay.forward_range(self.x[a:b], n, a, cache, self.o[a:b], relu=self.relu)
+            self.ev_f[i].record(main)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_f[i])
+                h_o[a:b].copy_(self.o[a:b], non_blocking=True)
+            main.wait_event(self.ev_g[i])
+            lay.backward_range(self.g[a:b], a, cache, self.di[a:b],
+                               relu_part=self.o[a:b] if self.relu else None)
+            self.ev_b[i].record(main)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_b[i])
+                h_di[a:b].copy_(self.di[a:b], non_blocking=True)
+        lay.backward_weights_cached(cache, out=self.dw)
+        self.ev_w.record(main)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_w)
+            h_dw.copy_(self.dw, non_blocking=True)
+            self.ev_done.record()
+        main.wait_stream(self.s_out)
+        return self.ev_done

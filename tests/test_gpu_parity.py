@@ -583,3 +583,62 @@ def test_host_step_pipeline_matches_device_path():
     assert np.array_equal(outs[0].numpy(), ref["o"])
     assert np.array_equal(outs[1].numpy(), ref["dw_raw"])
     assert np.array_equal(outs[2].numpy(), ref["di"])
+
+
+@pytest.mark.parametrize("name,n,chunks,relu", [("c1", 32, 4, False), ("c1", 32, 3, True), ("c0", 9, 2, False),
+                                                ("c0", 9, 1, True)])
+def test_pipelined_host_step_is_bitwise_the_whole_batch(name, n, chunks, relu):
+    """PipelinedHostStep (image-range forward/backward, dW once over the batch) returns exactly
+    what the whole-batch device calls return; c0 (T = 9) exercises the 4-column alignment."""
+    from paper_1702_08597_b200.pipeline import PipelinedHostStep
+
+    cfg = CONFIGS[name]
+    img, w_f, go = make_inputs(cfg, n=n)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    cache = layer.new_cache(n)
+    x, g = dev(img), dev(go)
+    o_ref = layer.forward(x, cache, relu=relu)
+    dw_ref = layer.backward_weights(g, cache, relu_out=o_ref if relu else None)
+    di_ref = layer.backward_input(cache)
+    torch.cuda.synchronize()
+    want = [t.cpu().numpy() for t in (o_ref, dw_ref, di_ref)]
+    xs, gs = torch.zeros_like(x), torch.zeros_like(g)
+    o, dw, di = torch.empty_like(o_ref), torch.empty_like(dw_ref), torch.empty_like(di_ref)
+    ps = PipelinedHostStep(layer, cache, xs, gs, o, dw, di, chunks=chunks, relu=relu)
+    h = [torch.from_numpy(a).pin_memory() for a in (img, go)]
+    outs = [torch.empty(t.shape).pin_memory() for t in (o, dw, di)]
+    for _ in range(2):
+        ps(h[0], h[1], *outs)
+    torch.cuda.synchronize()
+    for got, w in zip(outs, want):
+        assert np.array_equal(got.numpy(), w)
+    # and captured as one CUDA graph (copies + kernels on three streams)
+    from paper_1702_08597_b200.graph import GraphedStep
+
+    for t in outs:
+        t.zero_()
+    GraphedStep(lambda: ps(h[0], h[1], *outs)).replay()
+    torch.cuda.synchronize()
+    for got, w in zip(outs, want):
+        assert np.array_equal(got.numpy(), w)
+
+
+def test_range_calls_validate():
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=9)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    cache = layer.new_cache(9)
+    x = dev(img)
+    o = torch.empty((9, cfg.k, layer.ho, layer.wo), device="cuda")
+    with pytest.raises(wb.ShapeError):  # 1·T = 9 columns: not 16-byte aligned
+        layer.forward_range(x[1:3], 9, 1, cache, o[1:3])
+    with pytest.raises(wb.ShapeError):
+        layer.forward_range(x[4:9], 8, 4, cache, o[4:9])
+    with pytest.raises(wb.ConsistencyError):
+        layer.backward_weights_cached(layer.new_cache(9))
+    dense = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    dense.set_weights(np.where(w_f == 0, 0.5, w_f), dense=True)
+    with pytest.raises(wb.CapabilityError):
+        dense.forward_range(x[0:4], 9, 0, dense.new_cache(9), o[0:4])
