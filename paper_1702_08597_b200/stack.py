@@ -39,6 +39,7 @@ class WinogradStack:
         self._alloc_bucket()
         self.n_max = n_max
         self.outs = [None] * len(self.layers)
+        self.dis = [None] * len(self.layers)
         self._torch = torch
 
     def _alloc_bucket(self):
@@ -60,9 +61,12 @@ class WinogradStack:
         g = grad_out
         for i in range(len(self.layers) - 1, -1, -1):
             lay, cache = self.layers[i], self.caches[i]
-            lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.grads[i])
-            if i > 0:
-                g = lay.backward_input(cache)
+            if i > 0:  # dW_F concurrently with dI (wino_backward)
+                if self.dis[i] is None or self.dis[i].shape[0] != g.shape[0]:
+                    self.dis[i] = self._torch.empty((g.shape[0], lay.c, lay.h, lay.w), device=g.device)
+                _, g = lay.backward(g, cache, relu_out=self.outs[i], out_w=self.grads[i], out_i=self.dis[i])
+            else:
+                lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.grads[i])
         return self.bucket
 
     def step(self, x, grad_out, lr, n_global, l2=0.0, group=None, mode=None, lmbda=0.0, norm=1,
