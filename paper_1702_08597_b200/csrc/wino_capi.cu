@@ -768,10 +768,20 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
         wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN><<<grid, wino::tc::THREADS, wino::tc::SMEM_BYTES, st>>>(
             ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per);
     } else {
-        set_smem_attr(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>, wino::tc::flush::SMEM_BYTES);
-        wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>
-            <<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd, p->P2,
-                                                                                splits, kb_per);
+        // k-blocks (of 32) per fresh TMEM accumulator folded into fp64: 1 = most accurate; each
+        // fold costs one fp32->fp64 conversion per output element on the XU pipe
+        static const int fold = std::getenv("WINO_TC_FOLD") ? std::atoi(std::getenv("WINO_TC_FOLD")) : 1;
+        auto go = [&](auto kern) {
+            set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
+            kern<<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd,
+                                                                                     p->P2, splits, kb_per);
+        };
+        if (fold == 2)
+            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
+        else if (fold == 4)
+            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 4>);
+        else
+            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>);
     }
     return L.done();
 }
