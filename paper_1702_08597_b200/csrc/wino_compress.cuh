@@ -90,16 +90,22 @@ __global__ void compress_fill_rows_kernel(const double* __restrict__ w, int K, i
         const int64_t base = (int64_t)k * C * P2 + s;
         int e = rowptr[(int64_t)s * (K + 1) + k];
         int* prow = pos + ((int64_t)s * K + k) * C;
-        for (int c = 0; c < C; ++c) {
-            const double v = w[base + (int64_t)c * P2];
-            if (keep_weight(v, tol, keep_all)) {
-                const float f = (float)v;
-                colidx[e] = c;
-                vals[e] = f;
-                rowof[e] = k;
-                cv[e] = make_int2(c, __float_as_int(f));
-                prow[c] = e;
-                ++e;
+        for (int c0 = 0; c0 < C; c0 += 8) {  // 8 loads in flight, then the ordered appends
+            double vv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) vv[j] = c0 + j < C ? w[base + (int64_t)(c0 + j) * P2] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j;
+                if (c < C && keep_weight(vv[j], tol, keep_all)) {
+                    const float f = (float)vv[j];
+                    colidx[e] = c;
+                    vals[e] = f;
+                    rowof[e] = k;
+                    cv[e] = make_int2(c, __float_as_int(f));
+                    prow[c] = e;
+                    ++e;
+                }
             }
         }
     }
@@ -113,13 +119,19 @@ __global__ void compress_fill_cols_kernel(const double* __restrict__ w, int K, i
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int s = (int)(t % P2), c = (int)(t / P2);
         int d = colptr[(int64_t)s * (C + 1) + c];
-        for (int k = 0; k < K; ++k) {
-            const double v = w[((int64_t)k * C + c) * P2 + s];
-            if (keep_weight(v, tol, keep_all)) {
-                rowidx[d] = k;
-                perm[d] = pos[((int64_t)s * K + k) * C + c];
-                cvT[d] = make_int2(k, __float_as_int((float)v));
-                ++d;
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            double vv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) vv[j] = k0 + j < K ? w[((int64_t)(k0 + j) * C + c) * P2 + s] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = k0 + j;
+                if (k < K && keep_weight(vv[j], tol, keep_all)) {
+                    rowidx[d] = k;
+                    perm[d] = pos[((int64_t)s * K + k) * C + c];
+                    cvT[d] = make_int2(k, __float_as_int((float)vv[j]));
+                    ++d;
+                }
             }
         }
     }
