@@ -7,9 +7,11 @@ exception classes as its pybind11 module maps them (bindings.cpp:201-204).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libwino_b200.so"
+# WINO_LIB_PATH: load another build of the same C-ABI (A/B experiments); default in-tree
+LIB_PATH = Path(os.environ.get("WINO_LIB_PATH", Path(__file__).resolve().parent / "libwino_b200.so"))
 HEADER = Path(__file__).resolve().parent.parent / "include" / "wino_cuda.h"
 
 

@@ -771,12 +771,23 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
         // k-blocks (of 32) per fresh TMEM accumulator folded into fp64: 1 = most accurate; each
         // fold costs one fp32->fp64 conversion per output element on the XU pipe
         static const int fold = std::getenv("WINO_TC_FOLD") ? std::atoi(std::getenv("WINO_TC_FOLD")) : 1;
+        static const bool persistent = !(std::getenv("WINO_TC_PERSISTENT") &&
+                                         std::atoi(std::getenv("WINO_TC_PERSISTENT")) == 0);
+        const int ntiles = (int)(grid.x * grid.y * grid.z);
         auto go = [&](auto kern) {
             set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
             kern<<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd,
                                                                                      p->P2, splits, kb_per);
         };
-        if (fold == 2)
+        auto go_p = [&](auto kern) {
+            set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
+            const int ctas = std::min(ntiles, p->sm_count);
+            kern<<<ctas, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(
+                ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y, ntiles);
+        };
+        if (persistent && fold == 1)
+            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1>);
+        else if (fold == 2)
             go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
         else if (fold == 4)
             go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 4>);

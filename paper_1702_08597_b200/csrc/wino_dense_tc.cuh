@@ -483,6 +483,194 @@ gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// Persistent form of the accurate kernel: one CTA per SM walks tiles blockIdx.x, +gridDim.x, …
+// with the TMA ring, the TMEM double buffer and every barrier phase carried across tiles by
+// global counters, so the prologue (barrier init, TMEM alloc), the pipeline fill and the epilogue
+// store of one tile overlap the next tile's loads and MMAs.  Same arithmetic per tile.
+template <bool A_SPLIT, bool B_MN, int F>
+__global__ void __launch_bounds__(flush::THREADS, 1)
+gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
+                                    const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N,
+                                    int Kd, int64_t ldd, int slices, int splits, int kb_per, int tiles_n,
+                                    int tiles_m, int ntiles) {
+    constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
+    constexpr int STAGE_BYTES = flush::STAGE_BYTES, TMEM_COLS = flush::TMEM_COLS;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* split = bars + STAGES;
+    uint64_t* empty = bars + 2 * STAGES;
+    uint64_t* tfull = bars + 3 * STAGES;
+    uint64_t* tempty = bars + 3 * STAGES + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kb_total = (Kd + BK - 1) / BK;
+    struct Tile { int n0, m0, s, q, kb0, kblocks; };
+    auto decode = [&](int tile) {
+        Tile t;
+        const int nt = tile % tiles_n, rest = tile / tiles_n;
+        const int mt = rest % tiles_m, z = rest / tiles_m;
+        t.n0 = nt * BN;
+        t.m0 = mt * BM;
+        t.s = z / splits;
+        t.q = z - t.s * splits;
+        t.kb0 = t.q * kb_per;
+        t.kblocks = max(0, min(kb_total, t.kb0 + kb_per) - t.kb0);
+        return t;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split[i], 256);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int kbg = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const Tile t = decode(tile);
+                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
+                    const int st = kbg % STAGES;
+                    if (kbg >= STAGES) mbar_wait(&empty[st], ((kbg / STAGES) - 1) & 1);
+                    uint8_t* base = stage_ptr(st);
+                    const int kk = (t.kb0 + kb) * BK;
+                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
+                    tma_load_3d(base, &mapAh, &full[st], kk, t.m0, t.s);
+                    if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, t.m0, t.s);
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 32; ++j)
+                            tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], t.n0 + 32 * j, kk, t.s);
+                    } else {
+                        tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, t.n0, t.s);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id = flush::idesc(B_MN);
+            int kbg = 0, gg = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const Tile t = decode(tile);
+                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
+                    const int st = kbg % STAGES, b = gg & 1;
+                    const bool first = (kb % F) == 0, last = (kb % F) == F - 1 || kb == t.kblocks - 1;
+                    if (first && gg >= 2) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
+                    mbar_wait(&split[st], (kbg / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a_hi = smem_u32(stage_ptr(st));
+                    const uint32_t a_lo = a_hi + A_TILE;
+                    const uint32_t b_hi = a_hi + 2 * A_TILE;
+                    const uint32_t b_lo = b_hi + B_TILE;
+                    const uint32_t acc = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+                        const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
+                        const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
+                        uint64_t dbh, dbl;
+                        if (B_MN) {
+                            dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                            dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                        } else {
+                            dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
+                            dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
+                        }
+                        mma_tf32(acc, dah, dbh, id, (first && k == 0) ? 0u : 1u);
+                        mma_tf32(acc, dah, dbl, id, 1u);
+                        mma_tf32(acc, dal, dbh, id, 1u);
+                    }
+                    mma_commit(&empty[st]);
+                    if (last) {
+                        mma_commit(&tfull[b]);
+                        ++gg;
+                    }
+                }
+            }
+        }
+    } else {
+        const int t256 = threadIdx.x - 64;
+        const int qd = warp & 3, half = (warp - 2) >> 2;
+        int total_kb = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) total_kb += decode(tile).kblocks;
+        auto split_stage = [&](int kbx) {
+            const int st = kbx % STAGES;
+            mbar_wait(&full[st], (kbx / STAGES) & 1);
+            uint8_t* base = stage_ptr(st);
+            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t256, 256);
+            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t256, 256);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&split[st]);
+        };
+        for (int kbx = 0; kbx < min(total_kb, STAGES - 1); ++kbx) split_stage(kbx);
+        int kbg = 0, gg = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const Tile t = decode(tile);
+            double accd[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) accd[j] = 0.0;
+            for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
+                if (kbg + STAGES - 1 < total_kb) split_stage(kbg + STAGES - 1);
+                if ((kb % F) != F - 1 && kb != t.kblocks - 1) continue;  // drain once per group
+                const int b = gg & 1;
+                mbar_wait(&tfull[b], (gg >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + half * 64);
+                uint32_t v[32];
+                tmem_ld32(ta, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) accd[j] += (double)__uint_as_float(v[j]);
+                tmem_ld32(ta + 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&tempty[b]);
+                ++gg;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) accd[32 + j] += (double)__uint_as_float(v[j]);
+            }
+            const int row = t.m0 + qd * 32 + lane;
+            if (row < M) {
+                float* drow = D + (((int64_t)t.q * slices + t.s) * M + row) * ldd + t.n0 + half * 64;
+                const int col0 = t.n0 + half * 64;
+                if (col0 + 64 <= N && (ldd & 3) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 64; j += 4)
+                        *reinterpret_cast<float4*>(drow + j) = make_float4((float)accd[j], (float)accd[j + 1],
+                                                                           (float)accd[j + 2], (float)accd[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (col0 + j < N) drow[j] = (float)accd[j];
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // dW_F from the split-K partials [splits][P2][K][C]: fp64 sum in split order, written in the
 // W_F layout K×C×p×q (layer.hpp:36).
 __global__ void reduce_dw_kernel(const float* __restrict__ part, float* __restrict__ dw, int K, int C, int P2,
