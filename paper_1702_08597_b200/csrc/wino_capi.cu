@@ -779,14 +779,17 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
             kern<<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd,
                                                                                      p->P2, splits, kb_per);
         };
-        auto go_p = [&](auto kern) {
+        static const int epi = std::getenv("WINO_TC_EPI") ? std::atoi(std::getenv("WINO_TC_EPI")) : 16;
+        auto go_p = [&](auto kern, int threads) {
             set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
             const int ctas = std::min(ntiles, p->sm_count);
-            kern<<<ctas, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(
-                ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y, ntiles);
+            kern<<<ctas, threads, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd, p->P2, splits,
+                                                                    kb_per, (int)grid.x, (int)grid.y, ntiles);
         };
-        if (persistent && fold == 1)
-            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1>);
+        if (persistent && fold == 1 && epi == 8)
+            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 8>, 64 + 32 * 8);
+        else if (persistent && fold == 1)
+            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 16>, 64 + 32 * 16);
         else if (fold == 2)
             go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
         else if (fold == 4)

@@ -136,6 +136,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -487,8 +495,8 @@ gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid
 // with the TMA ring, the TMEM double buffer and every barrier phase carried across tiles by
 // global counters, so the prologue (barrier init, TMEM alloc), the pipeline fill and the epilogue
 // store of one tile overlap the next tile's loads and MMAs.  Same arithmetic per tile.
-template <bool A_SPLIT, bool B_MN, int F>
-__global__ void __launch_bounds__(flush::THREADS, 1)
+template <bool A_SPLIT, bool B_MN, int F, int EPI>
+__global__ void __launch_bounds__(64 + 32 * EPI, 1)
 gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
                                     const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N,
                                     int Kd, int64_t ldd, int slices, int splits, int kb_per, int tiles_n,
@@ -523,12 +531,12 @@ gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, c
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&split[i], 256);
+            mbar_init(&split[i], 32 * EPI);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 256);
+            mbar_init(&tempty[i], 32 * EPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -608,16 +616,19 @@ gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, c
             }
         }
     } else {
-        const int t256 = threadIdx.x - 64;
-        const int qd = warp & 3, half = (warp - 2) >> 2;
+        // EPI epilogue warps: warp w reads TMEM lane quarter w % 4 (its sub-partition) and the
+        // column block (w - 2) / 4 of COLS columns
+        constexpr int NT_EPI = 32 * EPI, COLS = BN / (EPI / 4);
+        const int te = threadIdx.x - 64;
+        const int qd = warp & 3, cb = (warp - 2) >> 2;
         int total_kb = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) total_kb += decode(tile).kblocks;
         auto split_stage = [&](int kbx) {
             const int st = kbx % STAGES;
             mbar_wait(&full[st], (kbx / STAGES) & 1);
             uint8_t* base = stage_ptr(st);
-            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t256, 256);
-            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t256, 256);
+            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, te, NT_EPI);
+            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, te, NT_EPI);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&split[st]);
         };
@@ -625,41 +636,42 @@ gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, c
         int kbg = 0, gg = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const Tile t = decode(tile);
-            double accd[64];
+            double accd[COLS];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) accd[j] = 0.0;
+            for (int j = 0; j < COLS; ++j) accd[j] = 0.0;
             for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
                 if (kbg + STAGES - 1 < total_kb) split_stage(kbg + STAGES - 1);
                 if ((kb % F) != F - 1 && kb != t.kblocks - 1) continue;  // drain once per group
                 const int b = gg & 1;
                 mbar_wait(&tfull[b], (gg >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + half * 64);
-                uint32_t v[32];
-                tmem_ld32(ta, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + cb * COLS);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) accd[j] += (double)__uint_as_float(v[j]);
-                tmem_ld32(ta + 32, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&tempty[b]);
+                for (int c = 0; c < COLS; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(ta + c, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c + 16 == COLS) {  // the buffer is free once the last columns are in registers
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mbar_arrive(&tempty[b]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) accd[c + j] += (double)__uint_as_float(v[j]);
+                }
                 ++gg;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) accd[32 + j] += (double)__uint_as_float(v[j]);
             }
             const int row = t.m0 + qd * 32 + lane;
             if (row < M) {
-                float* drow = D + (((int64_t)t.q * slices + t.s) * M + row) * ldd + t.n0 + half * 64;
-                const int col0 = t.n0 + half * 64;
-                if (col0 + 64 <= N && (ldd & 3) == 0) {
+                float* drow = D + (((int64_t)t.q * slices + t.s) * M + row) * ldd + t.n0 + cb * COLS;
+                const int col0 = t.n0 + cb * COLS;
+                if (col0 + COLS <= N && (ldd & 3) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 64; j += 4)
+                    for (int j = 0; j < COLS; j += 4)
                         *reinterpret_cast<float4*>(drow + j) = make_float4((float)accd[j], (float)accd[j + 1],
                                                                            (float)accd[j + 2], (float)accd[j + 3]);
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
+                    for (int j = 0; j < COLS; ++j)
                         if (col0 + j < N) drow[j] = (float)accd[j];
                 }
             }
