@@ -232,8 +232,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         layer.set_dw_mode("tc")
     elif args.dw == "precise":
         layer.set_dw_mode("precise")
-    if args.contraction == "tc" and not dense:
-        layer.set_contraction("tc")
+    if args.contraction != "csr" and not dense:
+        layer.set_contraction(args.contraction)
     cache = layer.new_cache(n)
     x = torch.from_numpy(img).to(dev)
     g_o = torch.from_numpy(go).to(dev)
@@ -436,7 +436,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
                    "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
                              "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else
-                           ("csr" if args.contraction == "csr" else "tcgen05-3xtf32-fp64fold on zero-filled W_F"),
+                           {"csr": "csr", "tc": "tcgen05-3xtf32-fp64fold on zero-filled W_F",
+                            "auto": "auto (tensor cores at density >= 15%, else csr)"}[args.contraction],
                    "dw": {"sddmm": "masked-sddmm-exact", "tc": "tcgen05-3xtf32-fp64fold+mask-gather",
                           "precise": "masked-sddmm-exact on fp32 hi+lo operands"}[args.dw],
                    "l2_flush": "256 MB write between timed steps",
@@ -612,7 +613,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
     ap.add_argument("--separate-bwd", action="store_true",
                     help="backward_weights then backward_input instead of the concurrent wino_backward")
-    ap.add_argument("--contraction", default="csr", choices=["csr", "tc"],
+    ap.add_argument("--contraction", default="csr", choices=["csr", "tc", "auto"],
                     help="sparse plan: CSR kernels (bitwise reference order) or tcgen05 on zero-filled W_F")
     ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise"],
                     help="sparse dW_F: exact masked SDDMM (default) or tensor-core GEMM + mask gather")

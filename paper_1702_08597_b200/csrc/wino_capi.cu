@@ -200,7 +200,9 @@ struct wino_plan {
     bool tc_ready = false;
     bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
     int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather, 2 = precise
-    int contraction = 0;   // sparse plan: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
+    int contraction = 0;   // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
+    int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc + tc dW when dense enough)
+    int auto_permille = 150;   // auto: tensor cores at density >= this / 1000
     int64_t* d_slice_off = nullptr;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
@@ -846,6 +848,8 @@ int check_plan(const wino_plan* p) {
     return WINO_OK;
 }
 
+int apply_contraction(wino_plan* p);
+
 int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<int>& col,
                const std::vector<float>& val) {
     const int K = p->K, C = p->C, P2 = p->P2;
@@ -906,17 +910,37 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     p->has_weights = true;
     p->dense = false;
     plan_sddmm_all(p);
-    if (p->contraction == 1) {
-        const int rc2 = refresh_tc_operands(p, nullptr);
-        if (rc2) return rc2;
-        CUDA_TRY(cudaDeviceSynchronize());
-    }
+    if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
 
 // compress<float> on the device (wino_compress.cuh): W_F f64 is copied to HBM once, CSR + CSC +
 // position map are built there; only the two pointer arrays come back (launch partitioning).
 // keep_all = 1 keeps every coordinate (the dense plan's full CSR).
+// Put the requested contraction into effect for the current weights (sparse plans): auto picks
+// the tensor cores when the density reaches auto_permille/1000 (measured crossover).
+int apply_contraction(wino_plan* p) {
+    if (!p->has_weights || p->dense) return WINO_OK;
+    int eff = p->contraction_mode;
+    if (eff == 2) {
+        const double density = (double)p->nnz / ((double)p->P2 * p->K * p->C);
+        eff = (density * 1000.0 >= p->auto_permille && p->C % 4 == 0 && p->K % 4 == 0) ? 1 : 0;
+    }
+    p->contraction = eff;
+    if (eff == 1) {
+        if (!p->d_slice_off) {
+            CUDA_TRY(cudaMalloc(&p->d_slice_off, p->P2 * sizeof(int64_t)));
+            CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), p->P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
+        }
+        const int rc = refresh_tc_operands(p, nullptr);
+        if (rc) return rc;
+        CUDA_TRY(cudaDeviceSynchronize());
+    } else {
+        p->tc_ready = false;
+    }
+    return WINO_OK;
+}
+
 int compress_from_wsrc(wino_plan* p, double tol, int keep_all);
 
 int device_compress(wino_plan* p, const double* w_host, double tol, int keep_all) {
@@ -1005,11 +1029,7 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     p->has_weights = true;
     p->dense = false;
     plan_sddmm_all(p);
-    if (p->contraction == 1) {
-        const int rc2 = refresh_tc_operands(p, nullptr);
-        if (rc2) return rc2;
-        CUDA_TRY(cudaDeviceSynchronize());
-    }
+    if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
 
@@ -1370,7 +1390,8 @@ static int bwd_dw(wino_plan* p, const wino_cache* c, float* grad_w, cudaStream_t
     float* dwc = grad_w;
     if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
     if (p->dense) dwc = p->d_dwc;
-    if (!p->dense && p->dw_mode == 1 && p->nnz > 0)
+    const bool tc_dw = p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
+    if (!p->dense && tc_dw && p->nnz > 0)
         rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
     else if (precise)
         rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
@@ -1596,20 +1617,17 @@ int wino_recompress(wino_plan* p, double zero_tol) {
 int wino_set_option(wino_plan* p, int option, int value) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
     if (option == WINO_OPT_CONTRACTION) {
-        if (value < 0 || value > 1) return set_err(WINO_INVALID_ARGUMENT, "contraction must be 0 or 1");
+        if (value < 0 || value > 2) return set_err(WINO_INVALID_ARGUMENT, "contraction must be 0, 1 or 2");
         if (value == 1 && (p->C % 4 || p->K % 4))
             return set_err(WINO_CAPABILITY_ERROR, "tensor-core contraction needs C and K multiples of 4 (TMA strides)");
-        p->contraction = value;
-        if (p->has_weights && !p->dense) {
-            if (value == 1) {
-                const int rc = refresh_tc_operands(p, nullptr);
-                if (rc) return rc;
-                CUDA_TRY(cudaDeviceSynchronize());
-            } else {
-                p->tc_ready = false;
-            }
-        }
-        return WINO_OK;
+        p->contraction_mode = value;
+        p->contraction = value == 1 ? 1 : 0;
+        return apply_contraction(p);
+    }
+    if (option == WINO_OPT_AUTO_DENSITY) {
+        if (value < 0 || value > 1000) return set_err(WINO_INVALID_ARGUMENT, "auto density is per mille, 0..1000");
+        p->auto_permille = value;
+        return p->contraction_mode == 2 ? apply_contraction(p) : WINO_OK;
     }
     if (option != WINO_OPT_DW_MODE || value < 0 || value > 2)
         return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");

@@ -208,8 +208,13 @@ class WinogradLayer:
 
     def set_contraction(self, mode: str):
         """Sparse plan contractions: 'csr' (default; the reference's order, forward bitwise equal
-        to sparse_forward<float>) or 'tc' (3xTF32 tcgen05 GEMM over the zero-filled W_F slices)."""
-        check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1}[mode]))
+        to sparse_forward<float>), 'tc' (3xTF32 tcgen05 GEMM over the zero-filled W_F slices) or
+        'auto' (tensor cores, dW included, at density >= set_auto_density's value, else 'csr')."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1, "auto": 2}[mode]))
+
+    def set_auto_density(self, density: float):
+        """Density from which contraction 'auto' uses the tensor cores (default 0.15)."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_AUTO_DENSITY, int(round(density * 1000))))
 
     def weight_values(self):
         """Device pointer (int) of the live CSR values (nnz floats)."""

@@ -642,3 +642,27 @@ def test_range_calls_validate():
     dense.set_weights(np.where(w_f == 0, 0.5, w_f), dense=True)
     with pytest.raises(wb.CapabilityError):
         dense.forward_range(x[0:4], 9, 0, dense.new_cache(9), o[0:4])
+
+
+def test_auto_contraction_follows_density():
+    """contraction 'auto': tensor cores (incl. the tc dW) at density >= the threshold, the CSR path
+    below it (bitwise the default forward), re-decided when the weights change."""
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(with_sparsity(cfg, 0.5), n=2)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    layer.set_contraction("auto")
+    cache = layer.new_cache(2)
+    o = layer.forward(dev(img), cache).cpu().numpy()
+    dw = layer.backward_weights(dev(go), cache).cpu().numpy()
+    di = layer.backward_input(cache).cpu().numpy()
+    o64, dw64, di64 = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
+    assert_parity(o, o64, "auto O (tensor cores)")
+    assert_parity(di, di64, "auto dI (tensor cores)")
+    mask = w_f != 0
+    assert fail_fraction(layer.compact_to_dense(dw.astype(np.float64))[mask], dw64[mask]) < 1e-2
+    # below the threshold: the CSR kernels, bitwise the reference order
+    layer.set_auto_density(0.9)
+    o2 = layer.forward(dev(img)).cpu().numpy()
+    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
+    assert np.array_equal(o2, mir["o"])
