@@ -755,7 +755,6 @@ sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colid
     __syncthreads();
     const int ql = threadIdx.x & 7;
     const int quarter = threadIdx.x >> 3;
-    const unsigned qmask = 0xffu << (threadIdx.x & 24);
     const int nb = e1 - e0;
     const int per = (nb + NQ - 1) / NQ;
     const int qb = e0 + quarter * per;
@@ -795,38 +794,44 @@ sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colid
         else
             partial[(int64_t)blockIdx.z * nnz_total + e] = v;
     };
-    int e = qb;
+    // Warp-uniform trip counts (the longest of the warp's four quarters; a shorter quarter works on
+    // a clamped entry and does not store), so every shuffle below runs converged with a full mask.
+    const int cnt = qe - qb;
+    const int wmax = __reduce_max_sync(kFull, cnt > 0 ? cnt : 0);
+    const int nb4 = wmax >> 2;
     // batches of 4 nonzeros: a 4-value transpose-reduce across the 8 lanes (8 shuffles per batch
     // instead of 6 per nonzero); lanes 2j, 2j+1 end with nonzero j's sum
-    for (; e + 4 <= qe; e += 4) {
+    for (int i = 0; i < nb4; ++i) {
+        const int e = qb + 4 * i;
         double v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = lane_dot(e + j);
+        for (int j = 0; j < 4; ++j) v[j] = lane_dot(min(e + j, e1 - 1));
         {  // o = 4: exchange halves
             const bool hi = (ql & 4) != 0;
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const double send = hi ? v[i] : v[i + 2];
-                const double keep = hi ? v[i + 2] : v[i];
-                v[i] = keep + __shfl_xor_sync(qmask, send, 4);
+            for (int i2 = 0; i2 < 2; ++i2) {
+                const double send = hi ? v[i2] : v[i2 + 2];
+                const double keep = hi ? v[i2 + 2] : v[i2];
+                v[i2] = keep + __shfl_xor_sync(kFull, send, 4);
             }
         }
         {  // o = 2
             const bool hi = (ql & 2) != 0;
             const double send = hi ? v[0] : v[1];
             const double keep = hi ? v[1] : v[0];
-            v[0] = keep + __shfl_xor_sync(qmask, send, 2);
+            v[0] = keep + __shfl_xor_sync(kFull, send, 2);
         }
-        v[0] += __shfl_xor_sync(qmask, v[0], 1);
+        v[0] += __shfl_xor_sync(kFull, v[0], 1);
         // lane ql now holds the sum of nonzero ((ql >> 2) & 1) * 2 + ((ql >> 1) & 1)
-        if ((ql & 1) == 0) put(e + (((ql >> 2) & 1) << 1) + ((ql >> 1) & 1), v[0]);
+        const int eo = e + (((ql >> 2) & 1) << 1) + ((ql >> 1) & 1);
+        if ((ql & 1) == 0 && eo < qe) put(eo, v[0]);
     }
-    for (; e < qe; ++e) {
-        double v = lane_dot(e);
-        v += __shfl_xor_sync(qmask, v, 1);
-        v += __shfl_xor_sync(qmask, v, 2);
-        v += __shfl_xor_sync(qmask, v, 4);
-        if (ql == 0) put(e, v);
+    for (int e = qb + 4 * nb4; e < qb + wmax; ++e) {
+        double v = lane_dot(min(e, e1 - 1));
+        v += __shfl_xor_sync(kFull, v, 1);
+        v += __shfl_xor_sync(kFull, v, 2);
+        v += __shfl_xor_sync(kFull, v, 4);
+        if (ql == 0 && e < qe) put(e, v);
     }
 }
 
