@@ -304,6 +304,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
+    allreduce = None
+    if world > 1 and not fwd_only:  # the one exchange of the step, timed alone
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        dist.barrier()
+        for a, b in evs:
+            a.record()
+            dist.all_reduce(dw)
+            b.record()
+        torch.cuda.synchronize()
+        ar = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / len(evs)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ar, op=dist.ReduceOp.MAX)
+        allreduce = {"ms": float(ar.item()), "bytes": dw.numel() * 4, "share_of_step": float(ar.item()) / ms_max,
+                     "backend": dist.get_backend()}
     passes = 1 if fwd_only else 3
     flops_step = passes * flops_per_image(cfg) * n
     value = world * flops_step / (ms_max * 1e-3) / 1e9
@@ -449,6 +462,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item()), "mode": e2e_mode},
         "gpu_launches": launches,
+        "allreduce": allreduce,
         "launch_mode": graph_note,
         "clocks": clocks,
     }
@@ -550,6 +564,19 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    allreduce = None
+    if world > 1:  # the step's one exchange (the bucket of all layers' dW_F), timed alone
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        dist.barrier()
+        for a, b in evs:
+            a.record()
+            st.bucket.allreduce()
+            b.record()
+        torch.cuda.synchronize()
+        ar = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / len(evs)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ar, op=dist.ReduceOp.MAX)
+        allreduce = {"ms": float(ar.item()), "bytes": st.bucket.flat.numel() * 4,
+                     "share_of_step": float(ar.item()) / ms_max, "backend": dist.get_backend()}
     passes = 3 * layers - 1
     value = passes * flops_per_image(cfg) * n_global / (ms_max * 1e-3) / 1e9
     # end to end: host shard in, reduced gradient bucket out
@@ -594,7 +621,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
         "e2e": {"value": passes * flops_per_image(cfg) * n_global / (float(t2.item()) * 1e-3) / 1e9,
                 "unit": "GFLOP/s", "h2d_bytes_per_step": (h_img.numel() + h_go.numel()) * 4,
                 "d2h_bytes_per_step": h_b.numel() * 4, "ms_per_step": float(t2.item())},
-        "gpu_launches": launches, "launch_mode": graph_note, "clocks": clocks,
+        "gpu_launches": launches, "launch_mode": graph_note, "clocks": clocks, "allreduce": allreduce,
     }
     print(json.dumps(line), flush=True)
 

@@ -12,7 +12,7 @@ __global__ void conv_kernel(const float* in, double* out, int iters) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             acc[i] = acc[i] * 0.5 + (double)x[i];   // one F2F + one DFMA per element
-            x[i] = __int_as_float(__float_as_int(x[i]) ^ 1);  // keep x live and changing (ALU)
+            x[i] = fmaf(x[i], 1.0001f, 1e-7f);  // a new value every iteration: no conversion can be hoisted
         }
     }
     double s = 0;
