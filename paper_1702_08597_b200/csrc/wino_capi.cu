@@ -231,6 +231,7 @@ struct wino_cache {
     int64_t NTs = 0;
     float* V = nullptr;
     float* DZ = nullptr;
+    int dw_chunks = 0;      // SDDMM chunks whose dW partials backward_range already computed
     float* Vlo = nullptr;   // precise dW mode: fp32 residuals of Ĩ_F and dZ
     float* DZlo = nullptr;
     bool has_fwd = false;
@@ -505,10 +506,10 @@ void plan_sddmm_chunk(wino_plan* p) {
 
 template <int TW>
 void launch_sddmm_chunk_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
-                          const float* V, float* dW, double* partial, int NTs) {
+                          const float* V, float* dW, double* partial, int NTs, int z0 = 0) {
     set_smem_attr(wino::sddmm_chunk_kernel<TW, kChunkThreads>, (int)smem);
     wino::sddmm_chunk_kernel<TW, kChunkThreads><<<grid, kChunkThreads, smem, st>>>(
-        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NTs, p->lane_rows);
+        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NTs, p->lane_rows, z0);
 }
 
 template <int R, int MAXB, int STAGES, bool LO>
@@ -539,25 +540,27 @@ double* ensure_partial(wino_plan* p, size_t need, int* rc) {
     return p->d_partial;
 }
 
+// chunks [z0, z1) of the batch (default: all) -> fp64 partials; finish = sum them into dW
 int launch_sddmm_chunk(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
-                       int64_t NTs) {
+                       int64_t NTs, int z0 = 0, int z1 = -1, bool finish = true) {
     const int TW = p->lane_tw;
     const size_t smem = (size_t)(p->C + p->lane_rows) * TW * 4;
     const int groups = (p->K + p->lane_rows - 1) / p->lane_rows;
     const int chunks = (int)((NT + TW - 1) / TW);
+    if (z1 < 0) z1 = chunks;
     int rc = WINO_OK;
     double* partial = chunks > 1 ? ensure_partial(p, (size_t)chunks * p->nnz, &rc) : nullptr;
     if (rc) return rc;
-    const dim3 grid(groups, p->P2, chunks);
-    {
+    if (z1 > z0) {
+        const dim3 grid(groups, p->P2, z1 - z0);
         Launch L(p, st, K_SDDMM);
         if (TW == 128)
-            launch_sddmm_chunk_v<128>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs);
+            launch_sddmm_chunk_v<128>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs, z0);
         else
-            launch_sddmm_chunk_v<64>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs);
+            launch_sddmm_chunk_v<64>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs, z0);
         if ((rc = L.done())) return rc;
     }
-    if (chunks > 1) {
+    if (chunks > 1 && finish) {
         Launch L(p, st, K_SDDMM);
         wino::split_sum_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(partial, dW, p->nnz, chunks);
         return L.done();
@@ -1530,6 +1533,20 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
                           r.NTr)))
         return rc;
     if ((rc = DISPATCH_MP(p, launch_input_grad, p, st, DV, grad_input, n1 - n0, r.NTs))) return rc;
+    // dW_F partials of this range's t chunks, when the range is whole chunks of the chunk-form
+    // SDDMM (backward_weights_cached then only sums the chunks)
+    const int64_t NTfull = (int64_t)c->n * p->g.t;
+    if (p->sddmm_impl == 1 && p->dw_mode == 0 && !p->dense && p->nnz > 0 && p->lane_tw > 0) {
+        const int TW = p->lane_tw;
+        const int chunks = (int)((NTfull + TW - 1) / TW);
+        const bool last = n1 == c->n;
+        if (chunks > 1 && r.a % TW == 0 && (last || (r.a + r.NT) % TW == 0)) {
+            const int z0 = (int)(r.a / TW), z1 = last ? chunks : (int)((r.a + r.NT) / TW);
+            if ((rc = launch_sddmm_chunk(p, st, c->DZ, c->V, nullptr, NTfull, r.NTs, z0, z1, false))) return rc;
+            if (z0 == 0) c->dw_chunks = 0;
+            c->dw_chunks += z1 - z0;
+        }
+    }
     c->has_grad_z = true;
     return WINO_OK;
 }
@@ -1540,6 +1557,15 @@ int wino_backward_weights_cached(wino_plan* p, wino_cache* c, float* grad_w, voi
     if (!c || (!grad_w && p->nnz > 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (c->plan != p || !c->has_fwd || !c->has_grad_z)
         return set_err(WINO_CONSISTENCY_ERROR, "backward_weights_cached: dL/dZ missing; run backward_range first");
+    const int64_t NTfull = (int64_t)c->n * p->g.t;
+    if (p->sddmm_impl == 1 && p->dw_mode == 0 && !p->dense && p->lane_tw > 0 && p->nnz > 0 &&
+        c->dw_chunks == (int)((NTfull + p->lane_tw - 1) / p->lane_tw)) {
+        // every chunk's partials came from the ranges: only their ordered sum remains
+        const int rc2 = launch_sddmm_chunk(p, (cudaStream_t)stream, c->DZ, c->V, grad_w, NTfull, c->NTs, 0, 0, true);
+        c->dw_chunks = 0;
+        return rc2;
+    }
+    c->dw_chunks = 0;
     return bwd_dw(p, c, grad_w, (cudaStream_t)stream);
 }
 

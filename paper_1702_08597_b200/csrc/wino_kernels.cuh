@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                    const int* __restrict__ rowof, const float* __restrict__ DZ,
                    const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
-                   int64_t nnz_total, int K, int C, int NTs, int rows_per_block) {
+                   int64_t nnz_total, int K, int C, int NTs, int rows_per_block, int z0) {
     constexpr int Q = TW / 32;  // LDS.128 steps per lane per nonzero
     constexpr int NQ = THREADS / 8;
     extern __shared__ float4 smem_f4[];
@@ -745,7 +745,8 @@ sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colid
     const int nrb = r1 - r0;
     const int* rp = rowptr + (int64_t)s * (K + 1);
     const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
-    const int t0 = blockIdx.z * TW;
+    const int zc = z0 + (int)blockIdx.z;  // t chunk (a column range of the batch starts at chunk z0)
+    const int t0 = zc * TW;
     float* vs = reinterpret_cast<float*>(smem_f4);
     float* zs = vs + C * TW;
     stage_rows_async<TW>(V + (int64_t)s * C * NTs, vs, C, NTs, t0);
@@ -792,7 +793,7 @@ sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colid
         if (partial == nullptr)
             dW[e] = (float)v;
         else
-            partial[(int64_t)blockIdx.z * nnz_total + e] = v;
+            partial[(int64_t)zc * nnz_total + e] = v;
     };
     // Warp-uniform trip counts (the longest of the warp's four quarters; a shorter quarter works on
     // a clamped entry and does not store), so every shuffle below runs converged with a full mask.
