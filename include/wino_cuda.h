@@ -139,9 +139,15 @@ WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, co
                           wino_cache* cache, float* grad_w, int flags, void* stream);
 /* backward_weights + backward_input in one call: dZ first, then dW_F on an internal stream
  * concurrently with dĨ_F -> dI on `stream` (they share only the read-only dZ and Ĩ_F); `stream`
- * waits for both before the call's work is complete.  Same results as the two calls. */
+ * waits for both before the call's work is complete.  Same results as the two calls.
+ * grad_input may be NULL (no dI: the first layer of a stack, train.cpp:201). */
 WINO_API int wino_backward(wino_plan* plan, const float* grad_output, const float* relu_out,
                            wino_cache* cache, float* grad_w, float* grad_input, int flags, void* stream);
+/* The data-parallel exchange: sum grad_w (count floats; count < 0 = this plan's
+ * dW_F length, nnz-compact or K×C×p×q) in place over an NCCL communicator (`nccl_comm` is an
+ * ncclComm_t), on `stream`.  The scale 1/N_global of train.cpp:166,200 stays with the update.
+ * NCCL is resolved at run time (already-loaded libnccl.so.2 first); WINO_CAPABILITY_ERROR if none. */
+WINO_API int wino_allreduce_dw(wino_plan* plan, void* nccl_comm, float* grad_w, int64_t count, void* stream);
 /* Image ranges of one batch of n_total images, for overlapping host transfers with compute
  * (the CSR kernels only).  forward_range computes images [n0, n1) into the batch's cache (input
  * and output point at image n0); backward_range computes their dL/dZ, dĨ_F and dI (grad_output,

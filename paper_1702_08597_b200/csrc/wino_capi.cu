@@ -1,6 +1,7 @@
 // C-ABI implementation of include/wino_cuda.h: the drop-in boundary between the
 // reference's layer API (layer.hpp:28-43, sparse.hpp:40-82) and the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1438,8 +1439,12 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
                   float* grad_input, int flags, void* stream) {
     int rc = bwd_check(p, grad_output, relu_out, c, grad_w, flags);
     if (rc) return rc;
-    if (!grad_input) return set_err(WINO_INVALID_ARGUMENT, "null grad_input");
     cudaStream_t st = (cudaStream_t)stream;
+    if (!grad_input) {  // no dI wanted (the first layer of a stack, train.cpp:201): dW only
+        if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
+        c->has_grad_z = true;
+        return bwd_dw(p, c, grad_w, st);
+    }
     if (!p->side) {
         CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
@@ -1567,6 +1572,42 @@ int wino_backward_weights_cached(wino_plan* p, wino_cache* c, float* grad_w, voi
     }
     c->dw_chunks = 0;
     return bwd_dw(p, c, grad_w, (cudaStream_t)stream);
+}
+
+// ---- the data-parallel exchange: one in-place sum of dW_F over an NCCL communicator ----
+// NCCL is resolved at run time (the process's already-loaded libnccl, e.g. PyTorch's, else the
+// system one), so the library has no link-time NCCL dependency.  ABI constants of nccl.h:
+// ncclFloat32 = 7, ncclSum = 0, ncclSuccess = 0.
+namespace {
+using nccl_allreduce_t = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+using nccl_errstr_t = const char* (*)(int);
+nccl_allreduce_t g_nccl_allreduce = nullptr;
+nccl_errstr_t g_nccl_errstr = nullptr;
+std::once_flag g_nccl_once;
+
+void resolve_nccl() {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    g_nccl_allreduce = reinterpret_cast<nccl_allreduce_t>(dlsym(h, "ncclAllReduce"));
+    g_nccl_errstr = reinterpret_cast<nccl_errstr_t>(dlsym(h, "ncclGetErrorString"));
+}
+}  // namespace
+
+int wino_allreduce_dw(wino_plan* p, void* nccl_comm, float* grad_w, int64_t count, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!nccl_comm || (!grad_w && count != 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    if (count < 0) count = p->dense ? (int64_t)p->P2 * p->K * p->C : p->nnz;
+    if (count == 0) return WINO_OK;
+    std::call_once(g_nccl_once, resolve_nccl);
+    if (!g_nccl_allreduce) return set_err(WINO_CAPABILITY_ERROR, "allreduce_dw: libnccl.so.2 not found");
+    const int r = g_nccl_allreduce(grad_w, grad_w, (size_t)count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, nccl_comm,
+                                   (cudaStream_t)stream);
+    if (r != 0)
+        return set_err(WINO_CUDA_ERROR, std::string("ncclAllReduce: ") + (g_nccl_errstr ? g_nccl_errstr(r) : "error"));
+    return WINO_OK;
 }
 
 int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, void* stream) {

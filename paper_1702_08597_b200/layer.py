@@ -270,8 +270,15 @@ class WinogradLayer:
                                           _stream_ptr(stream)))
         return out
 
-    def backward(self, grad_o, cache: ForwardCache, relu_out=None, out_w=None, out_i=None, stream=None):
-        """backward_weights + backward_input in one call, dW_F computed concurrently with dI."""
+    def allreduce_dw(self, grad_w, nccl_comm: int, count: int = -1, stream=None):
+        """Sum grad_w in place over an NCCL communicator (an ncclComm_t address)."""
+        check(lib().wino_allreduce_dw(self._h, C.c_void_p(nccl_comm), _dptr(grad_w), count, _stream_ptr(stream)))
+        return grad_w
+
+    def backward(self, grad_o, cache: ForwardCache, relu_out=None, out_w=None, out_i=None, stream=None,
+                 want_input_grad: bool = True):
+        """backward_weights + backward_input in one call, dW_F computed concurrently with dI
+        (want_input_grad=False: dW_F only, as for the first layer of a stack)."""
         import torch
 
         n = cache.n
@@ -280,7 +287,7 @@ class WinogradLayer:
             self._check_dev(relu_out, (n, self.k, self.ho, self.wo), "relu_out")
         if out_w is None:
             out_w = torch.empty(self.grad_w_shape(), device=grad_o.device, dtype=torch.float32)
-        if out_i is None:
+        if out_i is None and want_input_grad:
             out_i = torch.empty((max(n, 1), self.c, self.h, self.w), device=grad_o.device, dtype=torch.float32)
         check(lib().wino_backward(self._h, _dptr(grad_o), _dptr(relu_out), cache._h, _dptr(out_w), _dptr(out_i),
                                   _lib.WINO_BWD_RELU_MASK if relu_out is not None else 0, _stream_ptr(stream)))

@@ -223,3 +223,64 @@ def test_winograd_conv2d_optimizer_updates_live_weights():
     lay = wb.WinogradLayer(4, 8, 9, 9, pad=1, m=4)
     lay.set_weights(after)
     assert torch.equal(out, lay.forward(x, relu=True))
+
+
+def _nccl():
+    import ctypes
+    import os
+    import site
+
+    try:
+        return ctypes.CDLL("libnccl.so.2", mode=os.RTLD_NOLOAD | os.RTLD_NOW)
+    except OSError:
+        for sp in site.getsitepackages():
+            p = os.path.join(sp, "nvidia", "nccl", "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return ctypes.CDLL(p, mode=os.RTLD_GLOBAL)
+        return ctypes.CDLL("libnccl.so.2", mode=os.RTLD_GLOBAL)
+
+
+def test_allreduce_dw_over_a_single_rank_communicator():
+    """wino_allreduce_dw through a real (one-rank) NCCL communicator: the sum over one rank is the
+    identity, in place, on the given stream; the default count is the plan's dW length."""
+    import ctypes
+
+    nccl = _nccl()
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    nccl.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, UniqueId, ctypes.c_int]
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    try:
+        cfg = CONFIGS["c0"]
+        _, w_f, _ = make_inputs(cfg, n=1)
+        layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+        layer.set_weights(w_f)
+        g = torch.randn(layer.nnz, device="cuda")
+        want = g.clone()
+        layer.allreduce_dw(g, comm.value)
+        torch.cuda.synchronize()
+        assert torch.equal(g, want)
+        bucket = torch.randn(3 * layer.nnz, device="cuda")  # a bucket of several layers: explicit count
+        want = bucket.clone()
+        layer.allreduce_dw(bucket, comm.value, count=bucket.numel())
+        torch.cuda.synchronize()
+        assert torch.equal(bucket, want)
+    finally:
+        nccl.ncclCommDestroy(comm)
+
+
+def test_backward_without_input_gradient():
+    cfg = CONFIGS["c0"]
+    img, w_f, go = make_inputs(cfg, n=2)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f)
+    cache = layer.new_cache(2)
+    layer.forward(dev(img), cache)
+    dw_ref = layer.backward_weights(dev(go), cache)
+    dw, di = layer.backward(dev(go), cache, want_input_grad=False)
+    assert di is None and torch.equal(dw, dw_ref)
