@@ -222,3 +222,10 @@ def threshold_to_density(w, density):
 def checkpoint_roundtrip(dir_in, dir_out):
     """The reference loads dir_in and saves what it loaded to dir_out."""
     _check(lib().wref_checkpoint_roundtrip(str(dir_in).encode(), str(dir_out).encode()))
+
+
+def train_steps(seed, steps, batch, mode=0):
+    """The reference trainer: losses of `steps` train_step calls on its toy Winograd network."""
+    out = np.zeros(steps)
+    _check(lib().wref_train_steps(C.c_ulonglong(seed), steps, batch, mode, _ptr(out)))
+    return out

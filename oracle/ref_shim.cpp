@@ -327,4 +327,23 @@ int wref_checkpoint_roundtrip(const char* dir_in, const char* dir_out) {
     GUARD({ harness::save_checkpoint(dir_out, harness::load_checkpoint(dir_in)); })
 }
 
+
+// The reference's own trainer: `steps` plain-mode SGD steps of make_toy_network (Winograd
+// domain) on synth_dataset, minibatches in order; losses[i] = train_step's minibatch loss.
+int wref_train_steps(unsigned long long seed, int steps, int batch, int mode, double* losses) {
+    GUARD({
+        train::Network net = train::make_toy_network(seed, train::Domain::winograd);
+        for (auto& conv : net.convs) conv.lambda = mode == 1 ? 1e-3 : 0.0;
+        train::Dataset data = train::synth_dataset(seed, (std::size_t)(steps * batch));
+        train::PruneConfig cfg;
+        cfg.batch_size = (std::size_t)batch;
+        const train::StepMode sm = mode == 1 ? train::StepMode::prune : train::StepMode::plain;
+        for (int s = 0; s < steps; ++s) {
+            std::vector<std::size_t> idx;
+            for (int b = 0; b < batch; ++b) idx.push_back((std::size_t)(s * batch + b));
+            losses[s] = train::train_step(net, data, idx, cfg, cfg.base_lr, sm);
+        }
+    })
+}
+
 }  // extern "C"

@@ -1,0 +1,248 @@
+// The reference's C++ layer API (include/wino/layer.hpp:28-43, include/wino/sparse.hpp:77-82)
+// served by the B200 C-ABI (include/wino_cuda.h).  Compiled in place of the reference's
+// src/layer.cpp; the reference's headers, types and callers stay unchanged — the trainer
+// (train.cpp), the pybind11 module and the CLI pick these definitions up at link time.
+//
+//   winograd_forward / _backward_weights / _backward_input : a dense plan in the exact
+//       (reference-order SIMT) mode; f64 host tensors are cast to fp32 at the edge, as the
+//       reference's own f32 path casts them (sparse.cpp:99-100, 181)
+//   sparse_forward<float>  : a CSR plan from the caller's PointwiseCsr (validated), batched
+//   lift_spatial_weights   : G1·W·G2ᵀ on the host (tiny)
+//
+// ForwardCache has no field for device state, so the shim keeps the device plan + cache of each
+// ForwardCache in a side table keyed by its address (a cache is never shared across threads,
+// SPEC.md:316-317); forward refreshes the entry, and k/c/t/p/q are filled as the reference fills
+// them so check_cache keeps its semantics.  Status codes map back onto the reference's
+// exception classes.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <unordered_map>
+#include <vector>
+
+#include "wino/layer.hpp"
+#include "wino/sparse.hpp"
+#include "wino_cuda.h"
+
+namespace wino {
+namespace {
+
+void check(int rc) {
+    if (rc == WINO_OK) return;
+    const std::string m = wino_last_error();
+    switch (rc) {
+        case WINO_SHAPE_ERROR: throw ShapeError(m);
+        case WINO_CONSISTENCY_ERROR: throw ConsistencyError(m);
+        case WINO_CORRUPT_FORMAT: throw CorruptFormatError(m);
+        case WINO_CAPABILITY_ERROR: throw CapabilityError(m);
+        default: throw std::runtime_error(m);
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// fp32 device buffer filled from / read back into an f64 host Tensor
+struct DevBuf {
+    float* p = nullptr;
+    size_t n = 0;
+    explicit DevBuf(size_t n_) : n(n_) { cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)), "cudaMalloc"); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { cudaFree(p); }
+    void upload(const std::vector<double>& h) {
+        std::vector<float> f(h.begin(), h.end());
+        cuda_check(cudaMemcpy(p, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice), "H2D");
+    }
+    void download(std::vector<double>& h) const {
+        std::vector<float> f(n);
+        cuda_check(cudaMemcpy(f.data(), p, n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+        h.assign(f.begin(), f.end());
+    }
+};
+
+struct Plan {
+    wino_plan* plan = nullptr;
+    ~Plan() {
+        if (plan) wino_plan_destroy(plan);
+    }
+};
+
+std::unique_ptr<Plan> make_plan(const TransformSet& t, const TileGeometry& g, size_t k) {
+    if (t.m != t.n || t.r != t.s) throw CapabilityError("the B200 layer builds square tiles and kernels only");
+    wino_layer_desc d{};
+    d.c = (int)g.c;
+    d.k = (int)k;
+    d.h = (int)g.h_i;
+    d.w = (int)g.w_i;
+    d.pad = 0;  // the reference's geometry is already the (padded) input
+    d.m = (int)t.m;
+    d.r = (int)t.r;
+    d.a = t.a1.entries().data();
+    d.b = t.b1.entries().data();
+    d.device = 0;
+    auto p = std::make_unique<Plan>();
+    check(wino_plan_create(&d, &p->plan));
+    return p;
+}
+
+struct DeviceCache {
+    std::unique_ptr<Plan> plan;
+    wino_cache* cache = nullptr;
+    ~DeviceCache() {
+        if (cache) wino_cache_destroy(cache);
+    }
+};
+
+std::mutex g_mu;
+// never destroyed: at process exit the CUDA context may already be gone
+auto& g_caches = *new std::unordered_map<const ForwardCache*, std::unique_ptr<DeviceCache>>();
+
+DeviceCache* find_cache(const ForwardCache& c) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_caches.find(&c);
+    return it == g_caches.end() ? nullptr : it->second.get();
+}
+
+void check_cache(const ForwardCache& cache, const TileGeometry& geom) {  // layer.cpp:22-25
+    if (cache.t != geom.t || cache.p != geom.p || cache.q != geom.q || cache.c != geom.c)
+        throw ConsistencyError("forward cache does not match the given geometry");
+}
+
+}  // namespace
+
+// number of layer calls served by the GPU (tests check that the reference API really lands here)
+std::atomic<long long> shim_gpu_calls{0};
+
+Tensor lift_spatial_weights(const Tensor& w, const TransformSet& tset) {
+    if (w.rank() != 4 || w.extent(2) != tset.r || w.extent(3) != tset.s)
+        throw ShapeError("lift_spatial_weights: kernel " + shape_str(w.shape()) +
+                         " inconsistent with transform r,s = " + shape_str({tset.r, tset.s}));
+    const size_t kn = w.extent(0), cn = w.extent(1), p = tset.p, q = tset.q, r = tset.r, s = tset.s;
+    Tensor w_f({kn, cn, p, q});
+    const auto& g1 = tset.g1.entries();  // p x r
+    const auto& g2 = tset.g2.entries();  // q x s
+    for (size_t k = 0; k < kn; ++k)
+        for (size_t c = 0; c < cn; ++c)
+            for (size_t i = 0; i < p; ++i)
+                for (size_t j = 0; j < q; ++j) {
+                    double acc = 0.0;
+                    for (size_t u = 0; u < r; ++u)
+                        for (size_t v = 0; v < s; ++v) acc += g1[i * r + u] * w(k, c, u, v) * g2[j * s + v];
+                    w_f(k, c, i, j) = acc;
+                }
+    return w_f;
+}
+
+Tensor winograd_forward(const Tensor& img, const Tensor& w_f, const TransformSet& tset, const TileGeometry& geom,
+                        ForwardCache* cache, OpCounter* /*counter*/) {
+    ++shim_gpu_calls;
+    if (w_f.rank() != 4 || w_f.extent(2) != tset.p || w_f.extent(3) != tset.q)
+        throw ShapeError("winograd_forward: weights " + shape_str(w_f.shape()) +
+                         " inconsistent with transform p,q = " + shape_str({tset.p, tset.q}));
+    if (w_f.extent(1) != geom.c)
+        throw ShapeError("winograd_forward: weights expect " + std::to_string(w_f.extent(1)) +
+                         " channels, image has " + std::to_string(geom.c));
+    if (img.rank() != 3 || img.extent(0) != geom.c || img.extent(1) != geom.h_i || img.extent(2) != geom.w_i)
+        throw ShapeError("winograd_forward: image " + shape_str(img.shape()) + " does not match the geometry");
+    const size_t kn = w_f.extent(0);
+    auto dc = std::make_unique<DeviceCache>();
+    dc->plan = make_plan(tset, geom, kn);
+    check(wino_set_weights(dc->plan->plan, w_f.data().data(), 0.0, /*exact dense*/ 1));
+    check(wino_cache_create(dc->plan->plan, 1, &dc->cache));
+    DevBuf in(img.size()), out(kn * geom.h_o * geom.w_o);
+    in.upload(img.data());
+    check(wino_forward(dc->plan->plan, 1, in.p, out.p, dc->cache, 0, nullptr));
+    Tensor o({kn, geom.h_o, geom.w_o});
+    out.download(o.data());
+    if (cache) {
+        cache->k = kn;
+        cache->c = geom.c;
+        cache->t = geom.t;
+        cache->p = geom.p;
+        cache->q = geom.q;
+        cache->grad_z.reset();  // layer.cpp:88: a new forward invalidates dL/dZ
+        std::lock_guard<std::mutex> lock(g_mu);
+        g_caches[cache] = std::move(dc);
+    }
+    return o;
+}
+
+Tensor winograd_backward_weights(const Tensor& grad_o, ForwardCache& cache, const TransformSet& /*tset*/,
+                                 const TileGeometry& geom) {
+    ++shim_gpu_calls;
+    check_cache(cache, geom);
+    DeviceCache* dc = find_cache(cache);
+    if (!dc) throw ConsistencyError("forward cache does not match the given geometry");
+    const size_t kn = cache.k;
+    if (grad_o.rank() != 3 || grad_o.extent(0) != kn || grad_o.extent(1) != geom.h_o || grad_o.extent(2) != geom.w_o)
+        throw ShapeError("backward_weights: upstream gradient " + shape_str(grad_o.shape()) +
+                         " does not match output " + shape_str({kn, geom.h_o, geom.w_o}));
+    DevBuf go(grad_o.size()), dw(kn * cache.c * geom.p * geom.q);
+    go.upload(grad_o.data());
+    check(wino_backward_weights(dc->plan->plan, go.p, nullptr, dc->cache, dw.p, 0, nullptr));
+    Tensor gw({kn, cache.c, geom.p, geom.q});
+    dw.download(gw.data());
+    cache.grad_z = Tensor();  // dL/dZ lives in the device cache; the flag is what layer.cpp:137 checks
+    return gw;
+}
+
+Tensor winograd_backward_input(const ForwardCache& cache, const Tensor& w_f, const TransformSet& /*tset*/,
+                               const TileGeometry& geom) {
+    ++shim_gpu_calls;
+    check_cache(cache, geom);
+    if (!cache.grad_z) throw ConsistencyError("backward_input: dL/dZ missing; run backward_weights first");
+    DeviceCache* dc = find_cache(cache);
+    if (!dc) throw ConsistencyError("forward cache does not match the given geometry");
+    if (w_f.extent(0) != cache.k || w_f.extent(1) != cache.c)
+        throw ShapeError("backward_input: weights " + shape_str(w_f.shape()) + " do not match cache");
+    // the weights of this call (normally the forward's) drive dĨ_F = W_Fᵀ·dZ
+    check(wino_set_weights(dc->plan->plan, w_f.data().data(), 0.0, 1));
+    DevBuf di(geom.c * geom.h_i * geom.w_i);
+    check(wino_backward_input(dc->plan->plan, dc->cache, di.p, nullptr));
+    Tensor gi({geom.c, geom.h_i, geom.w_i});
+    di.download(gi.data());
+    return gi;
+}
+
+// Explicit specialization: overrides the template instantiation sparse.cpp emits for float.
+template <>
+Tensor sparse_forward<float>(const Tensor& batch, const PointwiseCsr<float>& csr, const TransformSet& tset,
+                             const TileGeometry& geom, unsigned /*workers*/, OpCounter* /*counter*/) {
+    ++shim_gpu_calls;
+    if (batch.rank() != 4 || batch.extent(1) != geom.c || batch.extent(2) != geom.h_i || batch.extent(3) != geom.w_i)
+        throw ShapeError("sparse_forward: batch " + shape_str(batch.shape()) + " does not match the geometry");
+    if (csr.c != geom.c || csr.p != tset.p || csr.q != tset.q)
+        throw ShapeError("sparse_forward: CSR does not match the geometry");
+    const size_t n = batch.extent(0), kn = csr.k, p2 = csr.p * csr.q;
+    auto plan = make_plan(tset, geom, kn);
+    if (csr.slices.size() != p2) throw CorruptFormatError("sparse_forward: expected p*q CSR slices");
+    std::vector<std::vector<uint64_t>> rp(p2), ci(p2);
+    std::vector<const uint64_t*> prp(p2), pci(p2);
+    std::vector<const float*> pv(p2);
+    std::vector<uint64_t> nnz(p2);
+    for (size_t s = 0; s < p2; ++s) {
+        const auto& sl = csr.slices[s];
+        rp[s].assign(sl.row_ptr.begin(), sl.row_ptr.end());
+        ci[s].assign(sl.col_idx.begin(), sl.col_idx.end());
+        if (rp[s].size() != kn + 1) throw CorruptFormatError("sparse_forward: row_ptr length != K+1");
+        prp[s] = rp[s].data();
+        pci[s] = ci[s].data();
+        pv[s] = sl.values.data();
+        nnz[s] = sl.values.size();
+    }
+    check(wino_set_weights_csr(plan->plan, prp.data(), pci.data(), pv.data(), nnz.data()));
+    DevBuf in(batch.size()), out(n * kn * geom.h_o * geom.w_o);
+    in.upload(batch.data());
+    check(wino_forward(plan->plan, (int)n, in.p, out.p, nullptr, 0, nullptr));
+    Tensor o({n, kn, geom.h_o, geom.w_o});
+    out.download(o.data());
+    return o;
+}
+
+}  // namespace wino
