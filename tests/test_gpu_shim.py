@@ -107,3 +107,46 @@ def test_reference_trainer_runs_on_the_gpu(mode):
     calls = lib.shim_gpu_call_count() - before
     assert calls >= steps * batch * 2 * 2  # ≥ forward + backward_weights per conv layer per sample
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-6)
+
+
+# -- the reference's own pybind11 module (python/bindings.cpp) built over the shim ----------------
+def _module():
+    import importlib
+    import sys
+
+    build = str(SHIM.parent)
+    if not any(p.name.startswith("_wino") for p in SHIM.parent.glob("_wino*.so")):
+        pytest.skip("shim/_build/_wino not built")
+    if build not in sys.path:
+        sys.path.insert(0, build)
+    return importlib.import_module("_wino")
+
+
+@pytest.mark.gpu
+def test_reference_python_module_on_the_gpu():
+    """bindings.cpp unchanged, its layer calls served by the GPU: conv_winograd against the
+    reference's direct convolution, conv_winograd_grad and sparse_conv against the reference on
+    the CPU, worker-count invariance, and the reference's error mapping."""
+    wino = _module()
+    rng = np.random.default_rng(0)
+    img = rng.standard_normal((3, 9, 11))
+    w = rng.standard_normal((2, 3, 3, 3))
+    for m in (2, 4):
+        w_f = wino.lift(w, m=m)
+        np.testing.assert_allclose(wino.conv_winograd(img, w_f, m=m), wino.conv_direct(img, w), atol=1e-4)
+    img = rng.standard_normal((2, 10, 10))
+    w_f = rng.standard_normal((3, 2, 6, 6))
+    go = rng.standard_normal((3, 8, 8))
+    gw, gi = wino.conv_winograd_grad(img, w_f, go, m=4)
+    want = ref.layer(img, w_f, go, m=4)
+    assert_parity(gw, want["grad_wf"], "module dW_F")
+    assert_parity(gi, want["grad_in"], "module dI")
+    batch = rng.standard_normal((3, 2, 10, 10))
+    w_f[np.abs(w_f) < 0.8] = 0.0
+    out = wino.sparse_conv(batch, w_f, m=4, workers=1, precision="f32")  # GPU (the shim)
+    assert np.array_equal(out, wino.sparse_conv(batch, w_f, m=4, workers=4, precision="f32"))
+    assert np.array_equal(out, ref.sparse_forward(batch, w_f, m=4, workers=1, precision=32))
+    # the module's default precision is f64: the reference's own CPU path, untouched by the shim
+    assert np.array_equal(wino.sparse_conv(batch, w_f, m=4), ref.sparse_forward(batch, w_f, m=4, precision=64))
+    with pytest.raises(ValueError):
+        wino.conv_winograd(rng.standard_normal((4, 10, 10)), w_f, m=4)
