@@ -389,10 +389,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
     pk = peaks()
     kb = kernel_bytes(cfg, layer, n)
     kernels = {}
+    # a kind can launch more than once per step (SDDMM + its split_sum, the dW GEMM + its fp64
+    # reduce): times and achieved bandwidth are per STEP of the kind (3 profiled steps), i.e. the
+    # algorithmic bytes of one pass over the kernel's data ÷ all of that pass's launches
     for name, (tot_ms, cnt) in prof.items():
-        avg = tot_ms / max(cnt, 1)
+        avg = tot_ms / 3
         bytes_ = kb.get(name)
-        kernels[name] = {"ms_per_launch": avg, "launches": cnt,
+        kernels[name] = {"ms_per_step": avg, "launches_per_step": cnt / 3,
                          "share": tot_ms / sum(v[0] for v in prof.values())}
         if bytes_:
             kernels[name]["alg_bytes"] = bytes_
@@ -407,19 +410,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
         # taken as half the measured bf16 GEMM peak (MEASURED_PEAKS.json)
         g = layer.geometry
         useful = 2.0 * (g["p"] ** 2) * cfg.k * cfg.c * n * g["t"]
-        avg_s = prof[dom][0] / max(prof[dom][1], 1) * 1e-3
+        avg_s = prof[dom][0] / 3 * 1e-3
         issued_tf = 3 * useful / avg_s / 1e12
         peak_tf = pk["bf16_tflops"] / 2
         roofline = {"bound": "tensor", "kernel": dom, "achieved": issued_tf, "peak": peak_tf,
                     "unit": "TFLOP/s", "frac": issued_tf / peak_tf, "traffic": traffic,
                     "peak_source": pk["source"] + " (bf16/2 for tf32)",
-                    "note": "issued TF32 FLOP/s of the 3xTF32 GEMM (useful = 1/3)"}
+                    "note": "issued TF32 FLOP/s of the 3xTF32 GEMM (useful = 1/3); time = the kind's launches per step"}
     else:
         dom_gbs = kernels[dom].get("GBps")
         roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": pk["hbm_gbs"],
                     "unit": "GB/s", "frac": (dom_gbs / pk["hbm_gbs"]) if dom_gbs else None,
                     "traffic": traffic, "peak_source": pk["source"],
-                    "note": ("per-launch algorithmic bytes / CUDA-event time on the launching stream; "
+                    "note": ("algorithmic bytes per step / CUDA-event time of the kind's launches in the step (on the launching stream); "
                              "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
     # the on-chip pipe that bounds the CSR contraction kernels: the SDDMM converts
     # one fp32 operand to fp64 per exact product on the XU pipe (16 lanes/clk/SM); the SpMMs read

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace wino {
 namespace tc {
 
@@ -69,6 +71,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+
+// TMA store of a shared-memory box into a 3-D tensor (out-of-range rows/columns are clipped)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     (uint64_t)map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (SM100 UMMA): start>>4 [0,14), LBO>>4 [16,30), SBO>>4
 // [32,46), version=1 [46,48), layout type [61,64): 2 = SWIZZLE_128B (K-major tf32),
@@ -118,6 +131,42 @@ __device__ __forceinline__ void split_tile(uint8_t* hi_buf, uint8_t* lo_buf, int
         asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(h0 + i), "f"(h.x), "f"(h.y), "f"(h.z), "f"(h.w));
         asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(l0 + i), "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w));
     }
+}
+
+// Same split with integer rounding, bitwise equal to split_tile for finite x: cvt.rna.tf32 (round
+// to nearest, ties away from zero) = add half a tf32 ulp to the sign-magnitude bit pattern and
+// clear the 13 low bits; hi = rna(x), lo = rna(x - hi) (x - hi is exact).  Five ALU/FP32
+// instructions per element instead of two emulated cvt.rna (~10).
+__device__ __forceinline__ uint32_t rna_bits(uint32_t x) { return (x + 0x1000u) & 0xffffe000u; }
+
+__device__ __forceinline__ void split_tile_fast(uint8_t* hi_buf, uint8_t* lo_buf, int bytes, int t, int nthreads) {
+    const uint32_t h0 = smem_u32(hi_buf), l0 = smem_u32(lo_buf);
+#pragma unroll 4
+    for (int i = t * 16; i < bytes; i += nthreads * 16) {
+        uint32_t x[4], h[4], l[4];
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(h0 + i));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            h[j] = rna_bits(x[j]);
+            l[j] = rna_bits(__float_as_uint(__fsub_rn(__uint_as_float(x[j]), __uint_as_float(h[j]))));
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(h0 + i), "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(l0 + i), "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3]));
+    }
+}
+
+// Kahan step on two lanes of fp32 pairs at once (FADD2): s += v with compensation c.
+__device__ __forceinline__ void kahan2(float& s0, float& s1, float& c0, float& c1, float v0, float v1) {
+    unsigned long long s, c, v, y, t, d;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(s) : "f"(s0), "f"(s1));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(c) : "f"(c0), "f"(c1));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(v0), "f"(v1));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(v), "l"(c));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(s), "l"(y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(t), "l"(s));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(c) : "l"(d), "l"(y));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(s0), "=f"(s1) : "l"(t));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
@@ -324,6 +373,7 @@ constexpr int A_TILE = BM * BK * 4;   // 16 KB
 constexpr int B_TILE = BK * BN * 4;   // 16 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256;
+constexpr int WS_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 8 * 4096;  // + barriers, 8 staging boxes
 constexpr int TMEM_COLS = 2 * BN;
 
 __host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
@@ -676,6 +726,220 @@ gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, c
                 }
             }
         }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// Warp-specialised form of the persistent accurate kernel.  In the kernels above the same
+// epilogue warps split the operands of stage kb+2 and then drain the accumulator of k-block kb,
+// so the split feeding the MMA waits behind every drain (ncu: tensor pipe ~20% active, warps
+// mostly waiting on mbarriers).  Here the roles are separate warps:
+//   warp 0 TMA · warp 1 TMEM alloc + MMA · SW split warps (hi/lo of the stage, runs up to STAGES
+//   ahead, gated only by TMA) · DW drain warps (fold each k-block's fresh accumulator; warp w
+//   reads TMEM lane quarter w % 4 and column block of COLS = BN/(DW/4) columns).
+// NBUF TMEM accumulators let the MMA run NBUF-1 k-blocks ahead of the drain.  Same arithmetic
+// per tile as gemm_3xtf32_flush_persistent_kernel (bitwise, with KAHAN = false).
+template <bool A_SPLIT, bool B_MN, int SW, int DW, bool KAHAN, int NBUF>
+__global__ void __launch_bounds__(64 + 32 * (SW + DW), 1)
+gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
+                      const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapD,
+                      float* __restrict__ D, int M, int N, int Kd,
+                      int64_t ldd, int slices, int splits, int kb_per, int tiles_n, int tiles_m, int ntiles) {
+    constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
+    constexpr int STAGE_BYTES = flush::STAGE_BYTES;
+    constexpr int TMEM_COLS = NBUF * BN;
+    static_assert(TMEM_COLS <= 512 && (NBUF & (NBUF - 1)) == 0, "TMEM holds 512 columns");
+    static_assert(DW == 8, "drain warps: 4 lane quarters x 2 column blocks, one 4 KB staging box each");
+    constexpr int COLS = BN / (DW / 4);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* split = bars + STAGES;
+    uint64_t* empty = bars + 2 * STAGES;
+    uint64_t* tfull = bars + 3 * STAGES;
+    uint64_t* tempty = bars + 3 * STAGES + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * NBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kb_total = (Kd + BK - 1) / BK;
+    struct Tile { int n0, m0, s, q, kb0, kblocks; };
+    auto decode = [&](int tile) {
+        Tile t;
+        const int nt = tile % tiles_n, rest = tile / tiles_n;
+        const int mt = rest % tiles_m, z = rest / tiles_m;
+        t.n0 = nt * BN;
+        t.m0 = mt * BM;
+        t.s = z / splits;
+        t.q = z - t.s * splits;
+        t.kb0 = t.q * kb_per;
+        t.kblocks = max(0, min(kb_total, t.kb0 + kb_per) - t.kb0);
+        return t;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split[i], 32 * SW);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < NBUF; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 32 * DW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int kbg = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const Tile t = decode(tile);
+                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
+                    const int st = kbg % STAGES;
+                    if (kbg >= STAGES) mbar_wait(&empty[st], ((kbg / STAGES) - 1) & 1);
+                    uint8_t* base = stage_ptr(st);
+                    const int kk = (t.kb0 + kb) * BK;
+                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
+                    tma_load_3d(base, &mapAh, &full[st], kk, t.m0, t.s);
+                    if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, t.m0, t.s);
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 32; ++j)
+                            tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], t.n0 + 32 * j, kk, t.s);
+                    } else {
+                        tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, t.n0, t.s);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id = flush::idesc(B_MN);
+            int kbg = 0, gg = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const Tile t = decode(tile);
+                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg, ++gg) {
+                    const int st = kbg % STAGES, b = gg % NBUF;
+                    if (gg >= NBUF) mbar_wait(&tempty[b], ((gg / NBUF) - 1) & 1);
+                    mbar_wait(&split[st], (kbg / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a_hi = smem_u32(stage_ptr(st));
+                    const uint32_t a_lo = a_hi + A_TILE;
+                    const uint32_t b_hi = a_hi + 2 * A_TILE;
+                    const uint32_t b_lo = b_hi + B_TILE;
+                    const uint32_t acc = tmem + (uint32_t)(b * BN);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+                        const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
+                        const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
+                        uint64_t dbh, dbl;
+                        if (B_MN) {
+                            dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                            dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
+                        } else {
+                            dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
+                            dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
+                        }
+                        mma_tf32(acc, dah, dbh, id, k == 0 ? 0u : 1u);  // fresh accumulator per k-block
+                        mma_tf32(acc, dah, dbl, id, 1u);
+                        mma_tf32(acc, dal, dbh, id, 1u);
+                    }
+                    mma_commit(&empty[st]);
+                    mma_commit(&tfull[b]);
+                }
+            }
+        }
+    } else if (warp < 2 + SW) {
+        const int ts = threadIdx.x - 64;
+        int kbg = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int kbl = decode(tile).kblocks;
+            for (int kb = 0; kb < kbl; ++kb, ++kbg) {
+                const int st = kbg % STAGES;
+                mbar_wait(&full[st], (kbg / STAGES) & 1);
+                uint8_t* base = stage_ptr(st);
+                if (A_SPLIT) split_tile_fast(base, base + A_TILE, A_TILE, ts, 32 * SW);
+                split_tile_fast(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, ts, 32 * SW);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&split[st]);
+            }
+        }
+    } else {
+        const int qd = warp & 3, cb = (warp - 2 - SW) >> 2;
+        float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024) + (warp - 2 - SW) * 1024;
+        int gg = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const Tile t = decode(tile);
+            using Acc = typename std::conditional<KAHAN, float, double>::type;
+            Acc accd[COLS];
+            float comp[KAHAN ? COLS : 1];
+#pragma unroll
+            for (int j = 0; j < COLS; ++j) accd[j] = Acc(0);
+#pragma unroll
+            for (int j = 0; j < (KAHAN ? COLS : 1); ++j) comp[j] = 0.f;
+            for (int kb = 0; kb < t.kblocks; ++kb, ++gg) {
+                const int b = gg % NBUF;
+                mbar_wait(&tfull[b], (gg / NBUF) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + cb * COLS);
+#pragma unroll
+                for (int c = 0; c < COLS; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(ta + c, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c + 16 == COLS) {  // the buffer is free once the last columns are in registers
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mbar_arrive(&tempty[b]);
+                    }
+                    if constexpr (KAHAN) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 2)
+                            kahan2(accd[c + j], accd[c + j + 1], comp[c + j], comp[c + j + 1], __uint_as_float(v[j]),
+                                   __uint_as_float(v[j + 1]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) accd[c + j] += (double)__uint_as_float(v[j]);
+                    }
+                }
+            }
+            if constexpr (KAHAN) {
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) accd[j] = __fsub_rn(accd[j], comp[j]);
+            }
+            // Output through a per-warp 32×32 staging box (128-byte swizzle: conflict-free float4
+            // writes, lane = row) and TMA stores — row-per-lane global stores hit 32 rows per
+            // instruction with half-sector writes (measured: +45% GEMM time at c3).
+#pragma unroll
+            for (int p = 0; p < COLS / 32; ++p) {
+                if (lane == 0) bulk_wait_read();  // the previous box has left shared memory
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                        make_float4((float)accd[p * 32 + 4 * j], (float)accd[p * 32 + 4 * j + 1],
+                                    (float)accd[p * 32 + 4 * j + 2], (float)accd[p * 32 + 4 * j + 3]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&mapD, stg, t.n0 + cb * COLS + p * 32, t.m0 + qd * 32, t.q * slices + t.s);
+                    bulk_commit();
+                }
+            }
+        }
+        if (lane == 0) bulk_wait_all();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
