@@ -793,26 +793,38 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
                                                                     kb_per, (int)grid.x, (int)grid.y, ntiles);
         };
         // Default: the warp-specialised kernel (split warps apart from drain warps, 4 TMEM
-        // accumulators, TMA-stored output) with the compensated fp32 fold; WINO_TC_ACC=fp64 keeps
-        // its fp64 fold, WINO_TC_WS=0 selects the round-1 persistent kernel (A/B builds).
+        // accumulators, TMA-stored output) with the compensated fp32 fold (fp64 for the dW GEMM);
+        // WINO_TC_ACC=fp64 selects the fp64 fold everywhere, WINO_TC_WS=0 the round-1 persistent
+        // kernel (A/B builds).
         static const bool ws = !(std::getenv("WINO_TC_WS") && std::atoi(std::getenv("WINO_TC_WS")) == 0);
-        static const bool fp64_fold = std::getenv("WINO_TC_ACC") && std::string(std::getenv("WINO_TC_ACC")) == "fp64";
+        // the dW GEMM (A split in shared memory too) measured faster with the fp64 fold (551 vs 584
+        // µs at c3): its two split warps, not the drain, bound it, and the fp64 fold does not spill
+        static const bool fp64_env = std::getenv("WINO_TC_ACC") && std::string(std::getenv("WINO_TC_ACC")) == "fp64";
+        const bool fp64_fold = fp64_env || A_SPLIT;
+        // drain warps: 8 (64 columns each, 4 KB SW128 output boxes; measured 4% faster at c3 than
+        // WINO_TC_DW=16 with 32 columns and 2 KB SW64 boxes)
+        static const int dw = std::getenv("WINO_TC_DW") ? std::atoi(std::getenv("WINO_TC_DW")) : 8;
         CUtensorMap md;
         const bool ws_ok = ws && persistent && fold == 1 && (ldd & 3) == 0 &&
-                           wino::make_map_3d(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2 * splits,
-                                             (uint64_t)ldd * 4, (uint64_t)M * ldd * 4, 32, 32);
+                           wino::make_map_3d_sw(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2 * splits,
+                                                (uint64_t)ldd * 4, (uint64_t)M * ldd * 4, dw == 8 ? 32 : 16, 32,
+                                                dw == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
         // 2 split warps: 4 would cap registers at 128/thread and spill the drain's 64 Kahan pairs
         constexpr int SW = 2;
-        auto go_ws = [&](auto kern) {
+        auto go_ws = [&](auto kern, int drain_warps) {
             set_smem_attr(kern, wino::tc::flush::WS_SMEM_BYTES);
             const int ctas = std::min(ntiles, p->sm_count);
-            kern<<<ctas, 64 + 32 * (SW + 8), wino::tc::flush::WS_SMEM_BYTES, st>>>(
+            kern<<<ctas, 64 + 32 * (SW + drain_warps), wino::tc::flush::WS_SMEM_BYTES, st>>>(
                 ah, al, b, md, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y, ntiles);
         };
-        if (ws_ok && !fp64_fold)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4>);
+        if (ws_ok && dw == 8 && !fp64_fold)
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4>, 8);
+        else if (ws_ok && dw == 8)
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, false, 4>, 8);
+        else if (ws_ok && !fp64_fold)
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, true, 4>, 16);
         else if (ws_ok)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, false, 4>);
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, false, 4>, 16);
         else if (persistent && fold == 1 && epi == 8)
             go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 8>, 64 + 32 * 8);
         else if (persistent && fold == 1)

@@ -752,8 +752,11 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
     constexpr int STAGE_BYTES = flush::STAGE_BYTES;
     constexpr int TMEM_COLS = NBUF * BN;
     static_assert(TMEM_COLS <= 512 && (NBUF & (NBUF - 1)) == 0, "TMEM holds 512 columns");
-    static_assert(DW == 8, "drain warps: 4 lane quarters x 2 column blocks, one 4 KB staging box each");
+    static_assert(DW == 8 || DW == 16, "drain warps: 4 lane quarters x 2 or 4 column blocks");
     constexpr int COLS = BN / (DW / 4);
+    // output staging box per drain warp: 32 rows x BOXC columns (4 KB with a 128-byte swizzle for
+    // DW = 8, 2 KB with a 64-byte swizzle for DW = 16) — 32 KB of shared memory either way
+    constexpr int BOXC = DW == 8 ? 32 : 16;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* full = bars;
@@ -879,7 +882,7 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
         }
     } else {
         const int qd = warp & 3, cb = (warp - 2 - SW) >> 2;
-        float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024) + (warp - 2 - SW) * 1024;
+        float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024) + (warp - 2 - SW) * 32 * BOXC;
         int gg = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const Tile t = decode(tile);
@@ -919,22 +922,26 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
 #pragma unroll
                 for (int j = 0; j < COLS; ++j) accd[j] = __fsub_rn(accd[j], comp[j]);
             }
-            // Output through a per-warp 32×32 staging box (128-byte swizzle: conflict-free float4
-            // writes, lane = row) and TMA stores — row-per-lane global stores hit 32 rows per
-            // instruction with half-sector writes (measured: +45% GEMM time at c3).
+            // Output through a per-warp 32-row staging box (swizzled: conflict-free float4 writes,
+            // lane = row) and TMA stores — row-per-lane global stores hit 32 rows per instruction
+            // with half-sector writes (measured: +45% GEMM time at c3).
 #pragma unroll
-            for (int p = 0; p < COLS / 32; ++p) {
+            for (int p = 0; p < COLS / BOXC; ++p) {
                 if (lane == 0) bulk_wait_read();  // the previous box has left shared memory
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) << 2)) =
-                        make_float4((float)accd[p * 32 + 4 * j], (float)accd[p * 32 + 4 * j + 1],
-                                    (float)accd[p * 32 + 4 * j + 2], (float)accd[p * 32 + 4 * j + 3]);
+                for (int j = 0; j < BOXC / 4; ++j) {
+                    // 16-byte chunk j of row `lane`: XOR with address bits 7.. (SW128: lane & 7,
+                    // SW64: (lane >> 1) & 3)
+                    const int pj = BOXC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
+                    *reinterpret_cast<float4*>(stg + lane * BOXC + (pj << 2)) =
+                        make_float4((float)accd[p * BOXC + 4 * j], (float)accd[p * BOXC + 4 * j + 1],
+                                    (float)accd[p * BOXC + 4 * j + 2], (float)accd[p * BOXC + 4 * j + 3]);
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_3d(&mapD, stg, t.n0 + cb * COLS + p * 32, t.m0 + qd * 32, t.q * slices + t.s);
+                    tma_store_3d(&mapD, stg, t.n0 + cb * COLS + p * BOXC, t.m0 + qd * 32, t.q * slices + t.s);
                     bulk_commit();
                 }
             }
