@@ -38,10 +38,12 @@ def timeit(fn, k=20):
         fn()
         b.record()
     torch.cuda.synchronize()
-    return sorted(a.elapsed_time(b) for a, b in ev)[k // 2] * 1e3
+    ts = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+    print(f"    [min {ts[0]:.0f} median {ts[k // 2]:.0f} mean {sum(ts) / k:.0f} max {ts[-1]:.0f} us]")
+    return ts[k // 2]
 
 
-for chunks in (1, 2, 4):
+for chunks in (1, 2, 4, 8):
     ps = PipelinedHostStep(layer, cache, x, g, o, dw, di, chunks=chunks)
     full = GraphedStep(lambda: ps(h[0], h[1], *outs)).replay
     print(f"chunks {chunks}: full {timeit(full):.0f} us")
