@@ -551,10 +551,13 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
         dist.barrier()
     clocks = sampler.stop()
     launches = per_step_launches * args.steps
+    # per-kernel times: one step with dW_F and dI serialised (concurrent kernels would share the
+    # GPU and inflate each other's event times)
     for lay in st.layers:
         lay.profile(True)
     flush.zero_()
-    step()
+    st.forward(x)
+    st.backward(g_o, serial=True)
     torch.cuda.synchronize()
     prof = {}
     for lay in st.layers:
@@ -608,7 +611,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     if rank != 0:
         return
     tot = sum(v[0] for v in prof.values())
-    kernels = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1], "share": v[0] / tot}
+    kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / tot}
                for k, v in prof.items()}
     line = {
         "metric": METRIC.replace("layer", "4-layer training step"), "value": value, "unit": "GFLOP/s",

@@ -55,16 +55,21 @@ class WinogradStack:
             cur = lay.forward(cur, cache, relu=True, out=self.outs[i])
         return cur
 
-    def backward(self, grad_out):
+    def backward(self, grad_out, serial: bool = False):
         """The backward chain of minibatch_grad (train.cpp:189-211) for the whole minibatch:
-        fills the gradient bucket with Σ_n dW_F per layer; no dI for layer 0 (train.cpp:201)."""
+        fills the gradient bucket with Σ_n dW_F per layer; no dI for layer 0 (train.cpp:201).
+        serial=True runs dW_F and dI one after the other (same results; per-kernel timing)."""
         g = grad_out
         for i in range(len(self.layers) - 1, -1, -1):
             lay, cache = self.layers[i], self.caches[i]
             if i > 0:  # dW_F concurrently with dI (wino_backward)
                 if self.dis[i] is None or self.dis[i].shape[0] != g.shape[0]:
                     self.dis[i] = self._torch.empty((g.shape[0], lay.c, lay.h, lay.w), device=g.device)
-                _, g = lay.backward(g, cache, relu_out=self.outs[i], out_w=self.grads[i], out_i=self.dis[i])
+                if serial:
+                    lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.grads[i])
+                    g = lay.backward_input(cache, out=self.dis[i])
+                else:
+                    _, g = lay.backward(g, cache, relu_out=self.outs[i], out_w=self.grads[i], out_i=self.dis[i])
             else:
                 lay.backward_weights(g, cache, relu_out=self.outs[i], out=self.grads[i])
         return self.bucket
