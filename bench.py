@@ -232,6 +232,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         layer.set_dw_mode("tc")
     elif args.dw == "precise":
         layer.set_dw_mode("precise")
+    elif args.dw == "int8" and not dense:
+        layer.set_dw_mode("int8")
     if args.contraction != "csr" and not dense:
         layer.set_contraction(args.contraction)
     cache = layer.new_cache(n)
@@ -455,7 +457,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                            {"csr": "csr", "tc": "tcgen05-3xtf32-fp64fold on zero-filled W_F",
                             "auto": "auto (tensor cores at density >= 15%, else csr)"}[args.contraction],
                    "dw": {"sddmm": "masked-sddmm-exact", "tc": "tcgen05-3xtf32-fp64fold+mask-gather",
-                          "precise": "masked-sddmm-exact on fp32 hi+lo operands"}[args.dw],
+                          "precise": "masked-sddmm-exact on fp32 hi+lo operands",
+                          "int8": "int8-tcgen05-exact-digit-products+mask-gather"}[args.dw],
                    "l2_flush": "256 MB write between timed steps",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
@@ -648,7 +651,7 @@ def main():
                     help="backward_weights then backward_input instead of the concurrent wino_backward")
     ap.add_argument("--contraction", default="csr", choices=["csr", "tc", "auto"],
                     help="sparse plan: CSR kernels (bitwise reference order) or tcgen05 on zero-filled W_F")
-    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise"],
+    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise", "int8"],
                     help="sparse dW_F: exact masked SDDMM (default) or tensor-core GEMM + mask gather")
     ap.add_argument("--dense", default=None, choices=["tc", "tc-fast", "exact"],
                     help="dense path at 0%% sparsity: 'tc' (default: 3xTF32 tcgen05, per-k-block fp64 "

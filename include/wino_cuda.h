@@ -204,7 +204,13 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *       dZ), each recomputed in fp64 with the reference's coefficients; the SDDMM forms
  *       zh·xh + zh·xl + zl·xh exactly in fp64, so dW_F matches the reference's f64 layer on
  *       every element (no fp32-storage floor).  ~2× the SDDMM time and 2× the cache memory;
- *       caches created before the switch allocate their residual buffers on first use. */
+ *       caches created before the switch allocate their residual buffers on first use.
+ *     3 int8 tensor cores — dZ and Ĩ_F split into 5 signed base-2^7 digits per value with one
+ *       exponent per 128-long block, the 15 digit pairs of weight < 5 multiplied exactly on
+ *       tcgen05 kind::i8 into int32 TMEM, blocks summed in fp64: the exact dot products of the
+ *       stored fp32 operands like mode 0 (within one fp32 rounding of it), then the surviving
+ *       entries gathered in CSR order.  Requires C, K multiples of 4; measured slower than
+ *       mode 0 on the BASELINE shapes. */
 #define WINO_OPT_DW_MODE 1
 /*   WINO_OPT_CONTRACTION: how a sparse plan runs Z = W_F·Ĩ_F and dĨ_F = W_Fᵀ·dZ:
  *     0 (default) the CSR kernels — the reference's association order, forward bitwise equal

@@ -16,6 +16,7 @@
 #include "wino_compress.cuh"
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
+#include "wino_ozaki.cuh"
 #include "wino_precise.cuh"
 #include "wino_tmap.h"
 #include "wino_update.cuh"
@@ -200,13 +201,16 @@ struct wino_plan {
     CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
     bool tc_ready = false;
     bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
-    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather, 2 = precise
+    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather, 2 = precise,
+                           // 3 = int8 tensor cores, exact products (wino_ozaki.cuh)
     int contraction = 0;   // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
     int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc + tc dW when dense enough)
     int auto_permille = 150;   // auto: tensor cores at density >= this / 1000
     int64_t* d_slice_off = nullptr;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;
+    uint8_t* d_oz = nullptr;  // int8 dW: digit tensors, block exponents, the dense K×C product
+    size_t oz_cap = 0;
     // scratch
     float* d_z = nullptr;
     size_t z_cap = 0;
@@ -879,6 +883,55 @@ int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
     return L.done();
 }
 
+// dW_F on the int8 tensor cores (wino_ozaki.cuh): digit split of dZ and Ĩ_F, the exact-product
+// GEMM per Winograd coordinate into a dense [P2][K][C] buffer, then the surviving entries
+// gathered in CSR order.
+int launch_ozaki_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
+                    int64_t NTs) {
+    namespace oz = wino::oz;
+    const int64_t NTp = (NT + oz::KB - 1) / oz::KB * oz::KB, nkb = NTp / oz::KB;
+    const int64_t P2 = p->P2, K = p->K, C = p->C;
+    const size_t dig_a = (size_t)oz::DIG * P2 * K * NTp, dig_b = (size_t)oz::DIG * P2 * C * NTp;
+    const size_t ex_a = (size_t)P2 * K * nkb * 4, ex_b = (size_t)P2 * C * nkb * 4;
+    const size_t dense = (size_t)P2 * K * C * 4;
+    auto up = [](size_t x) { return (x + 1023) / 1024 * 1024; };
+    const size_t need = up(dig_a) + up(dig_b) + up(ex_a) + up(ex_b) + up(dense);
+    if (p->oz_cap < need) {
+        if (p->d_oz) cudaFree(p->d_oz);
+        p->d_oz = nullptr;
+        p->oz_cap = 0;
+        CUDA_TRY(cudaMalloc(&p->d_oz, need));
+        p->oz_cap = need;
+    }
+    int8_t* da = reinterpret_cast<int8_t*>(p->d_oz);
+    int8_t* db = da + up(dig_a);
+    int* ea = reinterpret_cast<int*>(db + up(dig_b));
+    int* eb = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ea) + up(ex_a));
+    float* dd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(eb) + up(ex_b));
+    CUtensorMap ma, mb;
+    if (!wino::make_map_3d_sw(&ma, da, NTp, K, oz::DIG * P2, NTp, K * NTp, oz::KB, oz::BM,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT8) ||
+        !wino::make_map_3d_sw(&mb, db, NTp, C, oz::DIG * P2, NTp, C * NTp, oz::KB, oz::BN,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT8))
+        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the int8 digit tensors (CUresult " +
+                                            std::to_string(wino::last_tmap_error()) + ")");
+    Launch L(p, st, K_SDDMM);
+    oz::slice_kernel<<<grid_for(P2 * K * nkb * 32, 256, p->sm_count), 256, 0, st>>>(DZ, da, ea, (int)P2, (int)K,
+                                                                                   (int)NT, (int)NTs, (int)NTp);
+    oz::slice_kernel<<<grid_for(P2 * C * nkb * 32, 256, p->sm_count), 256, 0, st>>>(V, db, eb, (int)P2, (int)C,
+                                                                                   (int)NT, (int)NTs, (int)NTp);
+    const int tiles_n = (int)((C + oz::BN - 1) / oz::BN), tiles_m = (int)((K + oz::BM - 1) / oz::BM);
+    const int ntiles = tiles_n * tiles_m * (int)P2;
+    set_smem_attr(oz::gemm_kernel, oz::SMEM_BYTES);
+    oz::gemm_kernel<<<std::min(ntiles, p->sm_count), oz::THREADS, oz::SMEM_BYTES, st>>>(
+        ma, mb, ea, eb, dd, (int)P2, (int)K, (int)C, (int)nkb, tiles_n, tiles_m, ntiles);
+    const int per_slice = (int)std::max<int64_t>(1, std::min<int64_t>(64, p->nnz / P2 / 1024 + 1));
+    oz::gather_kernel<<<dim3(per_slice, (unsigned)P2), 256, 0, st>>>(dd, dW, p->d_rowof, p->d_colidx,
+                                                                    p->d_slice_off, p->K, p->C, p->P2, p->nnz);
+    p->launches += 3;  // Launch L counts one
+    return L.done();
+}
+
 int check_plan(const wino_plan* p) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
     if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan has no weights (call wino_set_weights*)");
@@ -1179,6 +1232,7 @@ int wino_plan_destroy(wino_plan* p) {
     free_compress_scratch(p);
     chk(cudaGetLastError(), "free_weights");
     if (p->d_dwc) chk(cudaFree(p->d_dwc), "d_dwc");
+    if (p->d_oz) chk(cudaFree(p->d_oz), "d_oz");
     if (p->d_z) chk(cudaFree(p->d_z), "d_z");
     if (p->d_dv) chk(cudaFree(p->d_dv), "d_dv");
     if (p->d_scalar) chk(cudaFree(p->d_scalar), "d_scalar");
@@ -1430,6 +1484,8 @@ static int bwd_dw(wino_plan* p, const wino_cache* c, float* grad_w, cudaStream_t
     const bool tc_dw = p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
     if (!p->dense && tc_dw && p->nnz > 0)
         rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
+    else if (!p->dense && p->dw_mode == 3 && p->nnz > 0)
+        rc = launch_ozaki_dw(p, st, c->DZ, c->V, dwc, NT, NTs);
     else if (precise)
         rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
     else
@@ -1729,9 +1785,9 @@ int wino_set_option(wino_plan* p, int option, int value) {
         p->auto_permille = value;
         return p->contraction_mode == 2 ? apply_contraction(p) : WINO_OK;
     }
-    if (option != WINO_OPT_DW_MODE || value < 0 || value > 2)
+    if (option != WINO_OPT_DW_MODE || value < 0 || value > 3)
         return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
-    if (value == 1) {
+    if (value == 1 || value == 3) {
         if (p->C % 4 || p->K % 4)
             return set_err(WINO_CAPABILITY_ERROR, "tensor-core dW needs C and K multiples of 4 (TMA strides)");
         if (!p->d_slice_off && p->has_weights) {

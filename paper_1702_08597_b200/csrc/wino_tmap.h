@@ -32,17 +32,21 @@ inline int& last_tmap_error() {
 }
 
 inline bool make_map_3d_sw(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                           uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw);
+                           uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
+                           CUtensorMapDataType dt);
 
 inline bool make_map_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
                         uint64_t s2, uint32_t b0, uint32_t b1, bool atom32 = false) {
     return make_map_3d_sw(map, base, d0, d1, d2, s1, s2, b0, b1,
-                          atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+                          atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-// same with an explicit swizzle mode (output staging boxes use 64- or 128-byte swizzles)
+// same with an explicit swizzle mode (output staging boxes use 64- or 128-byte swizzles) and
+// element type (uint8 for the int8 digit tensors of wino_ozaki.cuh)
 inline bool make_map_3d_sw(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                           uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw) {
+                           uint64_t s2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
+                           CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     EncodeTiledFn fn = encode_tiled_fn();
     if (!fn) {
         last_tmap_error() = -1;
@@ -52,7 +56,7 @@ inline bool make_map_3d_sw(CUtensorMap* map, const void* base, uint64_t d0, uint
     cuuint64_t strides[2] = {s1, s2};
     cuuint32_t box[3] = {b0, b1, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+    const CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     last_tmap_error() = (int)r;

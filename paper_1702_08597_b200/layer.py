@@ -202,9 +202,10 @@ class WinogradLayer:
 
     def set_dw_mode(self, mode: str):
         """'sddmm' (default: exact products of the fp32 operands), 'tc' (tensor-core GEMM + mask
-        gather) or 'precise' (operands carried as fp32 hi+lo pairs: the reference's f64 dW_F)."""
+        gather), 'precise' (operands carried as fp32 hi+lo pairs: the reference's f64 dW_F) or
+        'int8' (exact products on the int8 tensor cores from base-2^7 digit splits + mask gather)."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE,
-                                    {"sddmm": 0, "tc": 1, "precise": 2}[mode]))
+                                    {"sddmm": 0, "tc": 1, "precise": 2, "int8": 3}[mode]))
 
     def set_contraction(self, mode: str):
         """Sparse plan contractions: 'csr' (default; the reference's order, forward bitwise equal
