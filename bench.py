@@ -246,7 +246,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     fwd_only = not cfg.backward  # c2: the reference's sparse inference pass
 
-    def step():
+    def compute():
         layer.forward(x, cache, out=out)
         if fwd_only:
             return
@@ -255,7 +255,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             layer.backward_input(cache, out=di)
         else:  # dW_F concurrently with dI (wino_backward)
             layer.backward(g_o, cache, out_w=dw, out_i=di)
-        if world > 1:
+
+    def step():
+        compute()
+        if world > 1 and not fwd_only:
             dist.all_reduce(dw)
 
     for _ in range(args.warmup):
@@ -265,7 +268,16 @@ def run_gpu(args, cfg, rank, world, local_rank):
     step()
     torch.cuda.synchronize()
     per_step_launches = layer.launch_count()
-    run, graph_note = capture(step, args)
+    # the layer's kernels as one CUDA graph; the step's one collective (N > 1) is issued eagerly
+    # after the replay, on the same stream, so no NCCL call is ever graph-captured
+    run_c, graph_note = capture(compute, args)
+    if world > 1 and not fwd_only:
+        def run():
+            run_c()
+            dist.all_reduce(dw)
+        graph_note += " + eager NCCL all-reduce of dW_F"
+    else:
+        run = run_c
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -530,6 +542,17 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     def step():
         st.step(x, g_o, lr=1e-4, n_global=n_global)
 
+    # the same step in three parts (WinogradStack.step with mode=None): forward + backward and the
+    # masked SGD update each as a CUDA graph, the bucket's one all-reduce issued eagerly between
+    # them (no NCCL call is graph-captured)
+    def fwd_bwd():
+        st.forward(x)
+        st.backward(g_o)
+
+    def update():
+        for lay, gr in zip(st.layers, st.grads):
+            lay.sgd_step(gr, lr=1e-4, scale=1.0 / float(n_global), l2=0.0)
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -538,7 +561,15 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     step()
     torch.cuda.synchronize()
     per_step_launches = st.launch_count()
-    run, graph_note = capture(step, args)
+    run_fb, graph_note = capture(fwd_bwd, args)
+    run_up, _ = capture(update, args)
+
+    def run():
+        run_fb()
+        st.bucket.allreduce()
+        run_up()
+    if world > 1:
+        graph_note += " (forward+backward and update graphs, eager NCCL all-reduce between)"
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local_rank)
