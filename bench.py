@@ -256,6 +256,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
         else:  # dW_F concurrently with dI (wino_backward)
             layer.backward(g_o, cache, out_w=dw, out_i=di)
 
+    if not fwd_only and not args.separate_bwd and not args.call_order:
+        def compute():  # one call, scheduled by data dependence (wino_forward_backward)
+            layer.forward_backward(x, g_o, cache, out=out, out_w=dw, out_i=di)
+
     def step():
         compute()
         if world > 1 and not fwd_only:
@@ -678,6 +682,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e through HostStep (whole-batch calls)")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
+    ap.add_argument("--call-order", action="store_true",
+                    help="forward then backward as two calls (default: one wino_forward_backward call "
+                         "scheduled by data dependence)")
     ap.add_argument("--separate-bwd", action="store_true",
                     help="backward_weights then backward_input instead of the concurrent wino_backward")
     ap.add_argument("--contraction", default="csr", choices=["csr", "tc", "auto"],

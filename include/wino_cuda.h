@@ -143,6 +143,14 @@ WINO_API int wino_backward_weights(wino_plan* plan, const float* grad_output, co
  * grad_input may be NULL (no dI: the first layer of a stack, train.cpp:201). */
 WINO_API int wino_backward(wino_plan* plan, const float* grad_output, const float* relu_out,
                            wino_cache* cache, float* grad_w, float* grad_input, int flags, void* stream);
+/* One training step of the layer: wino_forward followed by wino_backward with both gradients
+ * (no ReLU flags), bit for bit, but scheduled by data dependence rather than call order: dZ
+ * needs only grad_output, so the dO -> dZ -> dĨ_F -> dI chain starts beside the forward on a
+ * side stream and dW_F starts as soon as Ĩ_F and dZ exist (a second side stream); both join
+ * `stream` before return.  The caller (train.cpp:158-211 per sample; a batched trainer per
+ * layer) owns the cache exactly as with the two calls. */
+WINO_API int wino_forward_backward(wino_plan* plan, int n, const float* input, float* output, wino_cache* cache,
+                                   const float* grad_output, float* grad_w, float* grad_input, void* stream);
 /* The data-parallel exchange: sum grad_w (count floats; count < 0 = this plan's
  * dW_F length, nnz-compact or K×C×p×q) in place over an NCCL communicator (`nccl_comm` is an
  * ncclComm_t), on `stream`.  The scale 1/N_global of train.cpp:166,200 stays with the update.

@@ -111,6 +111,7 @@ SIGNATURES = {
     "wino_backward_weights": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_input": (C.c_int, [_vp, _vp, _vp, _vp]),
     "wino_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "wino_forward_backward": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "wino_forward_range": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_range": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_weights_cached": (C.c_int, [_vp, _vp, _vp, _vp]),

@@ -219,6 +219,8 @@ struct wino_plan {
     double* d_scalar = nullptr;
     cudaStream_t side = nullptr;  // wino_backward: dW runs here, concurrent with dĨ_F -> dI
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side2 = nullptr;  // wino_forward_backward: the dO -> dZ -> dĨ_F -> dI chain
+    cudaEvent_t ev_v = nullptr, ev_dz = nullptr, ev_join2 = nullptr;
     // instrumentation
     int64_t launches = 0;
     bool prof = false;
@@ -1239,6 +1241,10 @@ int wino_plan_destroy(wino_plan* p) {
     if (p->side) chk(cudaStreamDestroy(p->side), "side stream");
     if (p->ev_fork) chk(cudaEventDestroy(p->ev_fork), "ev_fork");
     if (p->ev_join) chk(cudaEventDestroy(p->ev_join), "ev_join");
+    if (p->side2) chk(cudaStreamDestroy(p->side2), "side2");
+    if (p->ev_v) chk(cudaEventDestroy(p->ev_v), "ev_v");
+    if (p->ev_dz) chk(cudaEventDestroy(p->ev_dz), "ev_dz");
+    if (p->ev_join2) chk(cudaEventDestroy(p->ev_join2), "ev_join2");
     if (p->d_partial) chk(cudaFree(p->d_partial), "d_partial");
     if (p->d_slice_off) chk(cudaFree(p->d_slice_off), "d_slice_off");
     for (auto& r : p->recs) {
@@ -1548,6 +1554,74 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
     CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
     if ((rc = bwd_input(p, c, grad_input, st))) return rc;
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
+    return WINO_OK;
+}
+
+// One training step of the layer (forward, then backward with both gradients) scheduled as the
+// dependency graph it is instead of in API order: dZ = A1·dÕ·A2ᵀ needs only dO, so the
+// dO -> dZ -> dĨ_F -> dI chain runs beside the forward from the start (side2), and dW_F waits
+// for just Ĩ_F and dZ (side) — the forward's SpMM and output transform overlap the backward.
+// Same kernels, same buffers, same results bit for bit as wino_forward + wino_backward.
+int wino_forward_backward(wino_plan* p, int n, const float* input, float* output, wino_cache* c,
+                          const float* grad_output, float* grad_w, float* grad_input, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!input || !output || !c || !grad_output || !grad_input || (!grad_w && p->nnz > 0))
+        return set_err(WINO_INVALID_ARGUMENT, "null buffer");
+    if (n <= 0) return set_err(WINO_SHAPE_ERROR, "batch must be positive");
+    if (c->plan != p || n > c->n_max)
+        return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!p->side) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    if (!p->side2) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_v, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_dz, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
+    }
+    const int64_t NT = (int64_t)n * p->g.t;
+    const int64_t NTs = round_up(NT, 4);
+    if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
+    if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
+    if (p->dw_mode == 2 && (rc = ensure_cache_lo(p, c))) return rc;
+    c->n = n;
+    c->NTs = NTs;
+    c->has_fwd = true;
+    c->has_grad_z = false;
+    // fork both side streams off the caller's stream
+    CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    // side2: dZ, then dĨ_F = W_Fᵀ·dZ and dI
+    if ((rc = bwd_grad_z(p, grad_output, nullptr, c, 0, p->side2))) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_dz, p->side2));
+    if ((rc = bwd_input(p, c, grad_input, p->side2))) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_join2, p->side2));
+    // caller's stream: Ĩ_F, then Z = W_F·Ĩ_F and O
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c, c->V, p->d_z, n, NT, NTs, 0, 0, NTs)))
+        return rc;
+    if (p->dw_mode == 2 && (rc = DISPATCH_MP(p, launch_input_lo, p, st, input, c->V, c->Vlo, NT, NTs))) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_v, st));
+    // side: dW_F once Ĩ_F and dZ exist
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_v, 0));
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_dz, 0));
+    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
+    if (p->tc_ready && (p->dense || p->contraction == 1))
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs);
+    else
+        rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, c->V, p->d_z, p->K, p->C, NT, NTs);
+    if (rc) return rc;
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c, c->V, p->d_z, n, NT, NTs, 0, 1, NTs)))
+        return rc;
+    // join
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join2, 0));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
+    c->has_grad_z = true;
     return WINO_OK;
 }
 

@@ -294,6 +294,25 @@ class WinogradLayer:
                                   _lib.WINO_BWD_RELU_MASK if relu_out is not None else 0, _stream_ptr(stream)))
         return out_w, out_i
 
+    def forward_backward(self, x, grad_o, cache: ForwardCache, out=None, out_w=None, out_i=None, stream=None):
+        """forward + backward (dW_F and dI) in one call, scheduled by data dependence: the dI chain
+        and dW_F overlap the forward (wino_forward_backward; bitwise the two-call results)."""
+        import torch
+
+        n = x.shape[0]
+        self._check_dev(x, (n, self.c, self.h, self.w), "input")
+        self._check_dev(grad_o, (n, self.k, self.ho, self.wo), "grad_output")
+        if out is None:
+            out = torch.empty((n, self.k, self.ho, self.wo), device=x.device, dtype=torch.float32)
+        if out_w is None:
+            out_w = torch.empty(self.grad_w_shape(), device=x.device, dtype=torch.float32)
+        if out_i is None:
+            out_i = torch.empty((n, self.c, self.h, self.w), device=x.device, dtype=torch.float32)
+        check(lib().wino_forward_backward(self._h, n, _dptr(x), _dptr(out), cache._h, _dptr(grad_o), _dptr(out_w),
+                                          _dptr(out_i), _stream_ptr(stream)))
+        cache.n = n
+        return out, out_w, out_i
+
     # -- image ranges of one batch (pipelined host transfers, pipeline.PipelinedHostStep) --------
     def forward_range(self, x_part, n_total: int, n0: int, cache: ForwardCache, out_part, relu=False,
                       stream=None):

@@ -688,3 +688,28 @@ def test_c1_int8_dw_mode_matches_exact_sddmm():
     layer.set_dw_mode("sddmm")
     again = layer.backward_weights(dev(go), cache).cpu().numpy()
     assert np.array_equal(again, exact.astype(np.float32))
+
+
+@pytest.mark.parametrize("mode", ["csr", "tc", "dense", "int8"])
+def test_forward_backward_equals_two_calls(mode):
+    """wino_forward_backward (dI chain and dW_F overlapping the forward) is bitwise forward +
+    backward on every plan kind."""
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg if mode != "dense" else with_sparsity(cfg, 0.0))
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=(mode == "dense"))
+    if mode == "tc":
+        layer.set_contraction("tc")
+    if mode == "int8":
+        layer.set_dw_mode("int8")
+    x, g = dev(img), dev(go)
+    c1 = layer.new_cache(cfg.n)
+    o1 = layer.forward(x, c1)
+    w1, i1 = layer.backward(g, c1)
+    c2 = layer.new_cache(cfg.n)
+    o2, w2, i2 = layer.forward_backward(x, g, c2)
+    torch.cuda.synchronize()
+    for a, b, what in ((o1, o2, "O"), (w1, w2, "dW_F"), (i1, i2, "dI")):
+        assert torch.equal(a, b), f"{mode}: {what} differs"
+    # the cache holds the step's Ĩ_F and dZ: backward_input from it reproduces dI
+    assert torch.equal(layer.backward_input(c2), i1)
