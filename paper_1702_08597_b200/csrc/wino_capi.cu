@@ -1541,7 +1541,11 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
         return bwd_dw(p, c, grad_w, st);
     }
     if (!p->side) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        // dW_F is the longest chain of the step: its stream gets the greatest priority, so its
+        // blocks are scheduled first whenever SMs free up (c1 step 172 -> 169 µs measured)
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
         CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     }
@@ -1573,7 +1577,11 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
         return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
     cudaStream_t st = (cudaStream_t)stream;
     if (!p->side) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        // dW_F is the longest chain of the step: its stream gets the greatest priority, so its
+        // blocks are scheduled first whenever SMs free up (c1 step 172 -> 169 µs measured)
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
         CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     }
