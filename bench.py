@@ -471,7 +471,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
                              "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else
                            {"csr": "csr", "tc": "tcgen05-3xtf32-fp64fold on zero-filled W_F",
-                            "auto": "auto (tensor cores at density >= 15%, else csr)"}[args.contraction],
+                            "auto": "auto (tensor cores at density >= 8%, else csr)"}[args.contraction],
                    "dw": {"sddmm": "masked-sddmm-exact", "tc": "tcgen05-3xtf32-fp64fold+mask-gather",
                           "precise": "masked-sddmm-exact on fp32 hi+lo operands",
                           "int8": "int8-tcgen05-exact-digit-products+mask-gather"}[args.dw],

@@ -229,7 +229,7 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *       (the operands are re-scattered from the CSR values on every update).
  *       Requires C, K multiples of 4.  dW_F still follows WINO_OPT_DW_MODE. */
 /*     2 auto — tensor cores (for Z, dĨ_F and, in dW mode 0, a tensor-core dW + mask gather) when
- *       the plan's density reaches WINO_OPT_AUTO_DENSITY per mille (default 150), else the CSR
+ *       the plan's density reaches WINO_OPT_AUTO_DENSITY per mille (default 80), else the CSR
  *       kernels; re-decided whenever the weights change.  Fastest across the density sweep, with
  *       fp32-level (not bitwise / floor-exact) results on the tensor-core side. */
 #define WINO_OPT_CONTRACTION 2

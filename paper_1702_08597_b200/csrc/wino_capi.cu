@@ -205,7 +205,7 @@ struct wino_plan {
                            // 3 = int8 tensor cores, exact products (wino_ozaki.cuh)
     int contraction = 0;   // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
     int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc + tc dW when dense enough)
-    int auto_permille = 150;   // auto: tensor cores at density >= this / 1000
+    int auto_permille = 80;    // auto: tensor cores at density >= this / 1000 (measured crossover 5-10%)
     int64_t* d_slice_off = nullptr;
     float* d_dwc = nullptr;
     size_t dwc_cap = 0;

@@ -214,7 +214,7 @@ class WinogradLayer:
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1, "auto": 2}[mode]))
 
     def set_auto_density(self, density: float):
-        """Density from which contraction 'auto' uses the tensor cores (default 0.15)."""
+        """Density from which contraction 'auto' uses the tensor cores (default 0.08)."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_AUTO_DENSITY, int(round(density * 1000))))
 
     def weight_values(self):
