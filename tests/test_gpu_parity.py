@@ -713,3 +713,39 @@ def test_forward_backward_equals_two_calls(mode):
         assert torch.equal(a, b), f"{mode}: {what} differs"
     # the cache holds the step's Ĩ_F and dZ: backward_input from it reproduces dI
     assert torch.equal(layer.backward_input(c2), i1)
+
+
+@pytest.mark.parametrize("mode", ["dense", "tc", "int8", "fb"])
+def test_ragged_tile_shapes(mode):
+    """C, K and N·T that fill no tcgen05 tile evenly (C = 136, K = 200, 3 images of 9×9 → N·T = 27):
+    partial M, N and reduction blocks in the warp-specialised GEMM (TMA zero-fill, clipped TMA
+    stores), partial int8 digit blocks and a partial 48-column tile, against the f64 reference."""
+    from paper_1702_08597_b200.synth import LayerConfig
+
+    cfg = LayerConfig("ragged", 3, 136, 200, 9, 0.0 if mode == "dense" else 0.7)
+    img, w_f, go = make_inputs(cfg)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.h, pad=1, m=4)
+    layer.set_weights(w_f, dense=(mode == "dense"))
+    if mode == "tc":
+        layer.set_contraction("tc")
+        layer.set_dw_mode("tc")
+    if mode == "int8":
+        layer.set_dw_mode("int8")
+    cache = layer.new_cache(cfg.n)
+    x, g = dev(img), dev(go)
+    if mode == "fb":
+        o, dw, di = layer.forward_backward(x, g, cache)
+    else:
+        o = layer.forward(x, cache)
+        dw, di = layer.backward(g, cache)
+    o, dw, di = o.cpu().numpy(), dw.cpu().numpy(), di.cpu().numpy()
+    o64, dw64, di64 = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
+    assert_parity(o, o64, f"{mode} O")
+    assert_parity(di, di64, f"{mode} dI")
+    dwd = dw if mode == "dense" else layer.compact_to_dense(dw.astype(np.float64))
+    mask = w_f != 0
+    assert fail_fraction(np.asarray(dwd)[mask], dw64[mask]) < 1e-3, f"{mode} dW_F"
+    if mode == "int8":  # the exact-product SDDMM on the same operands, within one rounding
+        layer.set_dw_mode("sddmm")
+        ref = layer.backward_weights(g, cache).cpu().numpy()
+        assert_parity(dw, ref, "int8 dW_F vs SDDMM")
