@@ -496,7 +496,9 @@ constexpr int kChunkThreads = 1024;
 void plan_sddmm_chunk(wino_plan* p) {
     p->lane_rows = 0;
     const int64_t budget = std::min(p->max_smem, 220 * 1024);
+    static const int tw_env = std::getenv("WINO_SDDMM_TW") ? std::atoi(std::getenv("WINO_SDDMM_TW")) : 0;
     for (int tw : {128, 64}) {
+        if (tw_env && tw != tw_env) continue;
         const int64_t cap_rows = budget / (tw * 4) - p->C;
         if (cap_rows < 8) continue;
         const int64_t need = round_up(p->K, 8);
