@@ -241,6 +241,9 @@ struct wino_cache {
     int dw_chunks = 0;      // SDDMM chunks whose dW partials backward_range already computed
     float* Vlo = nullptr;   // precise dW mode: fp32 residuals of Ĩ_F and dZ
     float* DZlo = nullptr;
+    float* Vt = nullptr;    // tensor-core plans: tf32 lo halves of Ĩ_F and dZ (V / DZ hold the hi
+    float* DZt = nullptr;   // halves) when the producers split the operands (tf32_presplit)
+    bool v_split = false, dz_split = false;
     bool has_fwd = false;
     bool has_grad_z = false;
 };
@@ -640,7 +643,8 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, w
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
         wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTr, 256, p->sm_count), 256, 0, st>>>(
-            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr);
+            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr,
+            (c && c->v_split && V == c->V) ? c->Vt : nullptr);
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
@@ -656,18 +660,18 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, w
 
 template <int M, int P, class CF>
 int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
-                  int64_t NT, int64_t NTs, bool mask, int64_t NTr) {
+                  int64_t NT, int64_t NTs, bool mask, int64_t NTr, float* DZt = nullptr) {
     const wino_geometry& g = p->g;
     Launch L(p, st, K_GRADZ);
     const int grid = grid_for((int64_t)p->K * NTr, 256, p->sm_count);
     if (mask)
         wino::grad_z_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                              (int)NT, (int)NTs, (int)NTr);
+                                                              (int)NT, (int)NTs, (int)NTr, DZt);
     else
         wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                               (int)NT, (int)NTs, (int)NTr);
+                                                               (int)NT, (int)NTs, (int)NTr, DZt);
     return L.done();
 }
 
@@ -769,9 +773,12 @@ int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
     return WINO_OK;
 }
 
-template <bool A_SPLIT, bool B_MN>
+// B_PRE: B pre-split by its producer (bl = its tf32 lo half); only the warp-specialised kernel
+// takes it (tf32_presplit() guarantees that kernel is the one selected)
+template <bool A_SPLIT, bool B_MN, bool B_PRE = false>
 int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
-              const CUtensorMap& b, float* D, int M, int N, int Kd, int64_t ldd, int splits) {
+              const CUtensorMap& b, float* D, int M, int N, int Kd, int64_t ldd, int splits,
+              const CUtensorMap* bl = nullptr) {
     const int kb_total = (Kd + wino::tc::BK - 1) / wino::tc::BK;
     const int kb_per = (kb_total + splits - 1) / splits;
     const int bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
@@ -817,53 +824,64 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
                            wino::make_map_3d_sw(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2 * splits,
                                                 (uint64_t)ldd * 4, (uint64_t)M * ldd * 4, dw == 8 ? 32 : 16, 32,
                                                 dw == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-        // 2 split warps: 4 would cap registers at 128/thread and spill the drain's 64 Kahan pairs
-        constexpr int SW = 2;
+        // 2 split warps (4 would cap registers at 128/thread and spill the drain's 64 Kahan pairs);
+        // none when both operands arrive pre-split
+        constexpr int SW = (!A_SPLIT && B_PRE) ? 0 : 2;
         auto go_ws = [&](auto kern, int drain_warps) {
             set_smem_attr(kern, wino::tc::flush::WS_SMEM_BYTES);
             const int ctas = std::min(ntiles, p->sm_count);
             kern<<<ctas, 64 + 32 * (SW + drain_warps), wino::tc::flush::WS_SMEM_BYTES, st>>>(
-                ah, al, b, md, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y, ntiles);
+                ah, al, b, md, bl ? *bl : b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y,
+                ntiles);
         };
+        if (B_PRE && !(ws_ok && dw == 8))
+            return set_err(WINO_CAPABILITY_ERROR, "pre-split operands need the warp-specialised tcgen05 kernel");
         if (ws_ok && dw == 8 && !fp64_fold)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4>, 8);
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4, B_PRE>, 8);
         else if (ws_ok && dw == 8)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, false, 4>, 8);
-        else if (ws_ok && !fp64_fold)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, true, 4>, 16);
-        else if (ws_ok)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, false, 4>, 16);
-        else if (persistent && fold == 1 && epi == 8)
-            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 8>, 64 + 32 * 8);
-        else if (persistent && fold == 1)
-            go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 16>, 64 + 32 * 16);
-        else if (fold == 2)
-            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
-        else if (fold == 4)
-            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 4>);
-        else
-            go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>);
+            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, false, 4, B_PRE>, 8);
+        else if constexpr (!B_PRE) {
+            if (ws_ok && !fp64_fold)
+                go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, true, 4>, 16);
+            else if (ws_ok)
+                go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, false, 4>, 16);
+            else if (persistent && fold == 1 && epi == 8)
+                go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 8>, 64 + 32 * 8);
+            else if (persistent && fold == 1)
+                go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 16>, 64 + 32 * 16);
+            else if (fold == 2)
+                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
+            else if (fold == 4)
+                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 4>);
+            else
+                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>);
+        }
     }
     return L.done();
 }
 
 // D[s] = W-operand[s] · B[s] on the tensor cores; B = [P2][Kd][NTs] activations (MN-major).
 int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
-                   const float* B, float* D, int M, int Kd, int64_t NTs) {
-    CUtensorMap mb;
-    if (!wino::make_map_3d(&mb, B, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true))
+                   const float* B, float* D, int M, int Kd, int64_t NTs, const float* Blo = nullptr) {
+    CUtensorMap mb, mbl;
+    if (!wino::make_map_3d(&mb, B, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true) ||
+        (Blo && !wino::make_map_3d(&mbl, Blo, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true)))
         return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the activation operand (CUresult " +
                                             std::to_string(wino::last_tmap_error()) + ")");
+    if (Blo) return launch_tc<false, true, true>(p, st, kind, ah, al, mb, D, M, (int)NTs, Kd, NTs, 1, &mbl);
     return launch_tc<false, true>(p, st, kind, ah, al, mb, D, M, (int)NTs, Kd, NTs, 1);
 }
 
 // dW_F = dZ·Ĩ_Fᵀ on the tensor cores, split over NT, partials summed in fp64 -> K×C×p×q.
 int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs,
-                 bool masked = false) {
-    CUtensorMap ma, mb;
+                 bool masked = false, const float* DZlo = nullptr, const float* Vlo = nullptr) {
+    CUtensorMap ma, mb, mal, mbl;
     const uint32_t bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
+    const bool pre = DZlo && Vlo;  // both operands pre-split by their producers (K4, K1)
     if (!wino::make_map_3d(&ma, DZ, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128) ||
-        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn))
+        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn) ||
+        (DZlo && !wino::make_map_3d(&mal, DZlo, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128)) ||
+        (Vlo && !wino::make_map_3d(&mbl, Vlo, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn)))
         return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for dZ / Ĩ_F (CUresult " +
                                             std::to_string(wino::last_tmap_error()) + ")");
     const int tiles = ((p->C + (int)bn - 1) / (int)bn) * ((p->K + wino::tc::BM - 1) / wino::tc::BM) * p->P2;
@@ -876,7 +894,15 @@ int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V,
     if (rc) return rc;
     part = p->d_dwc;
     const int kind = masked ? K_SDDMM : K_DENSE_DW;
-    if ((rc = launch_tc<true, false>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits))) return rc;
+    if (pre)
+        rc = launch_tc<false, false, true>(p, st, kind, ma, mal, mb, part, p->K, p->C, (int)NTs, p->C, splits, &mbl);
+    else if (Vlo)  // only Ĩ_F pre-split (dZ from a range backward): A still split in shared memory
+        rc = launch_tc<true, false, true>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits, &mbl);
+    else if (DZlo)
+        rc = launch_tc<false, false>(p, st, kind, ma, mal, mb, part, p->K, p->C, (int)NTs, p->C, splits);
+    else
+        rc = launch_tc<true, false>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits);
+    if (rc) return rc;
     Launch L(p, st, kind);
     if (masked)
         wino::tc::reduce_dw_masked_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
@@ -1370,6 +1396,35 @@ int wino_values_updated(wino_plan* p, void* stream) {
     return rc;
 }
 
+// Every reader of Ĩ_F and dZ on this plan is a tcgen05 GEMM through the warp-specialised kernel
+// (dense plan, or tensor-core contraction with the tensor-core dW): the producers then write the
+// tf32 hi/lo split once (input_transform_kernel / grad_z_kernel) and the GEMMs skip their own.
+// Opt-in (WINO_TC_PRESPLIT=1): measured at c3 dense 2041 vs 1945 µs — the dW GEMM gains (581 ->
+// 401 µs) but K1/K4 write twice the bytes (+50/+90 µs) and the forward/dĨ_F GEMMs, which were not
+// split-bound, load twice the B bytes (+25/+40 µs); c1 with the tensor-core contraction: 141 vs 148.
+static bool ws_kernel_selected() {
+    static const bool ok = !(std::getenv("WINO_TC_WS") && std::atoi(std::getenv("WINO_TC_WS")) == 0) &&
+                           !(std::getenv("WINO_TC_FOLD") && std::atoi(std::getenv("WINO_TC_FOLD")) != 1) &&
+                           !(std::getenv("WINO_TC_PERSISTENT") && std::atoi(std::getenv("WINO_TC_PERSISTENT")) == 0) &&
+                           !(std::getenv("WINO_TC_DW") && std::atoi(std::getenv("WINO_TC_DW")) != 8);
+    return ok;
+}
+static bool tc_dw_path(const wino_plan* p) {
+    return p->dense || p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
+}
+static bool tf32_presplit(const wino_plan* p) {
+    static const bool env = std::getenv("WINO_TC_PRESPLIT") && std::atoi(std::getenv("WINO_TC_PRESPLIT")) == 1;
+    return env && p->tc_ready && !p->tc_fast && p->dw_mode != 2 && ws_kernel_selected() &&
+           (p->dense || p->contraction == 1) && tc_dw_path(p);
+}
+static int ensure_cache_t(wino_plan* p, wino_cache* c) {
+    if (c->Vt) return WINO_OK;
+    const int64_t NTs = round_up((int64_t)c->n_max * p->g.t, 4);
+    CUDA_TRY(cudaMalloc(&c->Vt, (size_t)p->P2 * p->C * NTs * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&c->DZt, (size_t)p->P2 * p->K * NTs * sizeof(float)));
+    return WINO_OK;
+}
+
 static int ensure_cache_lo(wino_plan* p, wino_cache* c) {
     if (c->Vlo) return WINO_OK;
     const int64_t NTs = round_up((int64_t)c->n_max * p->g.t, 4);
@@ -1407,6 +1462,8 @@ int wino_cache_destroy(wino_cache* c) {
     if (!c) return WINO_OK;
     if (c->V) cudaFree(c->V);
     if (c->DZ) cudaFree(c->DZ);
+    if (c->Vt) cudaFree(c->Vt);
+    if (c->DZt) cudaFree(c->DZt);
     if (c->Vlo) cudaFree(c->Vlo);
     if (c->DZlo) cudaFree(c->DZlo);
     delete c;
@@ -1432,6 +1489,10 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         V = p->d_dv;  // inference: the backward scratch doubles as Ĩ_F
     }
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
+    if (cache) {
+        cache->v_split = tf32_presplit(p);
+        if (cache->v_split && (rc = ensure_cache_t(p, cache))) return rc;
+    }
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0, NTs)))
         return rc;
     if (cache && p->dw_mode == 2) {
@@ -1439,7 +1500,8 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         if ((rc = DISPATCH_MP(p, launch_input_lo, p, st, input, V, cache->Vlo, NT, NTs))) return rc;
     }
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs,
+                            cache && cache->v_split ? cache->Vt : nullptr);
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
@@ -1473,7 +1535,13 @@ static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_
                       cudaStream_t st) {
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs);
+    c->dz_split = tf32_presplit(p);
+    if (c->dz_split) {
+        const int rc0 = ensure_cache_t(p, c);
+        if (rc0) return rc0;
+    }
+    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs,
+                         c->dz_split ? c->DZt : nullptr);
     if (rc) return rc;
     if (p->dw_mode == 2)
         rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask);
@@ -1485,13 +1553,18 @@ static int bwd_dw(wino_plan* p, const wino_cache* c, float* grad_w, cudaStream_t
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
     const bool precise = p->dw_mode == 2;
     int rc = WINO_OK;
-    if (p->dense && p->tc_ready && !precise) return launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs);
+    const float* dzt = c->dz_split ? c->DZt : nullptr;
+    const float* vt = c->v_split ? c->Vt : nullptr;
+    if (p->dense && p->tc_ready && !precise) return launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs, false, dzt, vt);
+    if ((c->v_split || c->dz_split) && !(!p->dense && tc_dw_path(p) && p->nnz > 0))
+        return set_err(WINO_CONSISTENCY_ERROR, "the cache holds tensor-core split operands: rerun the forward "
+                                               "after changing the dW mode / contraction");
     float* dwc = grad_w;
     if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
     if (p->dense) dwc = p->d_dwc;
     const bool tc_dw = p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
     if (!p->dense && tc_dw && p->nnz > 0)
-        rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true);
+        rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true, dzt, vt);
     else if (!p->dense && p->dw_mode == 3 && p->nnz > 0)
         rc = launch_ozaki_dw(p, st, c->DZ, c->V, dwc, NT, NTs);
     else if (precise)
@@ -1514,7 +1587,11 @@ static int bwd_input(wino_plan* p, const wino_cache* c, float* grad_input, cudaS
     int rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs);
     if (rc) return rc;
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
+        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs,
+                            c->dz_split ? c->DZt : nullptr);
+    else if (c->dz_split)
+        return set_err(WINO_CONSISTENCY_ERROR, "the cache holds tensor-core split operands: rerun the backward "
+                                               "after changing the contraction");
     else
         rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
     if (rc) return rc;
@@ -1598,6 +1675,8 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
     if (p->dw_mode == 2 && (rc = ensure_cache_lo(p, c))) return rc;
+    c->v_split = tf32_presplit(p);
+    if (c->v_split && (rc = ensure_cache_t(p, c))) return rc;
     c->n = n;
     c->NTs = NTs;
     c->has_fwd = true;
@@ -1622,7 +1701,8 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
     CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs);
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs,
+                            c->v_split ? c->Vt : nullptr);
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, c->V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
@@ -1674,6 +1754,7 @@ int wino_forward_range(wino_plan* p, int n_total, int n0, int n1, const float* i
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * r.NTs))) return rc;
     float* V = cache->V + r.a;
     float* Z = p->d_z + r.a;
+    cache->v_split = false;  // range calls run the CSR kernels on fp32 operands
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, Z, n1 - n0, r.NT, r.NTs, flags, 0,
                           r.NTr)))
         return rc;
@@ -1705,6 +1786,7 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * r.NTs))) return rc;
     float* DZ = c->DZ + r.a;
     float* DV = p->d_dv + r.a;
+    c->dz_split = false;
     if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, DZ, r.NT, r.NTs, mask, r.NTr)))
         return rc;
     if ((rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, DZ, DV, p->C, p->K, r.NT, r.NTs,

@@ -742,16 +742,20 @@ gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, c
 //   reads TMEM lane quarter w % 4 and column block of COLS = BN/(DW/4) columns).
 // NBUF TMEM accumulators let the MMA run NBUF-1 k-blocks ahead of the drain.  Same arithmetic
 // per tile as gemm_3xtf32_flush_persistent_kernel (bitwise, with KAHAN = false).
-template <bool A_SPLIT, bool B_MN, int SW, int DW, bool KAHAN, int NBUF>
+// B_PRE: B arrives already split (hi through mapB, lo through mapBl; the producers wrote both,
+// wino_kernels.cuh tf32_split); with A pre-split too there is nothing to split (SW = 0).
+template <bool A_SPLIT, bool B_MN, int SW, int DW, bool KAHAN, int NBUF, bool B_PRE = false>
 __global__ void __launch_bounds__(64 + 32 * (SW + DW), 1)
 gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
                       const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapD,
+                      const __grid_constant__ CUtensorMap mapBl,
                       float* __restrict__ D, int M, int N, int Kd,
                       int64_t ldd, int slices, int splits, int kb_per, int tiles_n, int tiles_m, int ntiles) {
     constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
     constexpr int STAGE_BYTES = flush::STAGE_BYTES;
     constexpr int TMEM_COLS = NBUF * BN;
     static_assert(TMEM_COLS <= 512 && (NBUF & (NBUF - 1)) == 0, "TMEM holds 512 columns");
+    static_assert(SW > 0 || (!A_SPLIT && B_PRE), "nothing to split needs no split warps");
     static_assert(DW == 8 || DW == 16, "drain warps: 4 lane quarters x 2 or 4 column blocks");
     constexpr int COLS = BN / (DW / 4);
     // output staging box per drain warp: 32 rows x BOXC columns (4 KB with a 128-byte swizzle for
@@ -785,7 +789,7 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&split[i], 32 * SW);
+            mbar_init(&split[i], SW > 0 ? 32 * SW : 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < NBUF; ++i) {
@@ -815,15 +819,20 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                     if (kbg >= STAGES) mbar_wait(&empty[st], ((kbg / STAGES) - 1) & 1);
                     uint8_t* base = stage_ptr(st);
                     const int kk = (t.kb0 + kb) * BK;
-                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
+                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + (B_PRE ? 2 : 1) * B_TILE);
                     tma_load_3d(base, &mapAh, &full[st], kk, t.m0, t.s);
                     if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, t.m0, t.s);
                     if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 32; ++j)
+                        for (int j = 0; j < BN / 32; ++j) {
                             tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], t.n0 + 32 * j, kk, t.s);
+                            if (B_PRE)
+                                tma_load_3d(base + 2 * A_TILE + B_TILE + j * (BK * 128), &mapBl, &full[st],
+                                            t.n0 + 32 * j, kk, t.s);
+                        }
                     } else {
                         tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, t.n0, t.s);
+                        if (B_PRE) tma_load_3d(base + 2 * A_TILE + B_TILE, &mapBl, &full[st], kk, t.n0, t.s);
                     }
                 }
             }
@@ -837,7 +846,10 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                 for (int kb = 0; kb < t.kblocks; ++kb, ++kbg, ++gg) {
                     const int st = kbg % STAGES, b = gg % NBUF;
                     if (gg >= NBUF) mbar_wait(&tempty[b], ((gg / NBUF) - 1) & 1);
-                    mbar_wait(&split[st], (kbg / STAGES) & 1);
+                    if constexpr (SW > 0)
+                        mbar_wait(&split[st], (kbg / STAGES) & 1);
+                    else
+                        mbar_wait(&full[st], (kbg / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t a_hi = smem_u32(stage_ptr(st));
                     const uint32_t a_lo = a_hi + A_TILE;
@@ -875,7 +887,7 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                 mbar_wait(&full[st], (kbg / STAGES) & 1);
                 uint8_t* base = stage_ptr(st);
                 if (A_SPLIT) split_tile_fast(base, base + A_TILE, A_TILE, ts, 32 * SW);
-                split_tile_fast(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, ts, 32 * SW);
+                if (!B_PRE) split_tile_fast(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, ts, 32 * SW);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&split[st]);
             }
@@ -898,23 +910,27 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                 mbar_wait(&tfull[b], (gg / NBUF) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + cb * COLS);
+                // 8-column TMEM loads: fewer live registers next to the 2·COLS accumulator words
 #pragma unroll
-                for (int c = 0; c < COLS; c += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(ta + c, v);
+                for (int c = 0; c < COLS; c += 8) {
+                    uint32_t v[8];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                                   "=r"(v[6]), "=r"(v[7])
+                                 : "r"(ta + c));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (c + 16 == COLS) {  // the buffer is free once the last columns are in registers
+                    if (c + 8 == COLS) {  // the buffer is free once the last columns are in registers
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         mbar_arrive(&tempty[b]);
                     }
                     if constexpr (KAHAN) {
 #pragma unroll
-                        for (int j = 0; j < 16; j += 2)
+                        for (int j = 0; j < 8; j += 2)
                             kahan2(accd[c + j], accd[c + j + 1], comp[c + j], comp[c + j + 1], __uint_as_float(v[j]),
                                    __uint_as_float(v[j + 1]));
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) accd[c + j] += (double)__uint_as_float(v[j]);
+                        for (int j = 0; j < 8; ++j) accd[c + j] += (double)__uint_as_float(v[j]);
                     }
                 }
             }

@@ -71,6 +71,14 @@ __device__ __forceinline__ float cmadd(float acc, float c, float x) {
     return madd(acc, c, x);
 }
 
+// tf32 hi/lo split of an fp32 value, bitwise the split the tcgen05 GEMM would do in shared
+// memory (wino_dense_tc.cuh split_tile_fast): hi = rna_tf32(x), lo = rna_tf32(x - hi).
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+    const uint32_t h = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+    hi = __uint_as_float(h);
+    lo = __uint_as_float((__float_as_uint(__fsub_rn(x, hi)) + 0x1000u) & 0xffffe000u);
+}
+
 // ---------------------------------------------------------------------------------
 // K1: φ gather (pad folded in) + Ĩ_F = B1ᵀ·d·B2   (transforms.cpp:196-210, sparse.cpp:94-120)
 // One thread per (c, nt); consecutive threads = consecutive tiles -> coalesced stores.
@@ -78,7 +86,10 @@ __device__ __forceinline__ float cmadd(float acc, float c, float x) {
 template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
-                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr) {
+                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr,
+                       float* __restrict__ Vt = nullptr) {
+    // Vt != nullptr (tensor-core plans): V receives the tf32 hi part and Vt the lo part, the
+    // operand split done once here instead of in every GEMM tile that reads the value
     // columns [0, NTr) of V rows with stride NTs (a column range of the batch when V and `in` are
     // offset to its first image); columns ≥ NT are the zero padding
     const int64_t plane = (int64_t)C * NTs;
@@ -126,7 +137,15 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                 float acc = 0.f;
 #pragma unroll
                 for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
-                V[(int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt] = acc;
+                const int64_t o = (int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt;
+                if (Vt) {
+                    float hi, lo;
+                    tf32_split(acc, hi, lo);
+                    V[o] = hi;
+                    Vt[o] = lo;
+                } else {
+                    V[o] = acc;
+                }
             }
     }
 }
@@ -189,7 +208,8 @@ template <int M, int P, bool MASK, class CF>
 __global__ void __launch_bounds__(256)
 grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
               float* __restrict__ DZ, const Coefs cf, int K, int Ho, int Wo, int tiles_x, int T,
-              int NT, int NTs, int NTr) {
+              int NT, int NTs, int NTr, float* __restrict__ DZt = nullptr) {
+    // DZt != nullptr: tf32 hi part into DZ, lo part into DZt (as input_transform_kernel)
     const int64_t plane = (int64_t)K * NTs;
     const int64_t items = (int64_t)K * NTr;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
@@ -239,7 +259,15 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
                 float acc = 0.f;
 #pragma unroll
                 for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), m1[i][x]);
-                DZ[(int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt] = acc;
+                const int64_t o = (int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt;
+                if (DZt) {
+                    float hi, lo;
+                    tf32_split(acc, hi, lo);
+                    DZ[o] = hi;
+                    DZt[o] = lo;
+                } else {
+                    DZ[o] = acc;
+                }
             }
     }
 }
