@@ -17,6 +17,7 @@
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
 #include "wino_ozaki.cuh"
+#include "wino_spmm_tmem.cuh"
 #include "wino_precise.cuh"
 #include "wino_tmap.h"
 #include "wino_update.cuh"
@@ -424,10 +425,38 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
 // X, Y may point at column `a` of their rows (a column range of the batch): NT = valid columns
 // of the range, NTs = the row stride, NTr = columns the range owns (≥ NT on the batch's last range,
 // which also owns the zero padding).  The whole batch: NTr = NTs.
+// the SpMM with X in tensor memory (wino_spmm_tmem.cuh): 16 rows per warp when that still fills
+// the GPU, else 8
+int launch_spmm_tmem(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
+                     const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NTs,
+                     int64_t NTr) {
+    namespace ws = wino::st;
+    const int chunks = (int)((NTr + ws::TW - 1) / ws::TW);
+    const int64_t base = (int64_t)chunks * p->P2;
+    const bool big = base * ((nrows + 63) / 64) >= p->sm_count;
+    const int rpb = big ? 64 : 32;
+    const size_t smem = (size_t)max_segment(hptr, p->P2, nrows, rpb) * sizeof(int2) + 16;
+    if ((int)smem > p->max_smem) return set_err(WINO_CAPABILITY_ERROR, "spmm (tmem): CSR segment exceeds shared memory");
+    Launch L(p, st, kind);
+    const dim3 grid((unsigned)((nrows + rpb - 1) / rpb), (unsigned)chunks, (unsigned)p->P2);
+    if (big) {
+        set_smem_attr(ws::spmm_tmem_kernel<16>, (int)smem);
+        ws::spmm_tmem_kernel<16><<<grid, ws::THREADS, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs,
+                                                                 (int)NTr, -0.0f);
+    } else {
+        set_smem_attr(ws::spmm_tmem_kernel<8>, (int)smem);
+        ws::spmm_tmem_kernel<8><<<grid, ws::THREADS, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs,
+                                                                (int)NTr, -0.0f);
+    }
+    return L.done();
+}
+
 int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs, int64_t NTr = -1) {
     if (NTr < 0) NTr = NTs;
+    static const bool tmem = std::getenv("WINO_SPMM_TMEM") && std::atoi(std::getenv("WINO_SPMM_TMEM")) == 1;
+    if (tmem && ncols <= 1024) return launch_spmm_tmem(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NTs, NTr);
     switch (spmm_r(ncols)) {
         case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
         case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
