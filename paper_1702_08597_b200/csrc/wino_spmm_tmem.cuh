@@ -18,10 +18,10 @@
 // tcgen05.st by the warps of the matching quarter.
 //
 // Status: opt-in (WINO_SPMM_TMEM=1), bitwise equal to spmm_kernel on every parity test, but
-// measured slower (c1 63 vs 40 µs, c3 727 vs 543 µs, c2 744 vs 703 µs): the kernel issues ~3x the
-// instructions of the microbenchmark loop per multiply-add (row/pass boundaries, tails of < 8
-// nonzeros per row and pass) and the TMEM fill is not overlapped with the products (one 512-column
-// buffer per SM); see DESIGN.md §7.
+// measured at parity at c2 (705 vs 703 µs) and slower at c1 (59 vs 40 µs) and c3 (696 vs 543 µs):
+// the kernel issues more instructions per multiply-add than the microbenchmark loop (row/pass
+// boundaries, tails of < 8 nonzeros per row and pass) and the TMEM fill is not overlapped with the
+// products (one 512-column buffer per SM); see DESIGN.md §7.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -164,15 +164,26 @@ spmm_tmem_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval
                     acc[i][1] = madd2(acc[i][1], w2, pk2(x[u][2], x[u][3]), n0);
                 }
             }
-            for (; e < ee; ++e) {  // tail, one at a time (a predicated batch measured slower)
-                const int2 cv = cvs[e];
-                float x[4];
-                tld4(tq + 4 * (cv.x - c0), x);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const float w = __int_as_float(cv.y);
-                const unsigned long long w2 = pk2(w, w);
-                acc[i][0] = madd2(acc[i][0], w2, pk2(x[0], x[1]), n0);
-                acc[i][1] = madd2(acc[i][1], w2, pk2(x[2], x[3]), n0);
+            // tail of < U entries in batches of 4, 2, 1: at most three load waits
+#pragma unroll
+            for (int b = U / 2; b >= 1; b >>= 1) {
+                if (ee - e >= b) {
+                    int2 cv[U / 2];
+                    float x[U / 2][4];
+#pragma unroll
+                    for (int u = 0; u < b; ++u) cv[u] = cvs[e + u];
+#pragma unroll
+                    for (int u = 0; u < b; ++u) tld4(tq + 4 * (cv[u].x - c0), x[u]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int u = 0; u < b; ++u) {
+                        const float w = __int_as_float(cv[u].y);
+                        const unsigned long long w2 = pk2(w, w);
+                        acc[i][0] = madd2(acc[i][0], w2, pk2(x[u][0], x[u][1]), n0);
+                        acc[i][1] = madd2(acc[i][1], w2, pk2(x[u][2], x[u][3]), n0);
+                    }
+                    e += b;
+                }
             }
         }
     }
