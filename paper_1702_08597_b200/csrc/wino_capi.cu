@@ -844,7 +844,8 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
         // the dW GEMM (A split in shared memory too) measured faster with the fp64 fold (551 vs 584
         // µs at c3): its two split warps, not the drain, bound it, and the fp64 fold does not spill
         static const bool fp64_env = std::getenv("WINO_TC_ACC") && std::string(std::getenv("WINO_TC_ACC")) == "fp64";
-        const bool fp64_fold = fp64_env || A_SPLIT;
+        static const bool dw_kahan = std::getenv("WINO_TC_DW_ACC") && std::string(std::getenv("WINO_TC_DW_ACC")) == "kahan";
+        const bool fp64_fold = fp64_env || (A_SPLIT && !dw_kahan);
         // drain warps: 8 (64 columns each, 4 KB SW128 output boxes; measured 4% faster at c3 than
         // WINO_TC_DW=16 with 32 columns and 2 KB SW64 boxes)
         static const int dw = std::getenv("WINO_TC_DW") ? std::atoi(std::getenv("WINO_TC_DW")) : 8;
