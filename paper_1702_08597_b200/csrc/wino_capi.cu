@@ -848,7 +848,13 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
         const bool fp64_fold = fp64_env || (A_SPLIT && !dw_kahan);
         // drain warps: 8 (64 columns each, 4 KB SW128 output boxes; measured 4% faster at c3 than
         // WINO_TC_DW=16 with 32 columns and 2 KB SW64 boxes)
-        static const int dw = std::getenv("WINO_TC_DW") ? std::atoi(std::getenv("WINO_TC_DW")) : 8;
+        static const int dw_env = std::getenv("WINO_TC_DW") ? std::atoi(std::getenv("WINO_TC_DW")) : 8;
+        // the dW GEMM (A and B split in shared memory, fp64 fold) is split-bound with 2 split warps:
+        // it runs 4 split warps next to 16 drain warps of 32 columns (80 registers per thread;
+        // c3: 581 -> 521 µs; 6 split warps 526 µs; WINO_TC_DWGEMM_SW=2 restores the 2 + 8 layout)
+        static const int dwgemm_sw = std::getenv("WINO_TC_DWGEMM_SW") ? std::atoi(std::getenv("WINO_TC_DWGEMM_SW")) : 4;
+        const bool wide_split = A_SPLIT && !B_PRE && fp64_fold && dwgemm_sw != 2;
+        const int dw = wide_split ? 16 : dw_env;
         CUtensorMap md;
         const bool ws_ok = ws && persistent && fold == 1 && (ldd & 3) == 0 &&
                            wino::make_map_3d_sw(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2 * splits,
@@ -866,6 +872,23 @@ int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, co
         };
         if (B_PRE && !(ws_ok && dw == 8))
             return set_err(WINO_CAPABILITY_ERROR, "pre-split operands need the warp-specialised tcgen05 kernel");
+        auto go_ws_sw = [&](auto kern, int split_warps, int drain_warps) {
+            set_smem_attr(kern, wino::tc::flush::WS_SMEM_BYTES);
+            const int ctas = std::min(ntiles, p->sm_count);
+            kern<<<ctas, 64 + 32 * (split_warps + drain_warps), wino::tc::flush::WS_SMEM_BYTES, st>>>(
+                ah, al, b, md, bl ? *bl : b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y,
+                ntiles);
+        };
+        if constexpr (A_SPLIT && !B_PRE) {
+            if (ws_ok && wide_split && dwgemm_sw == 4) {
+                go_ws_sw(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, 4, 16, false, 4>, 4, 16);
+                return L.done();
+            }
+            if (ws_ok && wide_split) {
+                go_ws_sw(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, 6, 16, false, 4>, 6, 16);
+                return L.done();
+            }
+        }
         if (ws_ok && dw == 8 && !fp64_fold)
             go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4, B_PRE>, 8);
         else if (ws_ok && dw == 8)
