@@ -1,7 +1,7 @@
 # SDDMM launch-shape sweep at c1 / c3 (env overrides of plan_sddmm); prints sddmm µs per step.
 mkdir -p gpurun_out/ss
 run() { tag=$1; shift; env "$@" python bench.py --steps 10 --warmup 3 --no-cpu-baseline $CFG > gpurun_out/ss/$tag.log 2>&1;
-  tail -1 gpurun_out/ss/$tag.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']['sddmm_dw']; print('$tag', round(d['ms_per_step']*1e3,1), 'us/step; sddmm', round(k['ms_per_step']*k['launches']/3*1e3,1), 'us/step')"; }
+  tail -1 gpurun_out/ss/$tag.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']['sddmm_dw']; print('$tag', round(d['ms_per_step']*1e3,1), 'us/step; sddmm', round(k['ms_per_step']*1e3,1), 'us/step')"; }
 CFG=""
 run c1_def X=1
 for sp in 1 2 4; do run c1_sp$sp WINO_SDDMM_SPLITS=$sp; done
