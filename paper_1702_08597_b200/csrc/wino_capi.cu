@@ -455,7 +455,8 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs, int64_t NTr = -1) {
     if (NTr < 0) NTr = NTs;
-    static const bool tmem = std::getenv("WINO_SPMM_TMEM") && std::atoi(std::getenv("WINO_SPMM_TMEM")) == 1;
+    // read on every launch (not cached): tests switch it per case
+    const bool tmem = std::getenv("WINO_SPMM_TMEM") && std::atoi(std::getenv("WINO_SPMM_TMEM")) == 1;
     if (tmem && ncols <= 1024) return launch_spmm_tmem(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NTs, NTr);
     switch (spmm_r(ncols)) {
         case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);

@@ -749,3 +749,40 @@ def test_ragged_tile_shapes(mode):
         layer.set_dw_mode("sddmm")
         ref = layer.backward_weights(g, cache).cpu().numpy()
         assert_parity(dw, ref, "int8 dW_F vs SDDMM")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tmem", [False, True])
+def test_c2_shape_forward_bitwise(tmem, monkeypatch):
+    """configs[2]'s layer shape (C = K = 512, H = W = 28, 90%) on 2 images: the SpMM takes its
+    2-wide-t variant (a 512-row X chunk does not fit shared memory at 4-wide) — or, with
+    WINO_SPMM_TMEM=1, the tensor-memory SpMM in 4 passes — and the forward stays bitwise the f32
+    mirror of the reference's sparse_forward<float>."""
+    from paper_1702_08597_b200.synth import LayerConfig
+
+    if tmem:
+        monkeypatch.setenv("WINO_SPMM_TMEM", "1")
+    cfg = CONFIGS["c2"]
+    img, w_f, _ = make_inputs(LayerConfig("c2", 2, cfg.c, cfg.k, cfg.h, 0.9))
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.h, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    o = layer.forward(dev(img)).cpu().numpy()
+    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
+    assert np.array_equal(o, mir["o"])
+
+
+def test_tmem_spmm_bitwise_equals_shared_memory_spmm(monkeypatch):
+    """configs[1] forward + backward with the tensor-memory SpMM (WINO_SPMM_TMEM=1: 2 passes for
+    the forward's 256 X rows, 3 for dĨ_F's 384) is bitwise the default shared-memory SpMM."""
+    cfg = CONFIGS["c1"]
+    img, w_f, go = make_inputs(cfg)
+    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    x, g = dev(img), dev(go)
+    ref = layer.forward_backward(x, g, layer.new_cache(cfg.n))
+    torch.cuda.synchronize()
+    monkeypatch.setenv("WINO_SPMM_TMEM", "1")
+    got = layer.forward_backward(x, g, layer.new_cache(cfg.n))
+    torch.cuda.synchronize()
+    for a, b, what in zip(ref, got, ("O", "dW_F", "dI")):
+        assert torch.equal(a, b), what
