@@ -786,3 +786,22 @@ def test_tmem_spmm_bitwise_equals_shared_memory_spmm(monkeypatch):
     torch.cuda.synchronize()
     for a, b, what in zip(ref, got, ("O", "dW_F", "dI")):
         assert torch.equal(a, b), what
+
+
+@pytest.mark.parametrize("name", LAYER_CASES)
+def test_forward_backward_golden(name):
+    """wino_forward_backward on every golden layer (F(2,3), F(4,3), F(6,3); odd, padded, dense, tiny
+    shapes): O bitwise the reference's f32 sparse_forward where the golden file has it, and O, dI,
+    dW_F bitwise the separate forward + backward calls."""
+    d = load_layer(name)
+    layer = wb.WinogradLayer(d["c"], d["k"], d["h"], d["w"], pad=d["pad"], m=d["m"])
+    layer.set_weights(d["w_f"], dense=False)
+    x, g = dev(d["img"]), dev(d["grad_o"])
+    c1 = layer.new_cache(d["n"])
+    o1 = layer.forward(x, c1)
+    w1, i1 = layer.backward(g, c1)
+    o2, w2, i2 = layer.forward_backward(x, g, layer.new_cache(d["n"]))
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(w1, w2) and torch.equal(i1, i2)
+    if "o_sparse_f32" in d:
+        assert np.array_equal(o2.cpu().numpy(), d["o_sparse_f32"])
