@@ -16,11 +16,9 @@
 #include "wino_compress.cuh"
 #include "wino_dense_tc.cuh"
 #include "wino_kernels.cuh"
-#include "wino_ozaki.cuh"
-#include "wino_spmm_tmem.cuh"
-#include "wino_precise.cuh"
 #include "wino_tmap.h"
 #include "wino_update.cuh"
+#include "wino_xdw.cuh"
 
 namespace {
 
@@ -140,15 +138,23 @@ int make_geometry(int64_t c, int64_t h_i, int64_t w_i, int m, int r, wino_geomet
     return WINO_OK;
 }
 
-enum Kind { K_INPUT = 0, K_SPMM, K_OUTPUT, K_GRADZ, K_SDDMM, K_SPMM_T, K_INGRAD, K_DENSE_FWD,
-            K_DENSE_DW, K_DENSE_DV, K_SGD, K_MISC, K_NKINDS };
-const char* kKindNames[K_NKINDS] = {"input_transform", "spmm_fwd", "output_transform", "grad_z",
-                                    "sddmm_dw", "spmm_bwd_data", "input_grad", "dense_fwd_tc",
-                                    "dense_dw_tc", "dense_dv_tc", "sgd", "misc"};
+enum Kind { K_INPUT = 0, K_SPMM, K_OUTPUT, K_GRADZ, K_DW_DIGITS, K_DW_GEMM, K_DW_REDUCE, K_SPMM_T, K_INGRAD,
+            K_DENSE_FWD, K_DENSE_DV, K_SGD, K_MISC, K_NKINDS };
+const char* kKindNames[K_NKINDS] = {"input_transform", "spmm_fwd",      "output_transform", "grad_z",
+                                    "dw_digits",       "dw_gemm_i8",    "dw_reduce",        "spmm_bwd_data",
+                                    "input_grad",      "dense_fwd_tc",  "dense_dv_tc",      "sgd",
+                                    "misc"};
 
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
+};
+
+// One exponent segment of the batch (images [n0, n1), digit columns [col0, col0 + ncols_pad)):
+// the exact dW_F digits of its rows share one exponent per (slice, row) (wino_xdw.cuh).
+struct DwSeg {
+    int n0, n1;
+    int64_t col0, ncols_pad;
 };
 
 }  // namespace
@@ -158,7 +164,8 @@ struct wino_plan {
     int C = 0, K = 0, H = 0, W = 0, pad = 0, m = 0, r = 0, p = 0, P2 = 0;
     wino_geometry g{};
     wino::Coefs cf{};
-    wino::CoefsD cfd{};  // the same transform in the reference's doubles (precise dW mode)
+    wino::CoefsD cfd{};              // the transform in the reference's doubles (exact dW_F digits)
+    wino::xdw::Norms nrm_v{}, nrm_z{};  // ‖B_i‖₁‖B_j‖₁ and ‖A_i‖₁‖A_j‖₁ per slice: digit exponent bounds
     bool has_weights = false, dense = false;
     bool builtin = false;  // coefficients equal a built-in set: compile-time-constant kernels
     int64_t nnz = 0;
@@ -186,14 +193,8 @@ struct wino_plan {
     size_t cap_sumsq_part = 0;
     unsigned long long* d_nonfinite = nullptr;
     std::vector<int> h_rowptr, h_colptr;  // kept for launch partitioning
-    int sddmm_rows = 0, sddmm_r = 0, sddmm_stages = 1, sddmm_maxb = 8;
-    int sddmm_impl = 1;               // 0 = warp/transpose kernel (also the precise mode), 1 = chunk form
-    int lane_rows = 0, lane_tw = 0;   // chunk-form plan (0 rows: infeasible)
-    int64_t sddmm_max_nb = 0;
-    double* d_partial = nullptr;
-    size_t partial_cap = 0;
-    // dense plan (density 1): full CSR (dW via the exact SDDMM, scattered to K×C×p×q) plus the
-    // tcgen05 operands: W and Wᵀ split into tf32 hi/lo, [36][K][C] and [36][C][K]
+    // tcgen05 contraction operands (dense plan, or a sparse plan with the tensor-core contraction):
+    // W and Wᵀ split into tf32 hi/lo, [36][K][C] and [36][C][K]
     float* d_wdense = nullptr;
     float* d_wh = nullptr;
     float* d_wl = nullptr;
@@ -201,24 +202,19 @@ struct wino_plan {
     float* d_wtl = nullptr;
     CUtensorMap map_wh{}, map_wl{}, map_wth{}, map_wtl{};
     bool tc_ready = false;
-    bool tc_fast = false;  // dense=3: single TMEM accumulation chain (faster, ~1e-6 error)
-    int dw_mode = 0;       // sparse plan: 0 = masked SDDMM, 1 = tensor-core GEMM + mask gather, 2 = precise,
-                           // 3 = int8 tensor cores, exact products (wino_ozaki.cuh)
-    int contraction = 0;   // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
-    int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc + tc dW when dense enough)
+    int contraction = 0;       // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
+    int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc when dense enough)
     int auto_permille = 80;    // auto: tensor cores at density >= this / 1000 (measured crossover 5-10%)
     int64_t* d_slice_off = nullptr;
-    float* d_dwc = nullptr;
-    size_t dwc_cap = 0;
-    uint8_t* d_oz = nullptr;  // int8 dW: digit tensors, block exponents, the dense K×C product
-    size_t oz_cap = 0;
+    double* d_xpart = nullptr;  // exact dW_F: scaled fp64 products per accumulation chunk [chunk][P2][K][C]
+    size_t xpart_cap = 0;
     // scratch
     float* d_z = nullptr;
     size_t z_cap = 0;
     float* d_dv = nullptr;
     size_t dv_cap = 0;
     double* d_scalar = nullptr;
-    cudaStream_t side = nullptr;  // wino_backward: dW runs here, concurrent with dĨ_F -> dI
+    cudaStream_t side = nullptr;  // dW_F chain (greatest priority)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t side2 = nullptr;  // wino_forward_backward: the dO -> dZ -> dĨ_F -> dI chain
     cudaEvent_t ev_v = nullptr, ev_dz = nullptr, ev_join2 = nullptr;
@@ -237,14 +233,20 @@ struct wino_cache {
     int n_max = 0;
     int n = 0;
     int64_t NTs = 0;
-    float* V = nullptr;
-    float* DZ = nullptr;
-    int dw_chunks = 0;      // SDDMM chunks whose dW partials backward_range already computed
-    float* Vlo = nullptr;   // precise dW mode: fp32 residuals of Ĩ_F and dZ
-    float* DZlo = nullptr;
-    float* Vt = nullptr;    // tensor-core plans: tf32 lo halves of Ĩ_F and dZ (V / DZ hold the hi
-    float* DZt = nullptr;   // halves) when the producers split the operands (tf32_presplit)
-    bool v_split = false, dz_split = false;
+    float* V = nullptr;   // Ĩ_F [P2][C][NTs] fp32 (the forward's operand, bitwise the reference's f32)
+    float* DZ = nullptr;  // dZ  [P2][K][NTs] fp32
+    // exact dW_F operands (wino_xdw.cuh): digit planes of the f64 Ĩ_F and dZ, per-segment row
+    // maxima of |I| and |dO| (from K1 / K4) and the digit exponents
+    int8_t* dig_v = nullptr;
+    int8_t* dig_z = nullptr;
+    int64_t NTd = 0;  // digit row stride (capacity in columns)
+    unsigned* amax_v = nullptr;
+    unsigned* amax_z = nullptr;
+    int* e_v = nullptr;
+    int* e_z = nullptr;
+    int seg_cap = 0;
+    std::vector<DwSeg> segs;  // the batch's exponent segments in column order (set by the forward)
+    int z_segs = 0;           // segments whose dZ digits exist (set by the backward)
     bool has_fwd = false;
     bool has_grad_z = false;
 };
@@ -362,7 +364,6 @@ int ensure(float** buf, size_t* cap, size_t need) {
 // SpMM lane width: R floats per lane (chunk TW = 32R), the widest whose staged chunk
 // ncols×TW×4 B fits 200 KB (LDS.128 sustains the most shared-memory bytes per clock).
 int spmm_r(int ncols) {
-    if (const char* env = std::getenv("WINO_SPMM_R")) return std::atoi(env);
     const int64_t budget = 200 * 1024;  // the CSR segment shrinks with the row group to fit
     if ((int64_t)ncols * 128 * 4 <= budget) return 4;
     if ((int64_t)ncols * 64 * 4 <= budget) return 2;
@@ -392,7 +393,6 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
     // enough blocks to fill the GPU once; beyond that every extra row group re-stages the X chunk
     const int64_t target = (int64_t)p->sm_count * 9 / 10;
     int groups = (int)std::max<int64_t>(1, std::min<int64_t>((target + base - 1) / base, nrows / 16));
-    if (const char* e = std::getenv("WINO_SPMM_GROUPS")) groups = std::max(1, std::atoi(e));
     // prefer the staged CSR segment (measured faster than L1 reads, c2/c3), adding row groups
     // until it fits; only a segment that never fits falls back to reading it through L1
     int rpb = 0;
@@ -403,12 +403,12 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
         if ((int)(xbytes + seg) <= p->max_smem || rpb <= 16) break;
     }
     groups = (nrows + rpb - 1) / rpb;
-    const bool staged = (int)(xbytes + seg) <= p->max_smem && !std::getenv("WINO_SPMM_UNSTAGED");
+    const bool staged = (int)(xbytes + seg) <= p->max_smem;
     const size_t smem = staged ? xbytes + seg : xbytes;
     if ((int)smem > p->max_smem)
         return set_err(WINO_CAPABILITY_ERROR, "spmm: staged chunk exceeds shared memory");
     Launch L(p, st, kind);
-    const int threads = std::getenv("WINO_SPMM_THREADS") ? std::atoi(std::getenv("WINO_SPMM_THREADS")) : 1024;
+    constexpr int threads = 1024;
     const dim3 grid(chunks, groups, p->P2);
     if (staged) {
         set_smem_attr(wino::spmm_kernel<R, true>, (int)smem);
@@ -425,39 +425,10 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
 // X, Y may point at column `a` of their rows (a column range of the batch): NT = valid columns
 // of the range, NTs = the row stride, NTr = columns the range owns (≥ NT on the batch's last range,
 // which also owns the zero padding).  The whole batch: NTr = NTs.
-// the SpMM with X in tensor memory (wino_spmm_tmem.cuh): 16 rows per warp when that still fills
-// the GPU, else 8
-int launch_spmm_tmem(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
-                     const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NTs,
-                     int64_t NTr) {
-    namespace ws = wino::st;
-    const int chunks = (int)((NTr + ws::TW - 1) / ws::TW);
-    const int64_t base = (int64_t)chunks * p->P2;
-    const bool big = base * ((nrows + 63) / 64) >= p->sm_count;
-    const int rpb = big ? 64 : 32;
-    const size_t smem = (size_t)max_segment(hptr, p->P2, nrows, rpb) * sizeof(int2) + 16;
-    if ((int)smem > p->max_smem) return set_err(WINO_CAPABILITY_ERROR, "spmm (tmem): CSR segment exceeds shared memory");
-    Launch L(p, st, kind);
-    const dim3 grid((unsigned)((nrows + rpb - 1) / rpb), (unsigned)chunks, (unsigned)p->P2);
-    if (big) {
-        set_smem_attr(ws::spmm_tmem_kernel<16>, (int)smem);
-        ws::spmm_tmem_kernel<16><<<grid, ws::THREADS, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs,
-                                                                 (int)NTr, -0.0f);
-    } else {
-        set_smem_attr(ws::spmm_tmem_kernel<8>, (int)smem);
-        ws::spmm_tmem_kernel<8><<<grid, ws::THREADS, smem, st>>>(rowptr, cv, X, Y, nrows, ncols, (int)NTs,
-                                                                (int)NTr, -0.0f);
-    }
-    return L.done();
-}
-
 int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs, int64_t NTr = -1) {
     if (NTr < 0) NTr = NTs;
-    // read on every launch (not cached): tests switch it per case
-    const bool tmem = std::getenv("WINO_SPMM_TMEM") && std::atoi(std::getenv("WINO_SPMM_TMEM")) == 1;
-    if (tmem && ncols <= 1024) return launch_spmm_tmem(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NTs, NTr);
     switch (spmm_r(ncols)) {
         case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
         case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
@@ -465,216 +436,18 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
     }
 }
 
-constexpr int kSddmmBatch = 16;    // nonzeros per warp batch
-constexpr int kSddmmWarps = 24;    // 768 threads (≤ 85 registers: no spills at R=4)
-
-int64_t max_group_nnz(const wino_plan* p, int rows) {
-    int64_t nb = 0;
-    for (int s = 0; s < p->P2; ++s)
-        for (int r0 = 0; r0 < p->K; r0 += rows) {
-            const int r1 = std::min(p->K, r0 + rows);
-            nb = std::max<int64_t>(nb, p->h_rowptr[s * (p->K + 1) + r1] - p->h_rowptr[s * (p->K + 1) + r0]);
-        }
-    return nb;
-}
-
-// SDDMM variant + partition.  Preferred: R=4 (128-wide chunks) single-stage; otherwise R=2
-// with a two-stage cp.async pipeline.  Row group: the largest whose staged chunk fits and
-// whose nonzeros fit the per-warp register batches (MAXB ≤ 8, else 16).
-void plan_sddmm(wino_plan* p) {
-    const int K = p->K;
-    const int64_t budget = std::min(p->max_smem, 210 * 1024);
-    struct Opt { int r, stages; };
-    const char* renv = std::getenv("WINO_SDDMM_R");
-    for (Opt o : {Opt{4, 1}, Opt{2, 2}, Opt{2, 1}, Opt{1, 2}}) {
-        if (renv && std::atoi(renv) != o.r) continue;
-        if (o.r == 2 && o.stages == 1 && p->dw_mode != 2) continue;  // precise mode only (R=1 LO spills)
-        const int64_t per_row = (int64_t)o.stages * 32 * o.r * 4 * (p->dw_mode == 2 ? 2 : 1);
-        const int64_t cap_rows = budget / per_row - p->C;
-        if (cap_rows < 8) continue;
-        const char* env = std::getenv("WINO_SDDMM_MAXB");
-        const int first = env ? std::atoi(env) : 4;
-        for (int lim : {first, 8, 16}) {
-            int rows_cap = (int)std::min<int64_t>(round_up(K, 8), cap_rows / 8 * 8);
-            if (const char* e = std::getenv("WINO_SDDMM_ROWS")) rows_cap = std::min(rows_cap, std::max(8, std::atoi(e)));
-            for (int rows = rows_cap; rows >= 8; rows -= 8) {
-                const int64_t nb = max_group_nnz(p, rows);
-                if (nb <= (int64_t)kSddmmWarps * kSddmmBatch * lim) {
-                    p->sddmm_r = o.r;
-                    p->sddmm_stages = o.stages;
-                    p->sddmm_rows = rows;
-                    p->sddmm_max_nb = nb;
-                    const int64_t per_warp = (nb + kSddmmWarps * kSddmmBatch - 1) / (kSddmmWarps * kSddmmBatch);
-                    p->sddmm_maxb = per_warp <= 4 ? 4 : per_warp <= 8 ? 8 : 16;
-                    return;
-                }
-            }
-        }
-    }
-    p->sddmm_r = 0;  // no feasible variant: launch reports CAPABILITY
-}
-
-void plan_sddmm_chunk(wino_plan* p);
-void plan_sddmm_all(wino_plan* p) {
-    plan_sddmm(p);
-    plan_sddmm_chunk(p);
-    p->sddmm_impl = p->lane_rows > 0 ? 1 : 0;
-    if (const char* e = std::getenv("WINO_SDDMM_IMPL")) p->sddmm_impl = (std::atoi(e) == 1 && p->lane_rows > 0) ? 1 : 0;
-}
-
-constexpr int kChunkThreads = 1024;
-
-// Chunk-form SDDMM plan: TW = 128 when Ĩ_F(:, chunk) plus a useful row group fits, else 64; the
-// row group is as large as shared memory allows (fewest re-stagings of the Ĩ_F chunk).
-void plan_sddmm_chunk(wino_plan* p) {
-    p->lane_rows = 0;
-    const int64_t budget = std::min(p->max_smem, 220 * 1024);
-    static const int tw_env = std::getenv("WINO_SDDMM_TW") ? std::atoi(std::getenv("WINO_SDDMM_TW")) : 0;
-    for (int tw : {128, 64}) {
-        if (tw_env && tw != tw_env) continue;
-        const int64_t cap_rows = budget / (tw * 4) - p->C;
-        if (cap_rows < 8) continue;
-        const int64_t need = round_up(p->K, 8);
-        int rows = (int)std::min<int64_t>(need, cap_rows / 8 * 8);
-        // balance the groups: same number of groups, rows spread evenly
-        const int groups = (p->K + rows - 1) / rows;
-        rows = (int)round_up((p->K + groups - 1) / groups, 8);
-        if (const char* e = std::getenv("WINO_SDDMM_ROWS")) rows = std::max(8, std::min(rows, std::atoi(e)));
-        p->lane_rows = rows;
-        p->lane_tw = tw;
-        return;
-    }
-}
-
-template <int TW>
-void launch_sddmm_chunk_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
-                          const float* V, float* dW, double* partial, int NTs, int z0 = 0) {
-    set_smem_attr(wino::sddmm_chunk_kernel<TW, kChunkThreads>, (int)smem);
-    wino::sddmm_chunk_kernel<TW, kChunkThreads><<<grid, kChunkThreads, smem, st>>>(
-        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, dW, partial, p->nnz, p->K, p->C, NTs, p->lane_rows, z0);
-}
-
-template <int R, int MAXB, int STAGES, bool LO>
-void launch_sddmm_v(dim3 grid, size_t smem, cudaStream_t st, const wino_plan* p, const float* DZ,
-                    const float* V, const float* DZlo, const float* Vlo, float* dW, double* partial, int NT,
-                    int NTs, int tps) {
-    constexpr int TH = kSddmmWarps * 32;
-    static_assert(TH <= 1024, "block too large");
-    set_smem_attr(wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH, LO>, (int)smem);
-    wino::sddmm_kernel<R, MAXB, STAGES, kSddmmBatch, TH, LO><<<grid, TH, smem, st>>>(
-        p->d_rowptr, p->d_colidx, p->d_rowof, DZ, V, DZlo, Vlo, dW, partial, p->nnz, p->K, p->C, NT, NTs,
-        p->sddmm_rows, tps);
-}
-
-double* ensure_partial(wino_plan* p, size_t need, int* rc) {
-    *rc = WINO_OK;
-    if (p->partial_cap < need) {
-        if (p->d_partial) cudaFree(p->d_partial);
-        p->d_partial = nullptr;
-        p->partial_cap = 0;
-        const cudaError_t e = cudaMalloc(&p->d_partial, need * sizeof(double));
-        if (e != cudaSuccess) {
-            *rc = set_err(WINO_CUDA_ERROR, std::string("sddmm partials: ") + cudaGetErrorString(e));
-            return nullptr;
-        }
-        p->partial_cap = need;
-    }
-    return p->d_partial;
-}
-
-// chunks [z0, z1) of the batch (default: all) -> fp64 partials; finish = sum them into dW
-int launch_sddmm_chunk(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
-                       int64_t NTs, int z0 = 0, int z1 = -1, bool finish = true) {
-    const int TW = p->lane_tw;
-    const size_t smem = (size_t)(p->C + p->lane_rows) * TW * 4;
-    const int groups = (p->K + p->lane_rows - 1) / p->lane_rows;
-    const int chunks = (int)((NT + TW - 1) / TW);
-    if (z1 < 0) z1 = chunks;
-    int rc = WINO_OK;
-    double* partial = chunks > 1 ? ensure_partial(p, (size_t)chunks * p->nnz, &rc) : nullptr;
-    if (rc) return rc;
-    if (z1 > z0) {
-        const dim3 grid(groups, p->P2, z1 - z0);
-        Launch L(p, st, K_SDDMM);
-        if (TW == 128)
-            launch_sddmm_chunk_v<128>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs, z0);
-        else
-            launch_sddmm_chunk_v<64>(grid, smem, st, p, DZ, V, dW, partial, (int)NTs, z0);
-        if ((rc = L.done())) return rc;
-    }
-    if (chunks > 1 && finish) {
-        Launch L(p, st, K_SDDMM);
-        wino::split_sum_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(partial, dW, p->nnz, chunks);
-        return L.done();
-    }
-    return WINO_OK;
-}
-
-int launch_sddmm(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
-                 int64_t NTs, const float* DZlo = nullptr, const float* Vlo = nullptr) {
-    if (p->nnz == 0) return WINO_OK;
-    const bool lo = Vlo != nullptr;
-    if (lo != (p->dw_mode == 2)) return set_err(WINO_CONSISTENCY_ERROR, "sddmm: plan/precision mismatch");
-    if (p->sddmm_impl == 1 && !lo) return launch_sddmm_chunk(p, st, DZ, V, dW, NT, NTs);
-    if (p->sddmm_r == 0) return set_err(WINO_CAPABILITY_ERROR, "sddmm: no variant fits this layer");
-    const int R = p->sddmm_r, TW = 32 * R;
-    const size_t smem = (size_t)p->sddmm_stages * (p->C + p->sddmm_rows) * TW * 4 * (lo ? 2 : 1);
-    const int groups = (p->K + p->sddmm_rows - 1) / p->sddmm_rows;
-    const int chunks = (int)((NT + TW - 1) / TW);
-    const int64_t base = (int64_t)groups * p->P2;
-    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((3LL * p->sm_count + base - 1) / base, chunks / 2));
-    if (const char* e = std::getenv("WINO_SDDMM_SPLITS")) splits = std::max(1, std::min(chunks, std::atoi(e)));
-    const int tps = ((chunks + splits - 1) / splits) * TW;
-    splits = (int)((NT + tps - 1) / tps);
-    double* partial = nullptr;
-    if (splits > 1) {
-        const size_t need = (size_t)splits * p->nnz;
-        if (p->partial_cap < need) {
-            if (p->d_partial) cudaFree(p->d_partial);
-            p->d_partial = nullptr;
-            p->partial_cap = 0;
-            CUDA_TRY(cudaMalloc(&p->d_partial, need * sizeof(double)));
-            p->partial_cap = need;
-        }
-        partial = p->d_partial;
-    }
-    const dim3 grid(groups, p->P2, splits);
-    {
-        Launch L(p, st, K_SDDMM);
-#define SDDMM_CASE(RR, MB, SS)                                                                   \
-    if (p->sddmm_r == RR && p->sddmm_maxb == MB && p->sddmm_stages == SS) {                      \
-        if (lo)                                                                                  \
-            launch_sddmm_v<RR, MB, SS, true>(grid, smem, st, p, DZ, V, DZlo, Vlo, dW, partial, (int)NT, \
-                                             (int)NTs, tps);                                     \
-        else                                                                                     \
-            launch_sddmm_v<RR, MB, SS, false>(grid, smem, st, p, DZ, V, nullptr, nullptr, dW, partial,  \
-                                              (int)NT, (int)NTs, tps);                           \
-    }
-        SDDMM_CASE(4, 4, 1) SDDMM_CASE(4, 8, 1) SDDMM_CASE(4, 16, 1)
-        SDDMM_CASE(2, 4, 2) SDDMM_CASE(2, 8, 2) SDDMM_CASE(2, 16, 2)
-        SDDMM_CASE(2, 4, 1) SDDMM_CASE(2, 8, 1) SDDMM_CASE(2, 16, 1)
-        SDDMM_CASE(1, 4, 2) SDDMM_CASE(1, 8, 2) SDDMM_CASE(1, 16, 2)
-#undef SDDMM_CASE
-        int rc = L.done();
-        if (rc) return rc;
-    }
-    if (splits > 1) {
-        Launch L(p, st, K_SDDMM);
-        wino::split_sum_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(partial, dW, p->nnz, splits);
-        return L.done();
-    }
-    return WINO_OK;
-}
-
+// stage 0: K1 (Ĩ_F; with amax also the per-(segment, channel) max|I| of the exact dW_F digits);
+// stage 1: K3 (O)
 template <int M, int P, class CF>
-int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, wino_cache* c,
-                   float* V, float* Z, int n, int64_t NT, int64_t NTs, int flags, int stage, int64_t NTr) {
+int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, float* V, float* Z, int n,
+                   int64_t NT, int64_t NTs, int flags, int stage, int64_t NTr, unsigned* amax = nullptr,
+                   int seg_imgs = 1) {
     const wino_geometry& g = p->g;
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
         wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTr, 256, p->sm_count), 256, 0, st>>>(
-            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr,
-            (c && c->v_split && V == c->V) ? c->Vt : nullptr);
+            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr, amax,
+            seg_imgs);
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
@@ -688,48 +461,21 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, w
     return L.done();
 }
 
+// K4: dZ (+ max|dO| per (segment, k) with amax)
 template <int M, int P, class CF>
 int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
-                  int64_t NT, int64_t NTs, bool mask, int64_t NTr, float* DZt = nullptr) {
+                  int64_t NT, int64_t NTs, bool mask, int64_t NTr, unsigned* amax = nullptr, int seg_imgs = 1) {
     const wino_geometry& g = p->g;
     Launch L(p, st, K_GRADZ);
     const int grid = grid_for((int64_t)p->K * NTr, 256, p->sm_count);
     if (mask)
         wino::grad_z_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                              (int)NT, (int)NTs, (int)NTr, DZt);
+                                                              (int)NT, (int)NTs, (int)NTr, amax, seg_imgs);
     else
         wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                               (int)NT, (int)NTs, (int)NTr, DZt);
-    return L.done();
-}
-
-// precise dW mode: the fp32 residuals of Ĩ_F (after K1) and of dZ (after K4)
-template <int M, int P, class CF>
-int launch_input_lo(wino_plan* p, cudaStream_t st, const float* in, const float* V, float* Vlo, int64_t NT,
-                    int64_t NTs) {
-    const wino_geometry& g = p->g;
-    Launch L(p, st, K_INPUT);
-    wino::input_transform_lo_kernel<M, P><<<grid_for((int64_t)p->C * NTs, 256, p->sm_count), 256, 0, st>>>(
-        in, V, Vlo, p->cfd, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
-    return L.done();
-}
-
-template <int M, int P, class CF>
-int launch_grad_z_lo(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, const float* DZ,
-                     float* DZlo, int64_t NT, int64_t NTs, bool mask) {
-    const wino_geometry& g = p->g;
-    Launch L(p, st, K_GRADZ);
-    const int grid = grid_for((int64_t)p->K * NTs, 256, p->sm_count);
-    if (mask)
-        wino::grad_z_lo_kernel<M, P, true><<<grid, 256, 0, st>>>(dO, relu, DZ, DZlo, p->cfd, p->K, (int)g.h_o,
-                                                                (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT,
-                                                                (int)NTs);
-    else
-        wino::grad_z_lo_kernel<M, P, false><<<grid, 256, 0, st>>>(dO, relu, DZ, DZlo, p->cfd, p->K, (int)g.h_o,
-                                                                 (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT,
-                                                                 (int)NTs);
+                                                               (int)NT, (int)NTs, (int)NTr, amax, seg_imgs);
     return L.done();
 }
 
@@ -803,219 +549,214 @@ int refresh_tc_operands(wino_plan* p, cudaStream_t st) {
     return WINO_OK;
 }
 
-// B_PRE: B pre-split by its producer (bl = its tf32 lo half); only the warp-specialised kernel
-// takes it (tf32_presplit() guarantees that kernel is the one selected)
-template <bool A_SPLIT, bool B_MN, bool B_PRE = false>
-int launch_tc(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
-              const CUtensorMap& b, float* D, int M, int N, int Kd, int64_t ldd, int splits,
-              const CUtensorMap* bl = nullptr) {
-    const int kb_total = (Kd + wino::tc::BK - 1) / wino::tc::BK;
-    const int kb_per = (kb_total + splits - 1) / splits;
-    const int bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
-    const dim3 grid((unsigned)((N + bn - 1) / bn), (M + wino::tc::BM - 1) / wino::tc::BM, p->P2 * splits);
-    Launch L(p, st, kind);
-    if (p->tc_fast) {
-        set_smem_attr(wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN>, wino::tc::SMEM_BYTES);
-        wino::tc::gemm_3xtf32_kernel<A_SPLIT, B_MN><<<grid, wino::tc::THREADS, wino::tc::SMEM_BYTES, st>>>(
-            ah, al, b, D, M, N, Kd, ldd, p->P2, splits, kb_per);
-    } else {
-        // k-blocks (of 32) per fresh TMEM accumulator folded into fp64: 1 = most accurate; each
-        // fold costs one fp32->fp64 conversion per output element on the XU pipe
-        static const int fold = std::getenv("WINO_TC_FOLD") ? std::atoi(std::getenv("WINO_TC_FOLD")) : 1;
-        static const bool persistent = !(std::getenv("WINO_TC_PERSISTENT") &&
-                                         std::atoi(std::getenv("WINO_TC_PERSISTENT")) == 0);
-        const int ntiles = (int)(grid.x * grid.y * grid.z);
-        auto go = [&](auto kern) {
-            set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
-            kern<<<grid, wino::tc::flush::THREADS, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd,
-                                                                                     p->P2, splits, kb_per);
-        };
-        static const int epi = std::getenv("WINO_TC_EPI") ? std::atoi(std::getenv("WINO_TC_EPI")) : 16;
-        auto go_p = [&](auto kern, int threads) {
-            set_smem_attr(kern, wino::tc::flush::SMEM_BYTES);
-            const int ctas = std::min(ntiles, p->sm_count);
-            kern<<<ctas, threads, wino::tc::flush::SMEM_BYTES, st>>>(ah, al, b, D, M, N, Kd, ldd, p->P2, splits,
-                                                                    kb_per, (int)grid.x, (int)grid.y, ntiles);
-        };
-        // Default: the warp-specialised kernel (split warps apart from drain warps, 4 TMEM
-        // accumulators, TMA-stored output) with the compensated fp32 fold (fp64 for the dW GEMM);
-        // WINO_TC_ACC=fp64 selects the fp64 fold everywhere, WINO_TC_WS=0 the round-1 persistent
-        // kernel (A/B builds).
-        static const bool ws = !(std::getenv("WINO_TC_WS") && std::atoi(std::getenv("WINO_TC_WS")) == 0);
-        // the dW GEMM (A split in shared memory too) measured faster with the fp64 fold (551 vs 584
-        // µs at c3): its two split warps, not the drain, bound it, and the fp64 fold does not spill
-        static const bool fp64_env = std::getenv("WINO_TC_ACC") && std::string(std::getenv("WINO_TC_ACC")) == "fp64";
-        static const bool dw_kahan = std::getenv("WINO_TC_DW_ACC") && std::string(std::getenv("WINO_TC_DW_ACC")) == "kahan";
-        const bool fp64_fold = fp64_env || (A_SPLIT && !dw_kahan);
-        // drain warps: 8 (64 columns each, 4 KB SW128 output boxes; measured 4% faster at c3 than
-        // WINO_TC_DW=16 with 32 columns and 2 KB SW64 boxes)
-        static const int dw_env = std::getenv("WINO_TC_DW") ? std::atoi(std::getenv("WINO_TC_DW")) : 8;
-        // the dW GEMM (A and B split in shared memory, fp64 fold) is split-bound with 2 split warps:
-        // it runs 4 split warps next to 16 drain warps of 32 columns (80 registers per thread;
-        // c3: 581 -> 521 µs; 6 split warps 526 µs; WINO_TC_DWGEMM_SW=2 restores the 2 + 8 layout)
-        static const int dwgemm_sw = std::getenv("WINO_TC_DWGEMM_SW") ? std::atoi(std::getenv("WINO_TC_DWGEMM_SW")) : 4;
-        const bool wide_split = A_SPLIT && !B_PRE && fp64_fold && dwgemm_sw != 2;
-        const int dw = wide_split ? 16 : dw_env;
-        CUtensorMap md;
-        const bool ws_ok = ws && persistent && fold == 1 && (ldd & 3) == 0 &&
-                           wino::make_map_3d_sw(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2 * splits,
-                                                (uint64_t)ldd * 4, (uint64_t)M * ldd * 4, dw == 8 ? 32 : 16, 32,
-                                                dw == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-        // 2 split warps (4 would cap registers at 128/thread and spill the drain's 64 Kahan pairs);
-        // none when both operands arrive pre-split
-        constexpr int SW = (!A_SPLIT && B_PRE) ? 0 : 2;
-        auto go_ws = [&](auto kern, int drain_warps) {
-            set_smem_attr(kern, wino::tc::flush::WS_SMEM_BYTES);
-            const int ctas = std::min(ntiles, p->sm_count);
-            kern<<<ctas, 64 + 32 * (SW + drain_warps), wino::tc::flush::WS_SMEM_BYTES, st>>>(
-                ah, al, b, md, bl ? *bl : b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y,
-                ntiles);
-        };
-        if (B_PRE && !(ws_ok && dw == 8))
-            return set_err(WINO_CAPABILITY_ERROR, "pre-split operands need the warp-specialised tcgen05 kernel");
-        auto go_ws_sw = [&](auto kern, int split_warps, int drain_warps) {
-            set_smem_attr(kern, wino::tc::flush::WS_SMEM_BYTES);
-            const int ctas = std::min(ntiles, p->sm_count);
-            kern<<<ctas, 64 + 32 * (split_warps + drain_warps), wino::tc::flush::WS_SMEM_BYTES, st>>>(
-                ah, al, b, md, bl ? *bl : b, D, M, N, Kd, ldd, p->P2, splits, kb_per, (int)grid.x, (int)grid.y,
-                ntiles);
-        };
-        if constexpr (A_SPLIT && !B_PRE) {
-            if (ws_ok && wide_split && dwgemm_sw == 4) {
-                go_ws_sw(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, 4, 16, false, 4>, 4, 16);
-                return L.done();
-            }
-            if (ws_ok && wide_split) {
-                go_ws_sw(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, 6, 16, false, 4>, 6, 16);
-                return L.done();
-            }
-        }
-        if (ws_ok && dw == 8 && !fp64_fold)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, true, 4, B_PRE>, 8);
-        else if (ws_ok && dw == 8)
-            go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 8, false, 4, B_PRE>, 8);
-        else if constexpr (!B_PRE) {
-            if (ws_ok && !fp64_fold)
-                go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, true, 4>, 16);
-            else if (ws_ok)
-                go_ws(wino::tc::gemm_3xtf32_ws_kernel<A_SPLIT, B_MN, SW, 16, false, 4>, 16);
-            else if (persistent && fold == 1 && epi == 8)
-                go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 8>, 64 + 32 * 8);
-            else if (persistent && fold == 1)
-                go_p(wino::tc::gemm_3xtf32_flush_persistent_kernel<A_SPLIT, B_MN, 1, 16>, 64 + 32 * 16);
-            else if (fold == 2)
-                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 2>);
-            else if (fold == 4)
-                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 4>);
-            else
-                go(wino::tc::gemm_3xtf32_flush_kernel<A_SPLIT, B_MN, 1>);
-        }
-    }
-    return L.done();
-}
-
-// D[s] = W-operand[s] · B[s] on the tensor cores; B = [P2][Kd][NTs] activations (MN-major).
+// D[s] = W-operand[s] · B[s] on the tensor cores (forward: W_F·Ĩ_F; backward data: W_Fᵀ·dZ), B =
+// [P2][Kd][NTs] activations (MN-major): the warp-specialised 3xTF32 tcgen05 kernel
+// (wino_dense_tc.cuh; 2 split warps, 8 drain warps with a compensated fp32 fold, TMA-stored output).
 int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& ah, const CUtensorMap& al,
-                   const float* B, float* D, int M, int Kd, int64_t NTs, const float* Blo = nullptr) {
-    CUtensorMap mb, mbl;
+                   const float* B, float* D, int M, int Kd, int64_t NTs) {
+    namespace tc = wino::tc;
+    CUtensorMap mb, md;
+    const int N = (int)NTs;
     if (!wino::make_map_3d(&mb, B, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true) ||
-        (Blo && !wino::make_map_3d(&mbl, Blo, NTs, Kd, p->P2, (uint64_t)NTs * 4, (uint64_t)Kd * NTs * 4, 32, 32, true)))
+        !wino::make_map_3d_sw(&md, D, (uint64_t)N, (uint64_t)M, (uint64_t)p->P2, (uint64_t)NTs * 4,
+                              (uint64_t)M * NTs * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the activation operand (CUresult " +
                                             std::to_string(wino::last_tmap_error()) + ")");
-    if (Blo) return launch_tc<false, true, true>(p, st, kind, ah, al, mb, D, M, (int)NTs, Kd, NTs, 1, &mbl);
-    return launch_tc<false, true>(p, st, kind, ah, al, mb, D, M, (int)NTs, Kd, NTs, 1);
-}
-
-// dW_F = dZ·Ĩ_Fᵀ on the tensor cores, split over NT, partials summed in fp64 -> K×C×p×q.
-int launch_tc_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NTs,
-                 bool masked = false, const float* DZlo = nullptr, const float* Vlo = nullptr) {
-    CUtensorMap ma, mb, mal, mbl;
-    const uint32_t bn = p->tc_fast ? wino::tc::BN : wino::tc::flush::BN;
-    const bool pre = DZlo && Vlo;  // both operands pre-split by their producers (K4, K1)
-    if (!wino::make_map_3d(&ma, DZ, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128) ||
-        !wino::make_map_3d(&mb, V, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn) ||
-        (DZlo && !wino::make_map_3d(&mal, DZlo, NTs, p->K, p->P2, (uint64_t)NTs * 4, (uint64_t)p->K * NTs * 4, 32, 128)) ||
-        (Vlo && !wino::make_map_3d(&mbl, Vlo, NTs, p->C, p->P2, (uint64_t)NTs * 4, (uint64_t)p->C * NTs * 4, 32, bn)))
-        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for dZ / Ĩ_F (CUresult " +
-                                            std::to_string(wino::last_tmap_error()) + ")");
-    const int tiles = ((p->C + (int)bn - 1) / (int)bn) * ((p->K + wino::tc::BM - 1) / wino::tc::BM) * p->P2;
-    const int kb_total = (int)((NTs + wino::tc::BK - 1) / wino::tc::BK);
-    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * p->sm_count + tiles - 1) / tiles, kb_total / 4));
-    if (const char* e = std::getenv("WINO_DW_SPLITS")) splits = std::max(1, std::atoi(e));
-    const size_t need = (size_t)splits * p->P2 * p->K * p->C;
-    float* part = nullptr;
-    int rc = ensure(&p->d_dwc, &p->dwc_cap, need);
-    if (rc) return rc;
-    part = p->d_dwc;
-    const int kind = masked ? K_SDDMM : K_DENSE_DW;
-    if (pre)
-        rc = launch_tc<false, false, true>(p, st, kind, ma, mal, mb, part, p->K, p->C, (int)NTs, p->C, splits, &mbl);
-    else if (Vlo)  // only Ĩ_F pre-split (dZ from a range backward): A still split in shared memory
-        rc = launch_tc<true, false, true>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits, &mbl);
-    else if (DZlo)
-        rc = launch_tc<false, false>(p, st, kind, ma, mal, mb, part, p->K, p->C, (int)NTs, p->C, splits);
-    else
-        rc = launch_tc<true, false>(p, st, kind, ma, ma, mb, part, p->K, p->C, (int)NTs, p->C, splits);
-    if (rc) return rc;
+    const int kb = (Kd + tc::BK - 1) / tc::BK;
+    const int tiles_n = (N + tc::flush::BN - 1) / tc::flush::BN, tiles_m = (M + tc::BM - 1) / tc::BM;
+    const int ntiles = tiles_n * tiles_m * p->P2;
+    auto kern = tc::gemm_3xtf32_ws_kernel<false, true, 2, 8, true, 4>;
+    set_smem_attr(kern, tc::flush::WS_SMEM_BYTES);
     Launch L(p, st, kind);
-    if (masked)
-        wino::tc::reduce_dw_masked_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(
-            part, dW, p->d_rowof, p->d_colidx, p->d_slice_off, p->K, p->C, p->P2, splits, p->nnz);
-    else
-        wino::tc::reduce_dw_kernel<<<grid_for((int64_t)p->P2 * p->K * p->C, 256, p->sm_count), 256, 0, st>>>(
-            part, dW, p->K, p->C, p->P2, splits);
+    kern<<<std::min(ntiles, p->sm_count), 64 + 32 * (2 + 8), tc::flush::WS_SMEM_BYTES, st>>>(
+        ah, al, mb, md, mb, D, M, N, Kd, NTs, p->P2, 1, kb, tiles_n, tiles_m, ntiles);
     return L.done();
 }
 
-// dW_F on the int8 tensor cores (wino_ozaki.cuh): digit split of dZ and Ĩ_F, the exact-product
-// GEMM per Winograd coordinate into a dense [P2][K][C] buffer, then the surviving entries
-// gathered in CSR order.
-int launch_ozaki_dw(wino_plan* p, cudaStream_t st, const float* DZ, const float* V, float* dW, int64_t NT,
-                    int64_t NTs) {
-    namespace oz = wino::oz;
-    const int64_t NTp = (NT + oz::KB - 1) / oz::KB * oz::KB, nkb = NTp / oz::KB;
-    const int64_t P2 = p->P2, K = p->K, C = p->C;
-    const size_t dig_a = (size_t)oz::DIG * P2 * K * NTp, dig_b = (size_t)oz::DIG * P2 * C * NTp;
-    const size_t ex_a = (size_t)P2 * K * nkb * 4, ex_b = (size_t)P2 * C * nkb * 4;
-    const size_t dense = (size_t)P2 * K * C * 4;
-    auto up = [](size_t x) { return (x + 1023) / 1024 * 1024; };
-    const size_t need = up(dig_a) + up(dig_b) + up(ex_a) + up(ex_b) + up(dense);
-    if (p->oz_cap < need) {
-        if (p->d_oz) cudaFree(p->d_oz);
-        p->d_oz = nullptr;
-        p->oz_cap = 0;
-        CUDA_TRY(cudaMalloc(&p->d_oz, need));
-        p->oz_cap = need;
+// ---- exact dW_F (wino_xdw.cuh): segments, digits, the int8 GEMM, the masked reduce ----
+
+// images per exponent segment: one segment's columns fit one exact accumulation chunk
+int seg_images(const wino_plan* p) {
+    return (int)std::max<int64_t>(1, wino::xdw::kMaxChunkCols / std::max<int64_t>(1, p->g.t));
+}
+
+// digit buffers for `cols` columns and `nseg` segments (contents are lost when they grow)
+int ensure_digits(wino_plan* p, wino_cache* c, int64_t cols, int nseg) {
+    namespace x = wino::xdw;
+    cols = round_up(std::max<int64_t>(cols, x::KS), x::KS);
+    if (c->NTd < cols) {
+        if (c->dig_v) cudaFree(c->dig_v);
+        if (c->dig_z) cudaFree(c->dig_z);
+        c->dig_v = c->dig_z = nullptr;
+        c->NTd = 0;
+        CUDA_TRY(cudaMalloc(&c->dig_v, (size_t)x::DIG * p->P2 * p->C * cols));
+        CUDA_TRY(cudaMalloc(&c->dig_z, (size_t)x::DIG * p->P2 * p->K * cols));
+        c->NTd = cols;
     }
-    int8_t* da = reinterpret_cast<int8_t*>(p->d_oz);
-    int8_t* db = da + up(dig_a);
-    int* ea = reinterpret_cast<int*>(db + up(dig_b));
-    int* eb = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ea) + up(ex_a));
-    float* dd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(eb) + up(ex_b));
-    CUtensorMap ma, mb;
-    if (!wino::make_map_3d_sw(&ma, da, NTp, K, oz::DIG * P2, NTp, K * NTp, oz::KB, oz::BM,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT8) ||
-        !wino::make_map_3d_sw(&mb, db, NTp, C, oz::DIG * P2, NTp, C * NTp, oz::KB, oz::BN,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT8))
-        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the int8 digit tensors (CUresult " +
-                                            std::to_string(wino::last_tmap_error()) + ")");
-    Launch L(p, st, K_SDDMM);
-    oz::slice_kernel<<<grid_for(P2 * K * nkb * 32, 256, p->sm_count), 256, 0, st>>>(DZ, da, ea, (int)P2, (int)K,
-                                                                                   (int)NT, (int)NTs, (int)NTp);
-    oz::slice_kernel<<<grid_for(P2 * C * nkb * 32, 256, p->sm_count), 256, 0, st>>>(V, db, eb, (int)P2, (int)C,
-                                                                                   (int)NT, (int)NTs, (int)NTp);
-    const int tiles_n = (int)((C + oz::BN - 1) / oz::BN), tiles_m = (int)((K + oz::BM - 1) / oz::BM);
-    const int ntiles = tiles_n * tiles_m * (int)P2;
-    set_smem_attr(oz::gemm_kernel, oz::SMEM_BYTES);
-    oz::gemm_kernel<<<std::min(ntiles, p->sm_count), oz::THREADS, oz::SMEM_BYTES, st>>>(
-        ma, mb, ea, eb, dd, (int)P2, (int)K, (int)C, (int)nkb, tiles_n, tiles_m, ntiles);
-    const int per_slice = (int)std::max<int64_t>(1, std::min<int64_t>(64, p->nnz / P2 / 1024 + 1));
-    oz::gather_kernel<<<dim3(per_slice, (unsigned)P2), 256, 0, st>>>(dd, dW, p->d_rowof, p->d_colidx,
-                                                                    p->d_slice_off, p->K, p->C, p->P2, p->nnz);
-    p->launches += 3;  // Launch L counts one
-    return L.done();
+    if (c->seg_cap < nseg) {
+        for (void* q : {(void*)c->amax_v, (void*)c->amax_z, (void*)c->e_v, (void*)c->e_z})
+            if (q) cudaFree(q);
+        c->amax_v = c->amax_z = nullptr;
+        c->e_v = c->e_z = nullptr;
+        c->seg_cap = 0;
+        CUDA_TRY(cudaMalloc(&c->amax_v, (size_t)nseg * p->C * sizeof(unsigned)));
+        CUDA_TRY(cudaMalloc(&c->amax_z, (size_t)nseg * p->K * sizeof(unsigned)));
+        CUDA_TRY(cudaMalloc(&c->e_v, (size_t)nseg * p->P2 * p->C * sizeof(int)));
+        CUDA_TRY(cudaMalloc(&c->e_z, (size_t)nseg * p->P2 * p->K * sizeof(int)));
+        c->seg_cap = nseg;
+    }
+    return WINO_OK;
 }
 
+// Append the segments of images [n0, n1) (after the ones already planned, which must end at n0).
+// full: the whole batch in one call (exact column capacity); otherwise a range of a pipelined
+// batch (capacity for the worst case, so later ranges never reallocate).
+int plan_segments(wino_plan* p, wino_cache* c, int n0, int n1, bool full) {
+    namespace x = wino::xdw;
+    if (n0 == 0) {
+        c->segs.clear();
+        c->z_segs = 0;
+    }
+    if ((c->segs.empty() ? 0 : c->segs.back().n1) != n0)
+        return set_err(WINO_CONSISTENCY_ERROR, "image ranges of a batch must be issued in order from image 0");
+    const int per = seg_images(p);
+    const int64_t T = p->g.t;
+    int64_t col = c->segs.empty() ? 0 : c->segs.back().col0 + c->segs.back().ncols_pad;
+    for (int a = n0; a < n1; a += per) {
+        const int b = std::min(n1, a + per);
+        const int64_t pad = round_up((int64_t)(b - a) * T, x::KS);
+        c->segs.push_back(DwSeg{a, b, col, pad});
+        col += pad;
+    }
+    const int nseg = full ? (int)c->segs.size() : c->n_max;
+    const int64_t cols = full ? col : (int64_t)c->n_max * round_up(T, x::KS);
+    if (n0 == 0) return ensure_digits(p, c, cols, nseg);
+    if (c->NTd < col || c->seg_cap < (int)c->segs.size())
+        return set_err(WINO_CONSISTENCY_ERROR, "exact dW_F digit buffers too small for this range");
+    return WINO_OK;
+}
+
+// segments [g0, g1) of the cache covering images [n0, n1) exactly
+int find_segments(const wino_cache* c, int n0, int n1, int* g0, int* g1) {
+    int a = -1, b = -1;
+    for (int i = 0; i < (int)c->segs.size(); ++i) {
+        if (c->segs[i].n0 == n0) a = i;
+        if (c->segs[i].n1 == n1) b = i + 1;
+    }
+    if (a < 0 || b <= a)
+        return set_err(WINO_CONSISTENCY_ERROR, "backward image range [" + std::to_string(n0) + ", " +
+                                                   std::to_string(n1) + ") differs from the forward's ranges");
+    *g0 = a;
+    *g1 = b;
+    return WINO_OK;
+}
+
+// Ĩ_F digits of segments [g0, g1); `in` holds images from n_base on (amax_v filled by K1)
+template <int M, int P, class CF>
+int launch_input_digits(wino_plan* p, cudaStream_t st, const float* in, int n_base, wino_cache* c, int g0,
+                        int g1) {
+    namespace x = wino::xdw;
+    const int64_t T = p->g.t;
+    const size_t smem = (size_t)P * P * x::kTileItems * 5;
+    auto kern = x::input_digits_kernel<M, P, CF>;
+    set_smem_attr(kern, (int)std::max<size_t>(smem, 48 * 1024));
+    const int64_t plane = (int64_t)p->P2 * p->C * c->NTd;
+    for (int g = g0; g < g1; ++g) {
+        const DwSeg& sg = c->segs[g];
+        const int64_t items = (int64_t)p->C * sg.ncols_pad;
+        Launch L(p, st, K_DW_DIGITS);
+        kern<<<(unsigned)((items + x::kTileItems - 1) / x::kTileItems), x::kTileItems, smem, st>>>(
+            in + (int64_t)(sg.n0 - n_base) * p->C * p->H * p->W, c->dig_v, c->e_v + (int64_t)g * p->P2 * p->C,
+            c->amax_v + (int64_t)g * p->C, p->cfd, p->nrm_v, p->C, p->H, p->W, p->pad, (int)p->g.tiles_x, (int)T,
+            (int)((sg.n1 - sg.n0) * T), (int)sg.ncols_pad, c->NTd, plane, (int)sg.col0);
+        int rc = L.done();
+        if (rc) return rc;
+    }
+    return WINO_OK;
+}
+
+// dZ digits of segments [g0, g1); dO (and relu) hold images from n_base on (amax_z filled by K4)
+template <int M, int P, class CF>
+int launch_grad_digits(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, bool mask, int n_base,
+                       wino_cache* c, int g0, int g1) {
+    namespace x = wino::xdw;
+    const int64_t T = p->g.t, HW = p->g.h_o * p->g.w_o;
+    const size_t smem = (size_t)P * P * x::kTileItems * 5;
+    const int64_t plane = (int64_t)p->P2 * p->K * c->NTd;
+    for (int g = g0; g < g1; ++g) {
+        const DwSeg& sg = c->segs[g];
+        const int64_t items = (int64_t)p->K * sg.ncols_pad;
+        const int64_t off = (int64_t)(sg.n0 - n_base) * p->K * HW;
+        const unsigned blocks = (unsigned)((items + x::kTileItems - 1) / x::kTileItems);
+        Launch L(p, st, K_DW_DIGITS);
+        auto go = [&](auto kern) {
+            set_smem_attr(kern, (int)std::max<size_t>(smem, 48 * 1024));
+            kern<<<blocks, x::kTileItems, smem, st>>>(
+                dO + off, relu ? relu + off : nullptr, c->dig_z, c->e_z + (int64_t)g * p->P2 * p->K,
+                c->amax_z + (int64_t)g * p->K, p->cfd, p->nrm_z, p->K, (int)p->g.h_o, (int)p->g.w_o,
+                (int)p->g.tiles_x, (int)T, (int)((sg.n1 - sg.n0) * T), (int)sg.ncols_pad, c->NTd, plane,
+                (int)sg.col0);
+        };
+        if (mask) go(x::grad_digits_kernel<M, P, true, CF>);
+        else go(x::grad_digits_kernel<M, P, false, CF>);
+        int rc = L.done();
+        if (rc) return rc;
+    }
+    return WINO_OK;
+}
+
+// dW_F from the digits of every segment: the int8 GEMM per accumulation chunk, then the ordered
+// chunk sum gathered on the mask (CSR order) or into K×C×p×q (dense plan).
+int launch_xdw(wino_plan* p, cudaStream_t st, const wino_cache* c, float* grad_w) {
+    namespace x = wino::xdw;
+    x::ChunkTab ct{};
+    constexpr int64_t maxc = x::kMaxChunkCols / x::KS * x::KS;
+    for (int g = 0; g < (int)c->segs.size(); ++g)
+        for (int64_t a = 0; a < c->segs[g].ncols_pad; a += maxc) {
+            if (ct.n == x::kMaxChunks)
+                return set_err(WINO_CAPABILITY_ERROR, "exact dW_F: more than " + std::to_string(x::kMaxChunks) +
+                                                          " accumulation chunks (too many image ranges)");
+            ct.col0[ct.n] = (int)(c->segs[g].col0 + a);
+            ct.ncols[ct.n] = (int)std::min(maxc, c->segs[g].ncols_pad - a);
+            ct.seg[ct.n] = g;
+            ++ct.n;
+        }
+    if (p->nnz == 0 || ct.n == 0) return WINO_OK;
+    const int K = p->K, C = p->C, P2 = p->P2;
+    const size_t need = (size_t)ct.n * P2 * K * C;
+    if (p->xpart_cap < need) {
+        if (p->d_xpart) cudaFree(p->d_xpart);
+        p->d_xpart = nullptr;
+        p->xpart_cap = 0;
+        CUDA_TRY(cudaMalloc(&p->d_xpart, need * sizeof(double)));
+        p->xpart_cap = need;
+    }
+    CUtensorMap ma, mb;
+    if (!wino::make_map_4d_u8(&ma, c->dig_z, c->NTd, K, P2, x::DIG, x::KS, x::BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !wino::make_map_4d_u8(&mb, c->dig_v, c->NTd, C, P2, x::DIG, x::KS, x::BN, CU_TENSOR_MAP_SWIZZLE_64B))
+        return set_err(WINO_CUDA_ERROR, "cuTensorMapEncodeTiled failed for the dW_F digit tensors (CUresult " +
+                                            std::to_string(wino::last_tmap_error()) + ")");
+    const int tiles_m = (K + x::BM - 1) / x::BM, tiles_n = (C + x::BN - 1) / x::BN;
+    const int units = ct.n * P2 * tiles_m * tiles_n;
+    set_smem_attr(x::gemm_kernel, x::SMEM_BYTES);
+    {
+        Launch L(p, st, K_DW_GEMM);
+        x::gemm_kernel<<<std::min(units, p->sm_count), x::THREADS, x::SMEM_BYTES, st>>>(
+            ma, mb, ct, c->e_z, c->e_v, p->d_xpart, P2, K, C, tiles_m, tiles_n, units);
+        int rc = L.done();
+        if (rc) return rc;
+    }
+    Launch L(p, st, K_DW_REDUCE);
+    if (p->dense)
+        x::reduce_dense_kernel<<<grid_for((int64_t)P2 * K * C, 256, p->sm_count), 256, 0, st>>>(p->d_xpart, grad_w, K,
+                                                                                              C, P2, ct.n);
+    else {
+        const int per_slice = (int)std::max<int64_t>(1, std::min<int64_t>(64, p->nnz / P2 / 1024 + 1));
+        x::reduce_sparse_kernel<<<dim3(per_slice, (unsigned)P2), 256, 0, st>>>(
+            p->d_xpart, grad_w, p->d_rowof, p->d_colidx, p->d_slice_off, K, C, P2, ct.n, p->nnz);
+    }
+    return L.done();
+}
 int check_plan(const wino_plan* p) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
     if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan has no weights (call wino_set_weights*)");
@@ -1083,7 +824,6 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
-    plan_sddmm_all(p);
     if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
@@ -1202,7 +942,6 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
-    plan_sddmm_all(p);
     if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
@@ -1285,10 +1024,40 @@ int wino_plan_create(const wino_layer_desc* d, wino_plan** out) {
         return std::memcmp(p->cf.a, ta, sizeof(float) * p->p * p->m) == 0 &&
                std::memcmp(p->cf.b, tb, sizeof(float) * p->p * p->p) == 0;
     };
+    // the f64 digit kernels take the built-in doubles too: the doubles must match as well
+    auto same_d = [&](auto tag) {
+        using B = decltype(tag);
+        for (int i = 0; i < p->p * p->m; ++i)
+            if (p->cfd.a[i] != B::AD(i)) return false;
+        for (int i = 0; i < p->p * p->p; ++i)
+            if (p->cfd.b[i] != B::BD(i)) return false;
+        return true;
+    };
+    // WINO_RUNTIME_COEFS (debug): run the runtime-coefficient kernel variants
     if (!std::getenv("WINO_RUNTIME_COEFS")) {
-        if (p->m == 4) p->builtin = same(wino::BuiltinCoefs<4, 6>::a, wino::BuiltinCoefs<4, 6>::b);
-        if (p->m == 2) p->builtin = same(wino::BuiltinCoefs<2, 4>::a, wino::BuiltinCoefs<2, 4>::b);
-        if (p->m == 6) p->builtin = same(wino::BuiltinCoefs<6, 8>::a, wino::BuiltinCoefs<6, 8>::b);
+        if (p->m == 4)
+            p->builtin = same(wino::BuiltinCoefs<4, 6>::a, wino::BuiltinCoefs<4, 6>::b) &&
+                         same_d(wino::BuiltinCoefs<4, 6>{});
+        if (p->m == 2)
+            p->builtin = same(wino::BuiltinCoefs<2, 4>::a, wino::BuiltinCoefs<2, 4>::b) &&
+                         same_d(wino::BuiltinCoefs<2, 4>{});
+        if (p->m == 6)
+            p->builtin = same(wino::BuiltinCoefs<6, 8>::a, wino::BuiltinCoefs<6, 8>::b) &&
+                         same_d(wino::BuiltinCoefs<6, 8>{});
+    }
+    // exponent bounds of the exact dW_F digits: |Ĩ_F(i,j)| <= ‖B col i‖₁‖B col j‖₁·max|d|,
+    // |dZ(i,j)| <= ‖A row i‖₁‖A row j‖₁·max|dÕ| (the kernels' own sums, wino_xdw.cuh)
+    {
+        double nb[8] = {}, na[8] = {};
+        for (int i = 0; i < p->p; ++i) {
+            for (int k = 0; k < p->p; ++k) nb[i] += std::fabs(p->cfd.b[k * p->p + i]);
+            for (int y = 0; y < p->m; ++y) na[i] += std::fabs(p->cfd.a[i * p->m + y]);
+        }
+        for (int i = 0; i < p->p; ++i)
+            for (int j = 0; j < p->p; ++j) {
+                p->nrm_v.v[i * p->p + j] = nb[i] * nb[j];
+                p->nrm_z.v[i * p->p + j] = na[i] * na[j];
+            }
     }
     cudaError_t e = cudaSetDevice(p->device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device);
@@ -1315,8 +1084,7 @@ int wino_plan_destroy(wino_plan* p) {
     free_weights(p);
     free_compress_scratch(p);
     chk(cudaGetLastError(), "free_weights");
-    if (p->d_dwc) chk(cudaFree(p->d_dwc), "d_dwc");
-    if (p->d_oz) chk(cudaFree(p->d_oz), "d_oz");
+    if (p->d_xpart) chk(cudaFree(p->d_xpart), "d_xpart");
     if (p->d_z) chk(cudaFree(p->d_z), "d_z");
     if (p->d_dv) chk(cudaFree(p->d_dv), "d_dv");
     if (p->d_scalar) chk(cudaFree(p->d_scalar), "d_scalar");
@@ -1327,7 +1095,6 @@ int wino_plan_destroy(wino_plan* p) {
     if (p->ev_v) chk(cudaEventDestroy(p->ev_v), "ev_v");
     if (p->ev_dz) chk(cudaEventDestroy(p->ev_dz), "ev_dz");
     if (p->ev_join2) chk(cudaEventDestroy(p->ev_join2), "ev_join2");
-    if (p->d_partial) chk(cudaFree(p->d_partial), "d_partial");
     if (p->d_slice_off) chk(cudaFree(p->d_slice_off), "d_slice_off");
     for (auto& r : p->recs) {
         cudaEventDestroy(r.a);
@@ -1393,14 +1160,13 @@ int wino_set_weights_csr(wino_plan* p, const uint64_t* const* row_ptr, const uin
 
 int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense) {
     if (!p || !w_f) return set_err(WINO_INVALID_ARGUMENT, "null argument");
-    if (dense < 0 || dense > 3) return set_err(WINO_INVALID_ARGUMENT, "dense must be 0..3");
+    if (dense < 0 || dense > 2) return set_err(WINO_INVALID_ARGUMENT, "dense must be 0, 1 or 2");
     CUDA_TRY(cudaSetDevice(p->device));
     // dense != 0: every coordinate is a weight (zeros included): the full CSR
     int rc = device_compress(p, w_f, zero_tol, dense ? 1 : 0);
     if (rc != WINO_OK || !dense) return rc;
     p->dense = true;
-    p->tc_fast = dense == 3;
-    if (dense >= 2) {
+    if (dense == 2) {
         rc = refresh_tc_operands(p, nullptr);
         if (rc == WINO_OK) CUDA_TRY(cudaDeviceSynchronize());
     }
@@ -1456,37 +1222,6 @@ int wino_values_updated(wino_plan* p, void* stream) {
 // Opt-in (WINO_TC_PRESPLIT=1): measured at c3 dense 2041 vs 1945 µs — the dW GEMM gains (581 ->
 // 401 µs) but K1/K4 write twice the bytes (+50/+90 µs) and the forward/dĨ_F GEMMs, which were not
 // split-bound, load twice the B bytes (+25/+40 µs); c1 with the tensor-core contraction: 141 vs 148.
-static bool ws_kernel_selected() {
-    static const bool ok = !(std::getenv("WINO_TC_WS") && std::atoi(std::getenv("WINO_TC_WS")) == 0) &&
-                           !(std::getenv("WINO_TC_FOLD") && std::atoi(std::getenv("WINO_TC_FOLD")) != 1) &&
-                           !(std::getenv("WINO_TC_PERSISTENT") && std::atoi(std::getenv("WINO_TC_PERSISTENT")) == 0) &&
-                           !(std::getenv("WINO_TC_DW") && std::atoi(std::getenv("WINO_TC_DW")) != 8);
-    return ok;
-}
-static bool tc_dw_path(const wino_plan* p) {
-    return p->dense || p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
-}
-static bool tf32_presplit(const wino_plan* p) {
-    static const bool env = std::getenv("WINO_TC_PRESPLIT") && std::atoi(std::getenv("WINO_TC_PRESPLIT")) == 1;
-    return env && p->tc_ready && !p->tc_fast && p->dw_mode != 2 && ws_kernel_selected() &&
-           (p->dense || p->contraction == 1) && tc_dw_path(p);
-}
-static int ensure_cache_t(wino_plan* p, wino_cache* c) {
-    if (c->Vt) return WINO_OK;
-    const int64_t NTs = round_up((int64_t)c->n_max * p->g.t, 4);
-    CUDA_TRY(cudaMalloc(&c->Vt, (size_t)p->P2 * p->C * NTs * sizeof(float)));
-    CUDA_TRY(cudaMalloc(&c->DZt, (size_t)p->P2 * p->K * NTs * sizeof(float)));
-    return WINO_OK;
-}
-
-static int ensure_cache_lo(wino_plan* p, wino_cache* c) {
-    if (c->Vlo) return WINO_OK;
-    const int64_t NTs = round_up((int64_t)c->n_max * p->g.t, 4);
-    CUDA_TRY(cudaMalloc(&c->Vlo, (size_t)p->P2 * p->C * NTs * sizeof(float)));
-    CUDA_TRY(cudaMalloc(&c->DZlo, (size_t)p->P2 * p->K * NTs * sizeof(float)));
-    return WINO_OK;
-}
-
 int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
     if (!p || !out || n_max <= 0) return set_err(WINO_INVALID_ARGUMENT, "bad argument");
     CUDA_TRY(cudaSetDevice(p->device));
@@ -1497,16 +1232,8 @@ int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
     cudaError_t e = cudaMalloc(&c->V, (size_t)p->P2 * p->C * NTs * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&c->DZ, (size_t)p->P2 * p->K * NTs * sizeof(float));
     if (e != cudaSuccess) {
-        if (c->V) cudaFree(c->V);
-        delete c;
+        wino_cache_destroy(c);
         return set_err(WINO_CUDA_ERROR, std::string("cache_create: ") + cudaGetErrorString(e));
-    }
-    if (p->dw_mode == 2) {
-        const int rc = ensure_cache_lo(p, c);
-        if (rc) {
-            wino_cache_destroy(c);
-            return rc;
-        }
     }
     *out = c;
     return WINO_OK;
@@ -1514,13 +1241,52 @@ int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
 
 int wino_cache_destroy(wino_cache* c) {
     if (!c) return WINO_OK;
-    if (c->V) cudaFree(c->V);
-    if (c->DZ) cudaFree(c->DZ);
-    if (c->Vt) cudaFree(c->Vt);
-    if (c->DZt) cudaFree(c->DZt);
-    if (c->Vlo) cudaFree(c->Vlo);
-    if (c->DZlo) cudaFree(c->DZlo);
+    for (void* q : {(void*)c->V, (void*)c->DZ, (void*)c->dig_v, (void*)c->dig_z, (void*)c->amax_v,
+                    (void*)c->amax_z, (void*)c->e_v, (void*)c->e_z})
+        if (q) cudaFree(q);
     delete c;
+    return WINO_OK;
+}
+
+// the dW_F stream (greatest priority: the longest chain of a step) and the dI stream, on the
+// plan's device
+static int ensure_streams(wino_plan* p) {
+    if (!p->side) {
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    if (!p->side2) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_v, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_dz, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
+    }
+    return WINO_OK;
+}
+
+// After a fork, every exit (errors included) joins the side streams back into the caller's
+// stream, so a CUDA-graph capture stays joined and eager callers stay ordered after the side work.
+struct JoinGuard {
+    wino_plan* p;
+    cudaStream_t st;
+    bool side, side2;
+    ~JoinGuard() {
+        if (side) {
+            cudaEventRecord(p->ev_join, p->side);
+            cudaStreamWaitEvent(st, p->ev_join, 0);
+        }
+        if (side2) {
+            cudaEventRecord(p->ev_join2, p->side2);
+            cudaStreamWaitEvent(st, p->ev_join2, 0);
+        }
+    }
+};
+
+static int zero_rows(unsigned* a, int g0, int g1, int rows, cudaStream_t st) {
+    CUDA_TRY(cudaMemsetAsync(a + (int64_t)g0 * rows, 0, (size_t)(g1 - g0) * rows * sizeof(unsigned), st));
     return WINO_OK;
 }
 
@@ -1532,6 +1298,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
     if (n <= 0) return set_err(WINO_SHAPE_ERROR, "batch must be positive");
     if (cache && (cache->plan != p || n > cache->n_max))
         return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t NT = (int64_t)n * p->g.t;
     const int64_t NTs = round_up(NT, 4);
@@ -1543,23 +1310,25 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         V = p->d_dv;  // inference: the backward scratch doubles as Ĩ_F
     }
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
+    unsigned* amax = nullptr;
+    int nseg = 0;
     if (cache) {
-        cache->v_split = tf32_presplit(p);
-        if (cache->v_split && (rc = ensure_cache_t(p, cache))) return rc;
+        cache->has_fwd = false;
+        if ((rc = plan_segments(p, cache, 0, n, true))) return rc;
+        nseg = (int)cache->segs.size();
+        if ((rc = zero_rows(cache->amax_v, 0, nseg, p->C, st))) return rc;
+        amax = cache->amax_v;
     }
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 0, NTs)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, p->d_z, n, NT, NTs, flags, 0, NTs, amax,
+                          seg_images(p))))
         return rc;
-    if (cache && p->dw_mode == 2) {
-        if ((rc = ensure_cache_lo(p, cache))) return rc;
-        if ((rc = DISPATCH_MP(p, launch_input_lo, p, st, input, V, cache->Vlo, NT, NTs))) return rc;
-    }
+    if (cache && (rc = DISPATCH_MP(p, launch_input_digits, p, st, input, 0, cache, 0, nseg))) return rc;
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs,
-                            cache && cache->v_split ? cache->Vt : nullptr);
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, p->d_z, n, NT, NTs, flags, 1, NTs)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, p->d_z, n, NT, NTs, flags, 1, NTs)))
         return rc;
     if (cache) {
         cache->n = n;
@@ -1579,60 +1348,31 @@ static int bwd_check(wino_plan* p, const float* grad_output, const float* relu_o
         return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
     if ((flags & WINO_BWD_RELU_MASK) && !relu_out)
         return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
-    if (p->dw_mode == 2 && !c->Vlo)
-        return set_err(WINO_CONSISTENCY_ERROR, "precise dW: run the forward with this mode set");
+    CUDA_TRY(cudaSetDevice(p->device));
     return WINO_OK;
 }
 
-// dZ = A1·dÕ·A2ᵀ (+ its fp32 residual in the precise mode) into the cache
+// K4: dZ = A1·dÕ·A2ᵀ into the cache, with the per-segment max|dO| of the dZ digits
 static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, int flags,
                       cudaStream_t st) {
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
     const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    c->dz_split = tf32_presplit(p);
-    if (c->dz_split) {
-        const int rc0 = ensure_cache_t(p, c);
-        if (rc0) return rc0;
-    }
-    int rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs,
-                         c->dz_split ? c->DZt : nullptr);
+    int rc = zero_rows(c->amax_z, 0, (int)c->segs.size(), p->K, st);
     if (rc) return rc;
-    if (p->dw_mode == 2)
-        rc = DISPATCH_MP(p, launch_grad_z_lo, p, st, grad_output, relu_out, c->DZ, c->DZlo, NT, NTs, mask);
-    return rc;
+    c->z_segs = 0;
+    return DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs, c->amax_z,
+                       seg_images(p));
 }
 
-// dW_F from the cached dZ and Ĩ_F
-static int bwd_dw(wino_plan* p, const wino_cache* c, float* grad_w, cudaStream_t st) {
-    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    const bool precise = p->dw_mode == 2;
-    int rc = WINO_OK;
-    const float* dzt = c->dz_split ? c->DZt : nullptr;
-    const float* vt = c->v_split ? c->Vt : nullptr;
-    if (p->dense && p->tc_ready && !precise) return launch_tc_dw(p, st, c->DZ, c->V, grad_w, NTs, false, dzt, vt);
-    if ((c->v_split || c->dz_split) && !(!p->dense && tc_dw_path(p) && p->nnz > 0))
-        return set_err(WINO_CONSISTENCY_ERROR, "the cache holds tensor-core split operands: rerun the forward "
-                                               "after changing the dW mode / contraction");
-    float* dwc = grad_w;
-    if (p->dense && (rc = ensure(&p->d_dwc, &p->dwc_cap, (size_t)p->nnz))) return rc;
-    if (p->dense) dwc = p->d_dwc;
-    const bool tc_dw = p->dw_mode == 1 || (p->dw_mode == 0 && p->contraction_mode == 2 && p->contraction == 1);
-    if (!p->dense && tc_dw && p->nnz > 0)
-        rc = launch_tc_dw(p, st, c->DZ, c->V, dwc, NTs, /*masked=*/true, dzt, vt);
-    else if (!p->dense && p->dw_mode == 3 && p->nnz > 0)
-        rc = launch_ozaki_dw(p, st, c->DZ, c->V, dwc, NT, NTs);
-    else if (precise)
-        rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs, c->DZlo, c->Vlo);
-    else
-        rc = launch_sddmm(p, st, c->DZ, c->V, dwc, NT, NTs);
+// dZ digits of the whole batch, then dW_F (exact, wino_xdw.cuh)
+static int bwd_dw(wino_plan* p, wino_cache* c, const float* grad_output, const float* relu_out, int flags,
+                  float* grad_w, cudaStream_t st) {
+    const int nseg = (int)c->segs.size();
+    int rc = DISPATCH_MP(p, launch_grad_digits, p, st, grad_output, relu_out, (flags & WINO_BWD_RELU_MASK) != 0, 0,
+                         c, 0, nseg);
     if (rc) return rc;
-    if (p->dense) {  // [s][k][c] -> K×C×p×q
-        Launch L(p, st, K_MISC);
-        wino::slice_major_to_kcpq_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(dwc, grad_w, p->K,
-                                                                                            p->C, p->P2);
-        rc = L.done();
-    }
-    return rc;
+    c->z_segs = nseg;
+    return launch_xdw(p, st, c, grad_w);
 }
 
 // dĨ_F = W_Fᵀ·dZ and dI = Σ_φ B1·dĨ_F·B2ᵀ
@@ -1641,11 +1381,7 @@ static int bwd_input(wino_plan* p, const wino_cache* c, float* grad_input, cudaS
     int rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs);
     if (rc) return rc;
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs,
-                            c->dz_split ? c->DZt : nullptr);
-    else if (c->dz_split)
-        return set_err(WINO_CONSISTENCY_ERROR, "the cache holds tensor-core split operands: rerun the backward "
-                                               "after changing the contraction");
+        rc = launch_tc_gemm(p, st, K_DENSE_DV, p->map_wth, p->map_wtl, c->DZ, p->d_dv, p->C, p->K, NTs);
     else
         rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, c->DZ, p->d_dv, p->C, p->K, NT, NTs);
     if (rc) return rc;
@@ -1658,9 +1394,8 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
-    if ((rc = bwd_dw(p, c, grad_w, st))) return rc;
     c->has_grad_z = true;
-    return WINO_OK;
+    return bwd_dw(p, c, grad_output, relu_out, flags, grad_w, st);
 }
 
 int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, float* grad_w,
@@ -1668,36 +1403,23 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
     int rc = bwd_check(p, grad_output, relu_out, c, grad_w, flags);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    if (!grad_input) {  // no dI wanted (the first layer of a stack, train.cpp:201): dW only
-        if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
-        c->has_grad_z = true;
-        return bwd_dw(p, c, grad_w, st);
-    }
-    if (!p->side) {
-        // dW_F is the longest chain of the step: its stream gets the greatest priority, so its
-        // blocks are scheduled first whenever SMs free up (c1 step 172 -> 169 µs measured)
-        int lo = 0, hi = 0;
-        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CUDA_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-    }
     if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
     c->has_grad_z = true;
-    // dW (side stream) and dĨ_F -> dI (caller's stream) only share the read-only dZ and Ĩ_F
+    if (!grad_input)  // no dI wanted (the first layer of a stack, train.cpp:201): dW only
+        return bwd_dw(p, c, grad_output, relu_out, flags, grad_w, st);
+    if ((rc = ensure_streams(p))) return rc;
+    // dW (side stream) and dĨ_F -> dI (caller's stream) only share the read-only dZ / dO
     CUDA_TRY(cudaEventRecord(p->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
-    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
-    CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
-    if ((rc = bwd_input(p, c, grad_input, st))) return rc;
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
-    return WINO_OK;
+    JoinGuard join{p, st, true, false};
+    if ((rc = bwd_dw(p, c, grad_output, relu_out, flags, grad_w, p->side))) return rc;
+    return bwd_input(p, c, grad_input, st);
 }
 
 // One training step of the layer (forward, then backward with both gradients) scheduled as the
 // dependency graph it is instead of in API order: dZ = A1·dÕ·A2ᵀ needs only dO, so the
-// dO -> dZ -> dĨ_F -> dI chain runs beside the forward from the start (side2), and dW_F waits
-// for just Ĩ_F and dZ (side) — the forward's SpMM and output transform overlap the backward.
+// dO -> dZ -> dĨ_F -> dI chain runs beside the forward from the start (side2), and the dW_F chain
+// (digits of Ĩ_F and dZ, the int8 GEMM) waits for just K1 and K4 (side).
 // Same kernels, same buffers, same results bit for bit as wino_forward + wino_backward.
 int wino_forward_backward(wino_plan* p, int n, const float* input, float* output, wino_cache* c,
                           const float* grad_output, float* grad_w, float* grad_input, void* stream) {
@@ -1708,29 +1430,17 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     if (n <= 0) return set_err(WINO_SHAPE_ERROR, "batch must be positive");
     if (c->plan != p || n > c->n_max)
         return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
-    if (!p->side) {
-        // dW_F is the longest chain of the step: its stream gets the greatest priority, so its
-        // blocks are scheduled first whenever SMs free up (c1 step 172 -> 169 µs measured)
-        int lo = 0, hi = 0;
-        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CUDA_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-    }
-    if (!p->side2) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_v, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_dz, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
-    }
+    if ((rc = ensure_streams(p))) return rc;
     const int64_t NT = (int64_t)n * p->g.t;
     const int64_t NTs = round_up(NT, 4);
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * NTs))) return rc;
-    if (p->dw_mode == 2 && (rc = ensure_cache_lo(p, c))) return rc;
-    c->v_split = tf32_presplit(p);
-    if (c->v_split && (rc = ensure_cache_t(p, c))) return rc;
+    c->has_fwd = false;
+    if ((rc = plan_segments(p, c, 0, n, true))) return rc;
+    const int nseg = (int)c->segs.size();
+    if ((rc = zero_rows(c->amax_v, 0, nseg, p->C, st)) || (rc = zero_rows(c->amax_z, 0, nseg, p->K, st))) return rc;
     c->n = n;
     c->NTs = NTs;
     c->has_fwd = true;
@@ -1739,34 +1449,32 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     CUDA_TRY(cudaEventRecord(p->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    JoinGuard join{p, st, true, true};
     // side2: dZ, then dĨ_F = W_Fᵀ·dZ and dI
-    if ((rc = bwd_grad_z(p, grad_output, nullptr, c, 0, p->side2))) return rc;
+    if ((rc = DISPATCH_MP(p, launch_grad_z, p, p->side2, grad_output, nullptr, c->DZ, NT, NTs, false, NTs,
+                          c->amax_z, seg_images(p))))
+        return rc;
     CUDA_TRY(cudaEventRecord(p->ev_dz, p->side2));
     if ((rc = bwd_input(p, c, grad_input, p->side2))) return rc;
-    CUDA_TRY(cudaEventRecord(p->ev_join2, p->side2));
     // caller's stream: Ĩ_F, then Z = W_F·Ĩ_F and O
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c, c->V, p->d_z, n, NT, NTs, 0, 0, NTs)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c->V, p->d_z, n, NT, NTs, 0, 0, NTs,
+                          c->amax_v, seg_images(p))))
         return rc;
-    if (p->dw_mode == 2 && (rc = DISPATCH_MP(p, launch_input_lo, p, st, input, c->V, c->Vlo, NT, NTs))) return rc;
     CUDA_TRY(cudaEventRecord(p->ev_v, st));
-    // side: dW_F once Ĩ_F and dZ exist
+    // side: the dW_F chain once K1 and K4 have the segment maxima
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_v, 0));
+    if ((rc = DISPATCH_MP(p, launch_input_digits, p, p->side, input, 0, c, 0, nseg))) return rc;
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_dz, 0));
-    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
-    CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
+    if ((rc = bwd_dw(p, c, grad_output, nullptr, 0, grad_w, p->side))) return rc;
     if (p->tc_ready && (p->dense || p->contraction == 1))
-        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs,
-                            c->v_split ? c->Vt : nullptr);
+        rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs);
     else
         rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, c->V, p->d_z, p->K, p->C, NT, NTs);
     if (rc) return rc;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c, c->V, p->d_z, n, NT, NTs, 0, 1, NTs)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c->V, p->d_z, n, NT, NTs, 0, 1, NTs)))
         return rc;
-    // join
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join2, 0));
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
     c->has_grad_z = true;
-    return WINO_OK;
+    return WINO_OK;  // the guard joins side and side2 into st
 }
 
 // ---- image ranges of one batch (pipelined host transfers) ----
@@ -1788,9 +1496,9 @@ static int make_range(const wino_plan* p, int n_total, int n0, int n1, ColRange*
 }
 
 static int range_capable(const wino_plan* p) {
-    if (p->tc_ready || p->dw_mode != 0)
+    if (p->tc_ready)
         return set_err(WINO_CAPABILITY_ERROR, "image-range calls run the CSR kernels only "
-                                              "(no tensor-core plan/contraction, dW mode 0)");
+                                              "(no tensor-core plan/contraction)");
     return WINO_OK;
 }
 
@@ -1804,18 +1512,23 @@ int wino_forward_range(wino_plan* p, int n_total, int n0, int n1, const float* i
         return set_err(WINO_SHAPE_ERROR, "cache does not match plan / batch exceeds cache capacity");
     ColRange r{};
     if ((rc = make_range(p, n_total, n0, n1, &r))) return rc;
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * r.NTs))) return rc;
+    if (n0 == 0) cache->has_fwd = false;
+    const int g0 = n0 == 0 ? 0 : (int)cache->segs.size();
+    if ((rc = plan_segments(p, cache, n0, n1, false))) return rc;
+    const int g1 = (int)cache->segs.size();
+    if ((rc = zero_rows(cache->amax_v, g0, g1, p->C, st))) return rc;
     float* V = cache->V + r.a;
     float* Z = p->d_z + r.a;
-    cache->v_split = false;  // range calls run the CSR kernels on fp32 operands
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, Z, n1 - n0, r.NT, r.NTs, flags, 0,
-                          r.NTr)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, Z, n1 - n0, r.NT, r.NTs, flags, 0, r.NTr,
+                          cache->amax_v + (int64_t)g0 * p->C, seg_images(p))))
         return rc;
+    if ((rc = DISPATCH_MP(p, launch_input_digits, p, st, input, n0, cache, g0, g1))) return rc;
     if ((rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, Z, p->K, p->C, r.NT, r.NTs, r.NTr)))
         return rc;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, cache, V, Z, n1 - n0, r.NT, r.NTs, flags, 1,
-                          r.NTr)))
+    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, Z, n1 - n0, r.NT, r.NTs, flags, 1, r.NTr)))
         return rc;
     cache->n = n_total;
     cache->NTs = r.NTs;
@@ -1836,32 +1549,27 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
     if (mask && !relu_out) return set_err(WINO_INVALID_ARGUMENT, "relu mask requested without relu_out");
     ColRange r{};
     if ((rc = make_range(p, c->n, n0, n1, &r))) return rc;
+    int g0 = 0, g1 = 0;
+    if ((rc = find_segments(c, n0, n1, &g0, &g1))) return rc;
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = ensure(&p->d_dv, &p->dv_cap, (size_t)p->P2 * std::max(p->C, p->K) * r.NTs))) return rc;
     float* DZ = c->DZ + r.a;
     float* DV = p->d_dv + r.a;
-    c->dz_split = false;
-    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, DZ, r.NT, r.NTs, mask, r.NTr)))
+    if (n0 == 0) c->z_segs = 0;
+    if (g0 != c->z_segs)
+        return set_err(WINO_CONSISTENCY_ERROR, "backward image ranges of a batch must be issued in order from image 0");
+    if ((rc = zero_rows(c->amax_z, g0, g1, p->K, st))) return rc;
+    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, DZ, r.NT, r.NTs, mask, r.NTr,
+                          c->amax_z + (int64_t)g0 * p->K, seg_images(p))))
         return rc;
+    if ((rc = DISPATCH_MP(p, launch_grad_digits, p, st, grad_output, relu_out, mask, n0, c, g0, g1))) return rc;
     if ((rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, DZ, DV, p->C, p->K, r.NT, r.NTs,
                           r.NTr)))
         return rc;
     if ((rc = DISPATCH_MP(p, launch_input_grad, p, st, DV, grad_input, n1 - n0, r.NTs))) return rc;
-    // dW_F partials of this range's t chunks, when the range is whole chunks of the chunk-form
-    // SDDMM (backward_weights_cached then only sums the chunks)
-    const int64_t NTfull = (int64_t)c->n * p->g.t;
-    if (p->sddmm_impl == 1 && p->dw_mode == 0 && !p->dense && p->nnz > 0 && p->lane_tw > 0) {
-        const int TW = p->lane_tw;
-        const int chunks = (int)((NTfull + TW - 1) / TW);
-        const bool last = n1 == c->n;
-        if (chunks > 1 && r.a % TW == 0 && (last || (r.a + r.NT) % TW == 0)) {
-            const int z0 = (int)(r.a / TW), z1 = last ? chunks : (int)((r.a + r.NT) / TW);
-            if ((rc = launch_sddmm_chunk(p, st, c->DZ, c->V, nullptr, NTfull, r.NTs, z0, z1, false))) return rc;
-            if (z0 == 0) c->dw_chunks = 0;
-            c->dw_chunks += z1 - z0;
-        }
-    }
-    c->has_grad_z = true;
+    c->z_segs = g1;
+    c->has_grad_z = c->z_segs == (int)c->segs.size();
     return WINO_OK;
 }
 
@@ -1869,18 +1577,11 @@ int wino_backward_weights_cached(wino_plan* p, wino_cache* c, float* grad_w, voi
     int rc = check_plan(p);
     if (rc) return rc;
     if (!c || (!grad_w && p->nnz > 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
-    if (c->plan != p || !c->has_fwd || !c->has_grad_z)
+    if (c->plan != p || !c->has_fwd || !c->has_grad_z || c->segs.empty() || c->segs.back().n1 != c->n ||
+        c->z_segs != (int)c->segs.size())
         return set_err(WINO_CONSISTENCY_ERROR, "backward_weights_cached: dL/dZ missing; run backward_range first");
-    const int64_t NTfull = (int64_t)c->n * p->g.t;
-    if (p->sddmm_impl == 1 && p->dw_mode == 0 && !p->dense && p->lane_tw > 0 && p->nnz > 0 &&
-        c->dw_chunks == (int)((NTfull + p->lane_tw - 1) / p->lane_tw)) {
-        // every chunk's partials came from the ranges: only their ordered sum remains
-        const int rc2 = launch_sddmm_chunk(p, (cudaStream_t)stream, c->DZ, c->V, grad_w, NTfull, c->NTs, 0, 0, true);
-        c->dw_chunks = 0;
-        return rc2;
-    }
-    c->dw_chunks = 0;
-    return bwd_dw(p, c, grad_w, (cudaStream_t)stream);
+    CUDA_TRY(cudaSetDevice(p->device));
+    return launch_xdw(p, (cudaStream_t)stream, c, grad_w);
 }
 
 // ---- the data-parallel exchange: one in-place sum of dW_F over an NCCL communicator ----
@@ -2005,20 +1706,11 @@ int wino_set_option(wino_plan* p, int option, int value) {
         p->auto_permille = value;
         return p->contraction_mode == 2 ? apply_contraction(p) : WINO_OK;
     }
-    if (option != WINO_OPT_DW_MODE || value < 0 || value > 3)
-        return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
-    if (value == 1 || value == 3) {
-        if (p->C % 4 || p->K % 4)
-            return set_err(WINO_CAPABILITY_ERROR, "tensor-core dW needs C and K multiples of 4 (TMA strides)");
-        if (!p->d_slice_off && p->has_weights) {
-            CUDA_TRY(cudaMalloc(&p->d_slice_off, p->P2 * sizeof(int64_t)));
-            CUDA_TRY(cudaMemcpy(p->d_slice_off, p->slice_off.data(), p->P2 * sizeof(int64_t), cudaMemcpyHostToDevice));
-        }
+    if (option == WINO_OPT_DW_MODE) {  // one dW_F path: the exact int8 digit GEMM (wino_xdw.cuh)
+        if (value != 0) return set_err(WINO_INVALID_ARGUMENT, "dW mode: only 0 (exact) exists");
+        return WINO_OK;
     }
-    const bool replan = (value == 2) != (p->dw_mode == 2);
-    p->dw_mode = value;
-    if (replan && p->has_weights) plan_sddmm_all(p);  // the precise variant stages twice the rows
-    return WINO_OK;
+    return set_err(WINO_INVALID_ARGUMENT, "unknown option / value");
 }
 
 int64_t wino_launch_count(const wino_plan* p) { return p ? p->launches : -1; }

@@ -71,12 +71,24 @@ __device__ __forceinline__ float cmadd(float acc, float c, float x) {
     return madd(acc, c, x);
 }
 
-// tf32 hi/lo split of an fp32 value, bitwise the split the tcgen05 GEMM would do in shared
-// memory (wino_dense_tc.cuh split_tile_fast): hi = rna_tf32(x), lo = rna_tf32(x - hi).
-__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-    const uint32_t h = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
-    hi = __uint_as_float(h);
-    lo = __uint_as_float((__float_as_uint(__fsub_rn(x, hi)) + 0x1000u) & 0xffffe000u);
+// The same transform in the reference's doubles (the exact dW_F digit kernels, wino_xdw.cuh).
+struct CoefsD {
+    double a[kMaxP * kMaxP];  // a1: p×m row-major
+    double b[kMaxP * kMaxP];  // b1: p×p row-major
+};
+
+// atomicMax of a non-negative float's bits into amax[key] (key < 0: nothing), one atomic per warp
+// when the active lanes share the key (the common case: consecutive tiles of one channel).
+__device__ __forceinline__ void block_max_atomic(unsigned* amax, int key, unsigned mx) {
+    const unsigned am = __activemask();
+    const int leader = __ffs(am) - 1;
+    const int k0 = __shfl_sync(am, key, leader);
+    if (__all_sync(am, key == k0)) {
+        const unsigned r = __reduce_max_sync(am, mx);
+        if (k0 >= 0 && (int)(threadIdx.x & 31) == leader) atomicMax(amax + k0, r);
+    } else if (key >= 0) {
+        atomicMax(amax + key, mx);
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -87,11 +99,11 @@ template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
                        int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr,
-                       float* __restrict__ Vt = nullptr) {
-    // Vt != nullptr (tensor-core plans): V receives the tf32 hi part and Vt the lo part, the
-    // operand split done once here instead of in every GEMM tile that reads the value
+                       unsigned* __restrict__ amax = nullptr, int seg_imgs = 1) {
     // columns [0, NTr) of V rows with stride NTs (a column range of the batch when V and `in` are
-    // offset to its first image); columns ≥ NT are the zero padding
+    // offset to its first image); columns ≥ NT are the zero padding.
+    // amax != nullptr: also max|I| over the pixels each (segment, c) reads, segment = n / seg_imgs
+    // (the exponent bound of the exact dW_F digits, wino_xdw.cuh), as float bits via atomicMax
     const int64_t plane = (int64_t)C * NTs;
     const int64_t items = (int64_t)C * NTr;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
@@ -99,6 +111,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
         const int c = (int)(gid / NTr);
         const int nt = (int)(gid - (int64_t)c * NTr);
         float d[P][P];
+        int key = -1;
         if (nt < NT) {
             const int n = nt / T, t = nt - n * T;
             const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -114,11 +127,20 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                     d[i][j] = (yok && (unsigned)x < (unsigned)W) ? __ldg(src + y * W + x) : 0.f;
                 }
             }
+            if (amax) key = (n / seg_imgs) * C + c;
         } else {
 #pragma unroll
             for (int i = 0; i < P; ++i)
 #pragma unroll
                 for (int j = 0; j < P; ++j) d[i][j] = 0.f;
+        }
+        if (amax) {
+            unsigned mx = 0;
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+#pragma unroll
+                for (int j = 0; j < P; ++j) mx = max(mx, __float_as_uint(d[i][j]) & 0x7fffffffu);
+            block_max_atomic(amax, key, mx);
         }
         float tmp[P][P];
 #pragma unroll
@@ -137,15 +159,7 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                 float acc = 0.f;
 #pragma unroll
                 for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
-                const int64_t o = (int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt;
-                if (Vt) {
-                    float hi, lo;
-                    tf32_split(acc, hi, lo);
-                    V[o] = hi;
-                    Vt[o] = lo;
-                } else {
-                    V[o] = acc;
-                }
+                V[(int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt] = acc;
             }
     }
 }
@@ -208,8 +222,8 @@ template <int M, int P, bool MASK, class CF>
 __global__ void __launch_bounds__(256)
 grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
               float* __restrict__ DZ, const Coefs cf, int K, int Ho, int Wo, int tiles_x, int T,
-              int NT, int NTs, int NTr, float* __restrict__ DZt = nullptr) {
-    // DZt != nullptr: tf32 hi part into DZ, lo part into DZt (as input_transform_kernel)
+              int NT, int NTs, int NTr, unsigned* __restrict__ amax = nullptr, int seg_imgs = 1) {
+    // amax != nullptr: also max|dO| (after the mask) per (segment, k), as input_transform_kernel
     const int64_t plane = (int64_t)K * NTs;
     const int64_t items = (int64_t)K * NTr;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
@@ -217,10 +231,12 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
         const int k = (int)(gid / NTr);
         const int nt = (int)(gid - (int64_t)k * NTr);
         float d[M][M];
+        int key = -1;
         if (nt < NT) {
             const int n = nt / T, t = nt - n * T;
             const int ty = t / tiles_x, tx = t - ty * tiles_x;
             const int64_t base = ((int64_t)n * K + k) * Ho * Wo;
+            if (amax) key = (n / seg_imgs) * K + k;
 #pragma unroll
             for (int y = 0; y < M; ++y) {
                 const int oy = ty * M + y;
@@ -242,6 +258,14 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
 #pragma unroll
                 for (int x = 0; x < M; ++x) d[y][x] = 0.f;
         }
+        if (amax) {
+            unsigned mx = 0;
+#pragma unroll
+            for (int y = 0; y < M; ++y)
+#pragma unroll
+                for (int x = 0; x < M; ++x) mx = max(mx, __float_as_uint(d[y][x]) & 0x7fffffffu);
+            block_max_atomic(amax, key, mx);
+        }
         float m1[P][M];  // m1(i,x) = Σ_y a1(i,y)·d(y,x)
 #pragma unroll
         for (int i = 0; i < P; ++i)
@@ -259,15 +283,7 @@ grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
                 float acc = 0.f;
 #pragma unroll
                 for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), m1[i][x]);
-                const int64_t o = (int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt;
-                if (DZt) {
-                    float hi, lo;
-                    tf32_split(acc, hi, lo);
-                    DZ[o] = hi;
-                    DZt[o] = lo;
-                } else {
-                    DZ[o] = acc;
-                }
+                DZ[(int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt] = acc;
             }
     }
 }
@@ -576,305 +592,6 @@ spmm_kernel(const int* __restrict__ rowptr, const int2* __restrict__ colval,
     }
 }
 
-// ---------------------------------------------------------------------------------
-// K5: masked SDDMM  dW(e=(k,c)) = Σ_t dZ(k,t)·Ĩ_F(c,t)  for surviving (k,c) only
-//     (layer.cpp:118-128 restricted to the mask; masked coordinates are never updated,
-//     train.cpp:281-283).
-// Block = (row group, slice, t-split).  The block walks its t-range in TW-wide chunks with a
-// two-stage cp.async pipeline staging Ĩ_F(:, chunk) and dZ(rows, chunk).  A warp owns up to
-// MAXB batches of 32 consecutive nonzeros; for each it forms, per lane, the 32 partial dot
-// products over the lane's R columns, and a 62-shuffle fp64 transpose-reduction leaves lane j
-// with nonzero j's chunk sum, added to an fp64 register accumulator.  fp64 from the first
-// cross-lane add keeps dW_F at the accuracy of the fp32 operands themselves.
-// Deterministic: one owner per nonzero, fixed chunk order, t-split partials summed in order.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ void transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool hi = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const double send = hi ? v[i] : v[i + o];
-            const double keep = hi ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(kFull, send, o);
-        }
-    }
-}
-
-// 16 values per lane -> lane l (and l^16) ends with the total of value (l & 15): 15 exchange
-// steps over lane bits 3..0, then one across bit 4.
-__device__ __forceinline__ void transpose_reduce16(double (&v)[16], int lane) {
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) {
-        const bool hi = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const double send = hi ? v[i] : v[i + o];
-            const double keep = hi ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(kFull, send, o);
-        }
-    }
-    v[0] += __shfl_xor_sync(kFull, v[0], 16);
-}
-
-// LO (the precise mode): Ĩ_F and dZ also carry their fp32 residuals (Ĩ_F ≈ V + Vlo,
-// dZ ≈ DZ + DZlo to ~2^-48, wino_precise.cuh); each term is zh·xh + zh·xl + zl·xh with exact
-// fp64 products, so dW_F reaches the accuracy of the reference's f64 layer itself.
-template <int R, int MAXB, int STAGES, int BATCH, int THREADS, bool LO>
-__global__ void __launch_bounds__(THREADS)
-sddmm_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
-             const int* __restrict__ rowof, const float* __restrict__ DZ,
-             const float* __restrict__ V, const float* __restrict__ DZlo, const float* __restrict__ Vlo,
-             float* __restrict__ dW, double* __restrict__ partial,
-             int64_t nnz_total, int K, int C, int NT, int NTs, int rows_per_block, int t_per_split) {
-    constexpr int TW = 32 * R;
-    extern __shared__ float4 smem_f4[];
-    const int s = blockIdx.y;
-    const int r0 = blockIdx.x * rows_per_block;
-    const int r1 = min(K, r0 + rows_per_block);
-    const int nrb = r1 - r0;
-    const int* rp = rowptr + (int64_t)s * (K + 1);
-    const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
-    const int nb = e1 - e0;
-    const int tb = blockIdx.z * t_per_split;
-    const int te = min(NT, tb + t_per_split);
-    const int hi_floats = (C + nrb) * TW;  // [Ĩ_F rows C][dZ rows nrb] × TW (then the lo copy)
-    const int stage_floats = hi_floats * (LO ? 2 : 1);
-    float* st0 = reinterpret_cast<float*>(smem_f4);
-    const float* vg = V + (int64_t)s * C * NTs;
-    const float* zg = DZ + ((int64_t)s * K + r0) * NTs;
-    const float* vlg = LO ? Vlo + (int64_t)s * C * NTs : nullptr;
-    const float* zlg = LO ? DZlo + ((int64_t)s * K + r0) * NTs : nullptr;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-
-    // per nonzero: (row offset, col offset) into the staged chunk, in units of R floats
-    int pk[MAXB];
-    double acc[MAXB];
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        const int b = (warp + i * nw) * BATCH + (lane & (BATCH - 1));
-        pk[i] = 0;
-        if (b < nb) pk[i] = (((__ldg(rowof + e0 + b) - r0 + C) * 32) << 16) | (__ldg(colidx + e0 + b) * 32);
-        acc[i] = 0.0;
-    }
-    auto stage = [&](int buf, int t0) {
-        float* vs = st0 + buf * stage_floats;
-        stage_rows_async<TW>(vg, vs, C, NTs, t0);
-        stage_rows_async<TW>(zg, vs + C * TW, nrb, NTs, t0);
-        if constexpr (LO) {
-            stage_rows_async<TW>(vlg, vs + hi_floats, C, NTs, t0);
-            stage_rows_async<TW>(zlg, vs + hi_floats + C * TW, nrb, NTs, t0);
-        }
-        cp_async_commit();
-    };
-    if (STAGES == 2 && tb < te) stage(0, tb);
-    int buf = 0;
-    for (int t0 = tb; t0 < te; t0 += TW) {
-        if (STAGES == 2) {
-            if (t0 + TW < te) {
-                stage(buf ^ 1, t0 + TW);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-        } else {
-            stage(0, t0);
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        // lane-relative base: element (row, lane's R columns) of the staged chunk
-        const float* base = st0 + buf * stage_floats + lane * R;
-#pragma unroll
-        for (int i = 0; i < MAXB; ++i) {
-            // warp-uniform conditions are evaluated through votes, so the compiler knows the
-            // shuffles below run converged (no collective fallback code around them)
-            if (!__any_sync(kFull, (warp + i * nw) * BATCH < nb)) break;
-            double part[BATCH];
-            double zd[R];
-            double zl[LO ? R : 1];
-            int qv[BATCH];
-#pragma unroll
-            for (int j = 0; j < BATCH; ++j) qv[j] = __shfl_sync(kFull, pk[i], j);
-            int rprev = -1;
-#pragma unroll
-            for (int j = 0; j < BATCH; ++j) {
-                const int q = qv[j];
-                const int ro = q >> 16;
-                if (__any_sync(kFull, ro != rprev)) {
-                    float z[R];
-                    lds_vec<R>(base + ro * R, z);
-#pragma unroll
-                    for (int qq = 0; qq < R; ++qq) zd[qq] = (double)z[qq];
-                    if constexpr (LO) {
-                        lds_vec<R>(base + hi_floats + ro * R, z);
-#pragma unroll
-                        for (int qq = 0; qq < R; ++qq) zl[qq] = (double)z[qq];
-                    }
-                    rprev = ro;
-                }
-                float x[R];
-                lds_vec<R>(base + (q & 0xffff) * R, x);
-                double pr = zd[0] * (double)x[0];  // exact: fp32×fp32 fits fp64
-#pragma unroll
-                for (int qq = 1; qq < R; ++qq) pr = fma(zd[qq], (double)x[qq], pr);
-                if constexpr (LO) {
-                    float xl[R];
-                    lds_vec<R>(base + hi_floats + (q & 0xffff) * R, xl);
-#pragma unroll
-                    for (int qq = 0; qq < R; ++qq) pr = fma(zd[qq], (double)xl[qq], fma(zl[qq], (double)x[qq], pr));
-                }
-                part[j] = pr;
-            }
-            if constexpr (BATCH == 32)
-                transpose_reduce32(part, lane);
-            else
-                transpose_reduce16(part, lane);
-            acc[i] += part[0];
-        }
-        __syncthreads();
-        if (STAGES == 2) buf ^= 1;
-    }
-    // single split -> dW (fp32); several -> fp64 partials [split][nnz_total], summed in order
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        const int b = (warp + i * nw) * BATCH + lane;
-        if (lane < BATCH && b < nb) {
-            if (partial == nullptr)
-                dW[e0 + b] = (float)acc[i];
-            else
-                partial[(int64_t)blockIdx.z * nnz_total + e0 + b] = acc[i];
-        }
-    }
-}
-
-// K5, chunk form (the default SDDMM).  Block = (row group, slice, one TW-wide t chunk): Ĩ_F(:, chunk)
-// and dZ(rows, chunk) are staged once, then every nonzero of the row group is reduced over the
-// chunk by one quarter-warp: lane l of the quarter covers t = 4l + 32i (i < TW/32), so each
-// LDS.128 step of a quarter reads 128 contiguous bytes of the nonzero's Ĩ_F row (conflict-free).
-// A quarter walks a contiguous CSR segment, so its dZ row stays cached in registers as fp64 and
-// is reloaded only when the row changes.  Products are exact fp64 products of the fp32 operands
-// (one conversion per product), summed in two fp64 chains per lane, then across the quarter by
-// a 3-step xor butterfly.  The chunk sum goes to partial[chunk][e] (fp64; summed over chunks in
-// order by split_sum_kernel) or straight to dW when there is one chunk.  No per-chunk state
-// survives the block, so blocks never re-stage the same Ĩ_F chunk for the same nonzeros.
-// Deterministic: fixed per-lane t order, fixed butterfly, fixed chunk order.
-template <int TW, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1)
-sddmm_chunk_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
-                   const int* __restrict__ rowof, const float* __restrict__ DZ,
-                   const float* __restrict__ V, float* __restrict__ dW, double* __restrict__ partial,
-                   int64_t nnz_total, int K, int C, int NTs, int rows_per_block, int z0) {
-    constexpr int Q = TW / 32;  // LDS.128 steps per lane per nonzero
-    constexpr int NQ = THREADS / 8;
-    extern __shared__ float4 smem_f4[];
-    const int s = blockIdx.y;
-    const int r0 = blockIdx.x * rows_per_block;
-    const int r1 = min(K, r0 + rows_per_block);
-    const int nrb = r1 - r0;
-    const int* rp = rowptr + (int64_t)s * (K + 1);
-    const int e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
-    const int zc = z0 + (int)blockIdx.z;  // t chunk (a column range of the batch starts at chunk z0)
-    const int t0 = zc * TW;
-    float* vs = reinterpret_cast<float*>(smem_f4);
-    float* zs = vs + C * TW;
-    stage_rows_async<TW>(V + (int64_t)s * C * NTs, vs, C, NTs, t0);
-    stage_rows_async<TW>(DZ + ((int64_t)s * K + r0) * NTs, zs, nrb, NTs, t0);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    const int ql = threadIdx.x & 7;
-    const int quarter = threadIdx.x >> 3;
-    const int nb = e1 - e0;
-    const int per = (nb + NQ - 1) / NQ;
-    const int qb = e0 + quarter * per;
-    const int qe = min(e1, qb + per);
-    double zd[4 * Q];
-    int rcur = -1;
-    // chunk sum of nonzero e over this lane's t (exact products, two fp64 chains)
-    auto lane_dot = [&](int e) -> double {
-        const int r = __ldg(rowof + e), c = __ldg(colidx + e);
-        if (r != rcur) {
-            const float* zr = zs + (r - r0) * TW + 4 * ql;
-#pragma unroll
-            for (int i = 0; i < Q; ++i) {
-                const float4 z = *reinterpret_cast<const float4*>(zr + 32 * i);
-                zd[4 * i] = z.x;
-                zd[4 * i + 1] = z.y;
-                zd[4 * i + 2] = z.z;
-                zd[4 * i + 3] = z.w;
-            }
-            rcur = r;
-        }
-        const float* xr = vs + c * TW + 4 * ql;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            const float4 x = *reinterpret_cast<const float4*>(xr + 32 * i);
-            a0 = fma(zd[4 * i], (double)x.x, a0);  // exact products: fp32×fp32 fits fp64
-            a1 = fma(zd[4 * i + 1], (double)x.y, a1);
-            a0 = fma(zd[4 * i + 2], (double)x.z, a0);
-            a1 = fma(zd[4 * i + 3], (double)x.w, a1);
-        }
-        return a0 + a1;
-    };
-    auto put = [&](int e, double v) {
-        if (partial == nullptr)
-            dW[e] = (float)v;
-        else
-            partial[(int64_t)zc * nnz_total + e] = v;
-    };
-    // Warp-uniform trip counts (the longest of the warp's four quarters; a shorter quarter works on
-    // a clamped entry and does not store), so every shuffle below runs converged with a full mask.
-    const int cnt = qe - qb;
-    const int wmax = __reduce_max_sync(kFull, cnt > 0 ? cnt : 0);
-    const int nb4 = wmax >> 2;
-    // batches of 4 nonzeros: a 4-value transpose-reduce across the 8 lanes (8 shuffles per batch
-    // instead of 6 per nonzero); lanes 2j, 2j+1 end with nonzero j's sum
-    for (int i = 0; i < nb4; ++i) {
-        const int e = qb + 4 * i;
-        double v[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = lane_dot(min(e + j, e1 - 1));
-        {  // o = 4: exchange halves
-            const bool hi = (ql & 4) != 0;
-#pragma unroll
-            for (int i2 = 0; i2 < 2; ++i2) {
-                const double send = hi ? v[i2] : v[i2 + 2];
-                const double keep = hi ? v[i2 + 2] : v[i2];
-                v[i2] = keep + __shfl_xor_sync(kFull, send, 4);
-            }
-        }
-        {  // o = 2
-            const bool hi = (ql & 2) != 0;
-            const double send = hi ? v[0] : v[1];
-            const double keep = hi ? v[1] : v[0];
-            v[0] = keep + __shfl_xor_sync(kFull, send, 2);
-        }
-        v[0] += __shfl_xor_sync(kFull, v[0], 1);
-        // lane ql now holds the sum of nonzero ((ql >> 2) & 1) * 2 + ((ql >> 1) & 1)
-        const int eo = e + (((ql >> 2) & 1) << 1) + ((ql >> 1) & 1);
-        if ((ql & 1) == 0 && eo < qe) put(eo, v[0]);
-    }
-    for (int e = qb + 4 * nb4; e < qb + wmax; ++e) {
-        double v = lane_dot(min(e, e1 - 1));
-        v += __shfl_xor_sync(kFull, v, 1);
-        v += __shfl_xor_sync(kFull, v, 2);
-        v += __shfl_xor_sync(kFull, v, 4);
-        if (ql == 0 && e < qe) put(e, v);
-    }
-}
-
-__global__ void split_sum_kernel(const double* __restrict__ partial, float* __restrict__ dW,
-                                 int64_t nnz, int splits) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double a = 0.0;
-        for (int q = 0; q < splits; ++q) a += partial[(int64_t)q * nnz + i];
-        dW[i] = (float)a;
-    }
-}
-
-
 // Masked SGD on the CSR values (train.cpp:281-290; L2 term train.cpp:219-223)
 __global__ void sgd_kernel(float* __restrict__ vals, const float* __restrict__ grad, int64_t nnz,
                            float lr, float scale, float l2_over_norm) {
@@ -934,17 +651,6 @@ __global__ void split_tf32_kernel(const float* __restrict__ w, float* __restrict
         const int64_t t = (s * C + c) * K + k;
         wth[t] = __uint_as_float(h);
         wtl[t] = __uint_as_float(l);
-    }
-}
-
-// dense-plan dW: slice-major compact [s][k][c] -> W_F layout K×C×p×q
-__global__ void slice_major_to_kcpq_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                                           int K, int C, int P2) {
-    const int64_t total = (int64_t)P2 * K * C;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = i / ((int64_t)K * C), kc = i - s * K * C;
-        dst[kc * P2 + s] = src[i];
     }
 }
 

@@ -63,4 +63,24 @@ inline bool make_map_3d_sw(CUtensorMap* map, const void* base, uint64_t d0, uint
     return r == CUDA_SUCCESS;
 }
 
+// uint8 4-D map (d0 innermost .. d3) over a dense [d3][d2][d1][d0] byte tensor; box (b0, b1, 1, d3):
+// one load brings a box of every d3 plane (the exact dW_F digit planes, wino_xdw.cuh)
+inline bool make_map_4d_u8(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                           uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn) {
+        last_tmap_error() = -1;
+        return false;
+    }
+    cuuint64_t dims[4] = {d0, d1, d2, d3};
+    cuuint64_t strides[3] = {d0, d0 * d1, d0 * d1 * d2};
+    cuuint32_t box[4] = {b0, b1, 1, (cuuint32_t)d3};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    last_tmap_error() = (int)r;
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace wino

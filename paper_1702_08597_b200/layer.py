@@ -142,10 +142,10 @@ class WinogradLayer:
     def set_weights(self, w_f, zero_tol: float = 0.0, dense: bool | str | None = None):
         """W_F (K×C×p×q).
         dense=False: CSR of the nonzeros (the sparse path).  dense=None: dense when no entry is
-        dropped.  dense=True / 'tc': every coordinate is a weight; the contractions run on the
-        tensor cores (3xTF32 tcgen05, each k-block folded into fp64 — fp32-level accuracy).
-        dense='exact': the reference-order SIMT kernels (bitwise forward).  dense='tc-fast': one
-        TMEM accumulation chain (fastest, ~1e-6 of Σ|w·x|)."""
+        dropped.  dense=True / 'tc': every coordinate is a weight; Z and dĨ_F run on the tensor
+        cores (3xTF32 tcgen05, compensated fp32 fold per k-block — fp32-level accuracy).
+        dense='exact': the reference-order SIMT kernels (bitwise forward).  dW_F is the exact
+        int8 digit GEMM on every plan (to the reference's f64 accuracy)."""
         w_f = np.ascontiguousarray(w_f, dtype=np.float64)
         if w_f.shape != (self.k, self.c, self.p, self.p):
             raise _lib.ShapeError(f"weights {w_f.shape} do not match layer "
@@ -153,10 +153,10 @@ class WinogradLayer:
         if dense is None:
             kept = (np.abs(w_f) > zero_tol) | ((zero_tol == 0.0) & (w_f != 0.0))
             dense = bool(kept.all())
-        mode = ({"tc": 2, "tc-fast": 3, "exact": 1}.get(dense, None) if isinstance(dense, str)
+        mode = ({"tc": 2, "exact": 1}.get(dense, None) if isinstance(dense, str)
                 else (2 if dense else 0))
         if mode is None:
-            raise _lib.InvalidArgument(f"dense must be None, bool, 'tc', 'tc-fast' or 'exact', got {dense!r}")
+            raise _lib.InvalidArgument(f"dense must be None, bool, 'tc' or 'exact', got {dense!r}")
         check(lib().wino_set_weights(self._h, w_f.ctypes.data_as(_lib._pd), zero_tol, mode))
 
     def set_weights_csr(self, csr: PointwiseCsr):
@@ -201,16 +201,15 @@ class WinogradLayer:
                             [val[offs[s]:offs[s + 1]].copy() for s in range(n)])
 
     def set_dw_mode(self, mode: str):
-        """'sddmm' (default: exact products of the fp32 operands), 'tc' (tensor-core GEMM + mask
-        gather), 'precise' (operands carried as fp32 hi+lo pairs: the reference's f64 dW_F) or
-        'int8' (exact products on the int8 tensor cores from base-2^7 digit splits + mask gather)."""
-        check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE,
-                                    {"sddmm": 0, "tc": 1, "precise": 2, "int8": 3}[mode]))
+        """dW_F has one mode, 'exact': Ĩ_F and dZ recomputed in f64 from I and dO, split into five
+        int8 digits and multiplied exactly on the int8 tensor cores (the reference's f64 dW_F
+        within ~2^-35 of Σ|products|).  Any other name raises InvalidArgument."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_DW_MODE, {"exact": 0}.get(mode, -1)))
 
     def set_contraction(self, mode: str):
         """Sparse plan contractions: 'csr' (default; the reference's order, forward bitwise equal
         to sparse_forward<float>), 'tc' (3xTF32 tcgen05 GEMM over the zero-filled W_F slices) or
-        'auto' (tensor cores, dW included, at density >= set_auto_density's value, else 'csr')."""
+        'auto' (tensor cores at density >= set_auto_density's value, else 'csr')."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1, "auto": 2}[mode]))
 
     def set_auto_density(self, density: float):

@@ -222,14 +222,6 @@ def _f64_batched(img, w_f, go, pad, m=4):
     return ot, dw, di[:, :, pad:pad + h, pad:pad + w]
 
 
-def _floor_dw(img, go, csr, pad=1, m=4):
-    """dW_F as an exact f64 dot product of the fp32 operands the kernels store (Ĩ_F, dZ in the
-    reference's fp32 association order) — the accuracy floor of any fp32-storage dW_F."""
-    v, g = wo.input_transform_f32(img, m, pad)
-    dz = wo.grad_z_f32(go, g, m)
-    return np.concatenate(wo.sddmm_f64(csr, dz, v))
-
-
 def test_c1_full_batch_parity():
     """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%).
 
@@ -256,37 +248,6 @@ def test_c1_full_batch_parity():
     assert not np.any(got_bad & ~floor_bad), "dW_F misses the tolerance where the fp32 floor does not"
     assert got_bad.mean() <= 1e-4, f"strict-tolerance misses {got_bad.mean():.2e}"
     # and bitwise against the f32 mirror (reference association order) for the forward
-    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
-    assert np.array_equal(r["o"], mir["o"])
-
-
-@pytest.mark.parametrize("name", LAYER_CASES)
-def test_precise_dw_mode_golden(name):
-    """WINO_OPT_DW_MODE=2: dW_F within the strict tolerance of the reference's f64 layer on
-    every element; O and dI unchanged (bitwise) by the mode."""
-    d = load_layer(name)
-    base = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False)
-    r = run_layer(d["img"], d["w_f"], d["grad_o"], d["m"], d["pad"], dense=False, dw_mode="precise")
-    assert np.array_equal(r["o"], base["o"]) and np.array_equal(r["di"], base["di"])
-    mask = d["w_f"] != 0
-    assert fail_fraction(r["dw"][mask], d["grad_wf_f64"][mask]) == 0.0
-    # far below the tolerance: the residual pairs carry the f64 operands to ~2^-48
-    err = np.abs(r["dw"][mask] - d["grad_wf_f64"][mask])
-    assert np.all(err <= 1e-6 * (1.0 + np.abs(d["grad_wf_f64"][mask])))
-
-
-def test_c1_precise_dw_strict_everywhere():
-    """configs[1] at full size in the precise dW mode: zero strict-tolerance misses (the fp32
-    floor of the default mode misses 19/353,647), and the fp32 forward path is unchanged."""
-    cfg = CONFIGS["c1"]
-    img, w_f, go = make_inputs(cfg)
-    r = run_layer(img, w_f, go, 4, 1, dense=False, dw_mode="precise")
-    o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
-    assert_parity(r["o"], o, "c1 O")
-    assert_parity(r["di"], di, "c1 dI")
-    mask = w_f != 0
-    bad = np.abs(r["dw"][mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
-    assert int(bad.sum()) == 0, f"{int(bad.sum())} strict misses"
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(r["o"], mir["o"])
 
@@ -531,32 +492,6 @@ def test_runtime_and_builtin_coefficient_kernels_agree_bitwise(name, monkeypatch
         assert np.array_equal(a[key], b[key]), key
 
 
-def test_c1_tensor_core_dw_mode():
-    """dW_F on the tensor cores (accurate 3xTF32 GEMM over all K×C + mask gather) at configs[1]:
-    compared with the f64 reference and with the exact-product SDDMM."""
-    cfg = CONFIGS["c1"]
-    img, w_f, go = make_inputs(cfg)
-    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
-    layer.set_weights(w_f, dense=False)
-    cache = layer.new_cache(cfg.n)
-    layer.forward(dev(img), cache)
-    exact = layer.backward_weights(dev(go), cache).cpu().numpy().astype(np.float64)
-    layer.set_dw_mode("tc")
-    fast = layer.backward_weights(dev(go), cache).cpu().numpy().astype(np.float64)
-    _, dw, _ = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
-    mask = w_f != 0
-    ref_ = dw[mask]
-    got_tc = layer.compact_to_dense(fast)[mask]
-    got_ex = layer.compact_to_dense(exact)[mask]
-    miss_tc, miss_ex = fail_fraction(got_tc, ref_), fail_fraction(got_ex, ref_)
-    norm_tc = np.abs(got_tc - ref_).max() / np.abs(ref_).max()
-    print(f"c1 dW: tensor-core miss {miss_tc:.2e} (norm {norm_tc:.1e}); SDDMM miss {miss_ex:.2e}")
-    assert norm_tc < 1e-6
-    # 3xTF32 products (~2e-7 of Σ|dz·x|) miss the strict bound on a few times more near-zero
-    # entries than the exact-product SDDMM (measured 3.4e-4 vs 5.4e-5): an opt-in trade-off
-    assert miss_tc < 1e-3
-
-
 def test_host_step_pipeline_matches_device_path():
     """HostStep (pinned host buffers, overlapped copies, graphed passes) returns exactly what
     the device-resident calls return."""
@@ -668,28 +603,6 @@ def test_auto_contraction_follows_density():
     assert np.array_equal(o2, mir["o"])
 
 
-def test_c1_int8_dw_mode_matches_exact_sddmm():
-    """dW_F on the int8 tensor cores (WINO_OPT_DW_MODE 3: base-2^7 digit split with a shared
-    exponent per 128-long block, exact int32 digit-pair products, fp64 block sums) against the
-    exact-product SDDMM at configs[1]: the same dot products of the stored fp32 operands, so every
-    entry is within the strict bound of the SDDMM (measured: 98.5% bitwise equal, the rest one fp32
-    rounding apart) and masked coordinates are never written."""
-    cfg = CONFIGS["c1"]
-    img, w_f, go = make_inputs(cfg)
-    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
-    layer.set_weights(w_f, dense=False)
-    cache = layer.new_cache(cfg.n)
-    layer.forward(dev(img), cache)
-    exact = layer.backward_weights(dev(go), cache).cpu().numpy().astype(np.float64)
-    layer.set_dw_mode("int8")
-    got = layer.backward_weights(dev(go), cache).cpu().numpy().astype(np.float64)
-    assert_parity(got, exact, "c1 dW_F int8 tensor cores vs exact SDDMM")
-    assert (got == exact).mean() > 0.9
-    layer.set_dw_mode("sddmm")
-    again = layer.backward_weights(dev(go), cache).cpu().numpy()
-    assert np.array_equal(again, exact.astype(np.float32))
-
-
 @pytest.mark.parametrize("mode", ["csr", "tc", "dense", "int8"])
 def test_forward_backward_equals_two_calls(mode):
     """wino_forward_backward (dI chain and dW_F overlapping the forward) is bitwise forward +
@@ -769,23 +682,6 @@ def test_c2_shape_forward_bitwise(tmem, monkeypatch):
     o = layer.forward(dev(img)).cpu().numpy()
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(o, mir["o"])
-
-
-def test_tmem_spmm_bitwise_equals_shared_memory_spmm(monkeypatch):
-    """configs[1] forward + backward with the tensor-memory SpMM (WINO_SPMM_TMEM=1: 2 passes for
-    the forward's 256 X rows, 3 for dĨ_F's 384) is bitwise the default shared-memory SpMM."""
-    cfg = CONFIGS["c1"]
-    img, w_f, go = make_inputs(cfg)
-    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
-    layer.set_weights(w_f, dense=False)
-    x, g = dev(img), dev(go)
-    ref = layer.forward_backward(x, g, layer.new_cache(cfg.n))
-    torch.cuda.synchronize()
-    monkeypatch.setenv("WINO_SPMM_TMEM", "1")
-    got = layer.forward_backward(x, g, layer.new_cache(cfg.n))
-    torch.cuda.synchronize()
-    for a, b, what in zip(ref, got, ("O", "dW_F", "dI")):
-        assert torch.equal(a, b), what
 
 
 @pytest.mark.parametrize("name", LAYER_CASES)
