@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """Benchmark of the Winograd-layer fwd+bwd hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--sparsity S]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--sparsity S]
     python bench.py --impl reference ...      # the reference's own CPU path on the host cores
 
-A step = forward (with ForwardCache) + backward_weights + backward_input of one layer over
-one batch of the config (configs[1] by default: N=32, C=256, K=384, H=W=13, F(4x4,3x3),
-pad 1, 90% W_F sparsity), inputs resident in HBM.  With N>1 GPUs (torchrun) every rank runs
-its own batch (weak scaling: batch sharding) and dW_F (nnz-compact) is all-reduced over NCCL
-inside the step.  Effective GFLOP/s follows the reference convention
-(tools/wino.cpp:362, perfmodel.cpp:6-9): 2·C·K·H²·9 per image and pass, 3 passes.
+A step = forward (with ForwardCache) + backward (dW_F and dI) of one layer over one batch of the
+config, inputs resident in HBM.  Default workload: configs[3] at 90% W_F sparsity (N=64,
+C=K=256, H=W=56, F(4x4,3x3), pad 1) — the metric's own sweep config; the line's "sweep" key
+carries the metric's sweep (c3 fwd+bwd at 0/50/80/90/95%, CSR and 'auto' contraction, c2 fwd at
+80/90/95%, c1) with each point's dominant kernel and its roofline fraction.  With N>1 GPUs every
+rank runs its own batch (weak scaling: batch sharding) and dW_F (nnz-compact) is all-reduced over
+NCCL inside the step; `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run.  Effective GFLOP/s follows the reference convention (tools/wino.cpp:362,
+perfmodel.cpp:6-9): 2·C·K·H²·9 per image and pass, 3 passes.
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
 launching stream, with a 256 MB write between steps (outside the events) to flush the 126 MB
@@ -49,11 +52,26 @@ def workload_name(cfg, passes):
 
 
 def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written: HBM copy, cuBLAS bf16), and the
+    tcgen05 TF32 / int8 rates measured with cuBLAS on this pool (profiles/r2_tc_peaks.json,
+    tools/measure_tc_peaks.py); int8 falls back to 2× bf16 (B200 dense int8 = 2× bf16), TF32 to
+    bf16 / 2."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+        out = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
+    else:
+        out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+    out["tf32_tflops"], out["tf32_source"] = out["bf16_tflops"] / 2, out["source"] + " bf16/2"
+    out["int8_tops"], out["int8_source"] = out["bf16_tflops"] * 2, out["source"] + " bf16x2"
+    tc = ROOT / "profiles" / "r2_tc_peaks.json"
+    if tc.exists():
+        d = json.loads(tc.read_text())
+        if d.get("tf32_tflops"):
+            out["tf32_tflops"], out["tf32_source"] = d["tf32_tflops"], "measured (cuBLAS tf32, profiles/r2_tc_peaks.json)"
+        if d.get("int8_tops"):
+            out["int8_tops"], out["int8_source"] = d["int8_tops"], "measured (cuBLAS int8, profiles/r2_tc_peaks.json)"
+    return out
 
 
 # -------------------------------------------------------------------------------------
@@ -189,10 +207,13 @@ def capture(step, args):
         return step, f"eager (graph capture failed: {type(e).__name__}: {e})"
 
 
-def kernel_bytes(cfg, layer, n):
-    """Algorithmic HBM bytes per launch of each kernel."""
+def kernel_work(cfg, layer, n):
+    """Algorithmic HBM bytes and tensor-pipe operations per STEP of each kernel
+    kind.  dw_digits: the two digit kernels (I -> Ĩ_F digits, dO -> dZ digits: 5 int8 digits per
+    value); dw_gemm_i8: 15 exact digit-pair MACs per (k, c, column) on tcgen05 kind::i8."""
     g = layer.geometry
     nt = n * g["t"]
+    ntd = -(-nt // 64) * 64
     p2 = g["p"] ** 2
     f = 4
     I = n * cfg.c * cfg.h * cfg.w * f
@@ -202,63 +223,198 @@ def kernel_bytes(cfg, layer, n):
     nnz = layer.nnz
     Wb = 8 * nnz + 4 * p2 * (cfg.k + 1)
     Wt = 8 * nnz + 4 * p2 * (cfg.c + 1)
-    dw = nnz * f
+    dig = 5 * p2 * (cfg.c + cfg.k) * ntd
+    dense_w = 2 * 4 * p2 * cfg.k * cfg.c  # tf32 hi/lo weight operands
     return {
-        "input_transform": I + V, "spmm_fwd": V + Z + Wb, "output_transform": Z + O,
-        "grad_z": O + Z, "sddmm_dw": Z + V + dw + 8 * nnz + 4 * p2 * (cfg.k + 1),
-        "spmm_bwd_data": Z + Wt + V, "input_grad": V + I,
+        "input_transform": {"bytes": I + V}, "spmm_fwd": {"bytes": V + Z + Wb},
+        "output_transform": {"bytes": Z + O}, "grad_z": {"bytes": O + Z},
+        "dw_digits": {"bytes": I + O + dig},
+        "dw_gemm_i8": {"bytes": dig, "ops": 2.0 * 15 * p2 * cfg.k * cfg.c * ntd, "pipe": "int8"},
+        "dw_reduce": {"bytes": 8 * p2 * cfg.k * cfg.c + (nnz * 12 if not layer.is_dense else 4 * nnz)},
+        "spmm_bwd_data": {"bytes": Z + Wt + V}, "input_grad": {"bytes": V + I},
+        "dense_fwd_tc": {"bytes": V + Z + dense_w, "ops": 3 * 2.0 * p2 * cfg.k * cfg.c * nt, "pipe": "tf32"},
+        "dense_dv_tc": {"bytes": V + Z + dense_w, "ops": 3 * 2.0 * p2 * cfg.k * cfg.c * nt, "pipe": "tf32"},
     }
+
+
+def kernel_table(prof, steps, cfg, layer, n, pk):
+    """Per-kind time per step (profiled steps, CUDA events on the launching stream) with its
+    roofline: tensor-pipe kinds against the measured TF32 / int8 rate, the rest against HBM."""
+    work = kernel_work(cfg, layer, n)
+    tot = sum(v[0] for v in prof.values()) or 1.0
+    out = {}
+    for name, (ms_tot, cnt) in prof.items():
+        ms = ms_tot / steps
+        k = {"ms_per_step": ms, "launches_per_step": cnt / steps, "share": ms_tot / tot}
+        w = work.get(name)
+        if w:
+            k["alg_bytes"] = w["bytes"]
+            k["GBps"] = w["bytes"] / (ms * 1e-3) / 1e9
+            if "ops" in w:
+                peak = pk["tf32_tflops"] if w["pipe"] == "tf32" else pk["int8_tops"]
+                ach = w["ops"] / (ms * 1e-3) / 1e12
+                k["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak, "frac": ach / peak,
+                                 "unit": "TFLOP/s" if w["pipe"] == "tf32" else "TOPS",
+                                 "peak_source": pk[w["pipe"] + "_source"],
+                                 "note": ("issued TF32 FLOPs of the 3xTF32 GEMM (useful = 1/3)" if w["pipe"] == "tf32"
+                                          else "issued int8 digit-pair ops (15 pairs per product)")}
+            else:
+                k["roofline"] = {"bound": "hbm", "achieved": k["GBps"], "peak": pk["hbm_gbs"],
+                                 "frac": k["GBps"] / pk["hbm_gbs"], "unit": "GB/s", "peak_source": pk["source"]}
+        out[name] = k
+    return out
+
+
+def dominant_roofline(kernels, traffic_key=None):
+    dom = max(kernels.items(), key=lambda kv: kv[1]["ms_per_step"])[0]
+    r = dict(kernels[dom].get("roofline") or {})
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if traffic_key and tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(f"{traffic_key}:{dom}")
+    r.update({"kernel": dom, "traffic": traffic,
+              "note": "algorithmic bytes (or issued ops) per step of the kind / its CUDA-event time per step "
+                      "(serialised profiled steps, launching stream)"})
+    return r
+
+
+class LayerBench:
+    """One layer configuration on the device: inputs, buffers, and the step variants."""
+
+    def __init__(self, cfg, dev, local_rank, contraction="csr", rank=0, world=1):
+        import torch
+
+        import paper_1702_08597_b200 as wb
+
+        self.cfg, self.dev = cfg, dev
+        n = cfg.n
+        img, w_f, go = make_inputs(cfg)
+        if world > 1:  # every rank draws its own shard of the global batch
+            from paper_1702_08597_b200.synth import Stream
+
+            img = Stream(cfg.seed + 1000 * rank, "shard/I").normal(img.shape).astype(np.float32)
+            go = Stream(cfg.seed + 1000 * rank, "shard/dO").normal(go.shape).astype(np.float32)
+        self.img, self.w_f, self.go = img, w_f, go
+        self.dense = cfg.sparsity == 0.0
+        layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
+        layer.set_weights(w_f, dense="tc" if self.dense else False)
+        if contraction != "csr" and not self.dense:
+            layer.set_contraction(contraction)
+        self.contraction = contraction
+        self.layer = layer
+        self.fwd_only = not cfg.backward
+        self.cache = layer.new_cache(n) if not self.fwd_only else None
+        self.x = torch.from_numpy(img).to(dev)
+        self.g = torch.from_numpy(go).to(dev)
+        self.out = torch.empty((n, cfg.k, layer.ho, layer.wo), device=dev)
+        self.dw = torch.empty(layer.grad_w_shape(), device=dev)
+        self.di = torch.empty((n, cfg.c, cfg.h, cfg.w), device=dev)
+
+    def path(self):
+        if self.dense:
+            return "dense plan: tcgen05 3xTF32 Z/dĨ_F"
+        return {"csr": "csr (reference order)", "tc": "tcgen05 3xTF32 on zero-filled W_F",
+                "auto": "auto (tcgen05 at density >= 8%, else csr)"}[self.contraction]
+
+    def compute(self):  # one call, scheduled by data dependence (wino_forward_backward)
+        if self.fwd_only:
+            self.layer.forward(self.x, None, out=self.out)
+        else:
+            self.layer.forward_backward(self.x, self.g, self.cache, out=self.out, out_w=self.dw, out_i=self.di)
+
+    def serial(self):  # the same kernels one after another (per-kernel attribution)
+        lay = self.layer
+        lay.forward(self.x, self.cache, out=self.out)
+        if not self.fwd_only:
+            lay.backward_weights(self.g, self.cache, out=self.dw)
+            lay.backward_input(self.cache, out=self.di)
+
+    def profile(self, flush, steps=3):
+        import torch
+
+        self.layer.profile(True)
+        for _ in range(steps):
+            flush.zero_()
+            self.serial()
+        torch.cuda.synchronize()
+        prof = self.layer.profile_read()
+        self.layer.profile(False)
+        return prof
+
+    def close(self):
+        self.layer.close()
+
+
+def time_steps(run, flush, steps):
+    import torch
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        run()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def sweep_point(cfg, dev, local_rank, flush, pk, args, contraction="csr"):
+    """One point of the metric's sweep: device-resident step time (CUDA graph, L2 flushed), the
+    serialised per-kernel table and the dominant kernel's roofline."""
+    import torch
+
+    lb = LayerBench(cfg, dev, local_rank, contraction)
+    for _ in range(3):
+        lb.compute()
+    run, _ = capture(lb.compute, args)
+    ms = statistics.median(time_steps(run, flush, args.sweep_steps))
+    kernels = kernel_table(lb.profile(flush), 3, cfg, lb.layer, cfg.n, pk)
+    passes = 1 if lb.fwd_only else 3
+    pt = {"sparsity": cfg.sparsity, "path": lb.path(), "nnz": lb.layer.nnz, "ms": ms,
+          "eff_tflops": passes * flops_per_image(cfg) * cfg.n / (ms * 1e-3) / 1e12,
+          "dominant": dominant_roofline(kernels, f"{cfg.name}:{cfg.sparsity}"),
+          "kernels": {k: {"ms": v["ms_per_step"], "frac": (v.get("roofline") or {}).get("frac"),
+                          "bound": (v.get("roofline") or {}).get("bound")} for k, v in kernels.items()}}
+    lb.close()
+    del lb, run
+    torch.cuda.empty_cache()
+    return pt
+
+
+def run_sweep(args, dev, local_rank, flush, pk):
+    """BASELINE metric: 'fwd+bwd effective GFLOP/s and ms/layer vs W_F sparsity, % roofline' —
+    configs[3] at 0/50/80/90/95% (CSR; and the 'auto' contraction where it differs), configs[2]
+    forward at 80/90/95%, configs[1]."""
+    sw = {"c3": [], "c3_auto": [], "c2_fwd": [], "c1": None}
+    for s in (0.0, 0.5, 0.8, 0.9, 0.95):
+        sw["c3"].append(sweep_point(with_sparsity(CONFIGS["c3"], s), dev, local_rank, flush, pk, args))
+        print(f"# sweep c3 {s:.2f}: {sw['c3'][-1]['ms']:.3f} ms", file=sys.stderr, flush=True)
+    for s in (0.5, 0.8, 0.9):
+        sw["c3_auto"].append(sweep_point(with_sparsity(CONFIGS["c3"], s), dev, local_rank, flush, pk, args, "auto"))
+    for s in (0.8, 0.9, 0.95):
+        sw["c2_fwd"].append(sweep_point(with_sparsity(CONFIGS["c2"], s), dev, local_rank, flush, pk, args))
+    sw["c1"] = sweep_point(CONFIGS["c1"], dev, local_rank, flush, pk, args)
+    return sw
 
 
 def run_gpu(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    import paper_1702_08597_b200 as wb
-
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     n = cfg.n
-    img, w_f, go = make_inputs(cfg)
-    if world > 1:  # every rank draws its own shard of the global batch
-        from paper_1702_08597_b200.synth import Stream
-
-        img = Stream(cfg.seed + 1000 * rank, "shard/I").normal(img.shape).astype(np.float32)
-        go = Stream(cfg.seed + 1000 * rank, "shard/dO").normal(go.shape).astype(np.float32)
-    layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=cfg.pad, m=cfg.m, device=local_rank)
-    dense = cfg.sparsity == 0.0
-    layer.set_weights(w_f, dense=(args.dense or "tc") if dense else False)
-    if args.dw == "tc" and not dense:
-        layer.set_dw_mode("tc")
-    elif args.dw == "precise":
-        layer.set_dw_mode("precise")
-    elif args.dw == "int8" and not dense:
-        layer.set_dw_mode("int8")
-    if args.contraction != "csr" and not dense:
-        layer.set_contraction(args.contraction)
-    cache = layer.new_cache(n)
-    x = torch.from_numpy(img).to(dev)
-    g_o = torch.from_numpy(go).to(dev)
-    out = torch.empty((n, cfg.k, layer.ho, layer.wo), device=dev)
-    dw = torch.empty(layer.grad_w_shape(), device=dev)
-    di = torch.empty((n, cfg.c, cfg.h, cfg.w), device=dev)
+    lb = LayerBench(cfg, dev, local_rank, args.contraction, rank, world)
+    layer, dw = lb.layer, lb.dw
+    img, w_f, go = lb.img, lb.w_f, lb.go
+    dense, fwd_only = lb.dense, lb.fwd_only
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
-
-    fwd_only = not cfg.backward  # c2: the reference's sparse inference pass
-
-    def compute():
-        layer.forward(x, cache, out=out)
-        if fwd_only:
-            return
-        if args.separate_bwd:
-            layer.backward_weights(g_o, cache, out=dw)
-            layer.backward_input(cache, out=di)
-        else:  # dW_F concurrently with dI (wino_backward)
-            layer.backward(g_o, cache, out_w=dw, out_i=di)
-
-    if not fwd_only and not args.separate_bwd and not args.call_order:
-        def compute():  # one call, scheduled by data dependence (wino_forward_backward)
-            layer.forward_backward(x, g_o, cache, out=out, out_w=dw, out_i=di)
+    if args.call_order and not fwd_only:
+        def compute():
+            layer.forward(lb.x, lb.cache, out=lb.out)
+            layer.backward(lb.g, lb.cache, out_w=lb.dw, out_i=lb.di)
+    else:
+        compute = lb.compute
 
     def step():
         compute()
@@ -284,40 +440,18 @@ def run_gpu(args, cfg, rank, world, local_rank):
         run = run_c
     if world > 1:
         dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     sampler = ClockSampler(local_rank)
     sampler.start()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    for a, b in ev:
-        flush.zero_()
-        a.record()
-        run()
-        b.record()
-    torch.cuda.synchronize()
+    times = time_steps(run, flush, args.steps)
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     launches = per_step_launches * args.steps
-    # per-kernel times for the roofline: eager steps with CUDA events around every launch, the
-    # backward serialised (in the timed step dW_F runs concurrently with dI, which would blur the
-    # attribution of time to kernels)
-    def step_serial():
-        layer.forward(x, cache, out=out)
-        if not fwd_only:
-            layer.backward_weights(g_o, cache, out=dw)
-            layer.backward_input(cache, out=di)
-
-    layer.profile(True)
-    for _ in range(3):
-        flush.zero_()
-        step_serial()
-    torch.cuda.synchronize()
-    prof = layer.profile_read()
-    layer.profile(False)
-    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    prof = lb.profile(flush)
+    ms = sum(times) / args.steps
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -340,6 +474,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     value = world * flops_step / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers (pinned) ----
+    x, g_o, out, di = lb.x, lb.g, lb.out, lb.di
     h_img = torch.from_numpy(img).pin_memory()
     h_go = torch.from_numpy(go).pin_memory()
     h_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
@@ -352,13 +487,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
             run()
             h_out.copy_(out, non_blocking=True)
         e2e_mode = "serial copies + forward"
-    elif world == 1 and not dense and args.contraction == "csr" and args.dw == "sddmm" and not args.no_pipeline:
+    elif world == 1 and not dense and args.contraction == "csr" and not args.no_pipeline:
         # public API: image chunks so every copy overlaps compute (paper_1702_08597_b200/pipeline.py)
+        from paper_1702_08597_b200.graph import GraphedStep
         from paper_1702_08597_b200.pipeline import PipelinedHostStep
 
-        ps = PipelinedHostStep(layer, cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
-        from paper_1702_08597_b200.graph import GraphedStep
-
+        ps = PipelinedHostStep(layer, lb.cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
         # the whole pipelined step (copies on 3 streams + range kernels) as one CUDA graph
         e2e_step = GraphedStep(lambda: ps(h_img, h_go, h_out, h_dw, h_di)).replay
         e2e_mode = (f"PipelinedHostStep in one CUDA graph: pinned host buffers, {len(ps.bounds)} image chunks, "
@@ -368,7 +502,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         # with the backward (paper_1702_08597_b200/pipeline.py)
         from paper_1702_08597_b200.pipeline import HostStep
 
-        hs = HostStep(layer, cache, x, g_o, out, dw, di)
+        hs = HostStep(layer, lb.cache, x, g_o, out, dw, di)
 
         def e2e_step():
             hs(h_img, h_go, h_out, h_dw, h_di)
@@ -386,100 +520,32 @@ def run_gpu(args, cfg, rank, world, local_rank):
     for _ in range(max(1, args.warmup)):
         e2e_step()
     torch.cuda.synchronize()
-    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for a, b in ev2:
-        flush.zero_()
-        a.record()
-        e2e_step()
-        b.record()
-    torch.cuda.synchronize()
-    ms_e2e = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
+    ms_e2e = sum(time_steps(e2e_step, flush, args.steps)) / args.steps
     t2 = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = world * flops_step / (float(t2.item()) * 1e-3) / 1e9
     h2d = h_img.numel() * 4 + (0 if fwd_only else h_go.numel() * 4)
     d2h = (h_out.numel() + (0 if fwd_only else h_dw.numel() + h_di.numel())) * 4
+    del h_img, h_go, h_out, h_dw, h_di
 
     if rank != 0:
         return
     pk = peaks()
-    kb = kernel_bytes(cfg, layer, n)
-    kernels = {}
-    # a kind can launch more than once per step (SDDMM + its split_sum, the dW GEMM + its fp64
-    # reduce): times and achieved bandwidth are per STEP of the kind (3 profiled steps), i.e. the
-    # algorithmic bytes of one pass over the kernel's data ÷ all of that pass's launches
-    for name, (tot_ms, cnt) in prof.items():
-        avg = tot_ms / 3
-        bytes_ = kb.get(name)
-        kernels[name] = {"ms_per_step": avg, "launches_per_step": cnt / 3,
-                         "share": tot_ms / sum(v[0] for v in prof.values())}
-        if bytes_:
-            kernels[name]["alg_bytes"] = bytes_
-            kernels[name]["GBps"] = bytes_ / (avg * 1e-3) / 1e9
-    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
-    traffic = None
-    tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(f"{cfg.name}:{cfg.sparsity}:{dom}")
-    if dom.startswith("dense_"):
-        # tensor-pipe roofline: 3xTF32 issues 3 TF32 products per useful MAC; TF32 dense peak is
-        # taken as half the measured bf16 GEMM peak (MEASURED_PEAKS.json)
-        g = layer.geometry
-        useful = 2.0 * (g["p"] ** 2) * cfg.k * cfg.c * n * g["t"]
-        avg_s = prof[dom][0] / 3 * 1e-3
-        issued_tf = 3 * useful / avg_s / 1e12
-        peak_tf = pk["bf16_tflops"] / 2
-        roofline = {"bound": "tensor", "kernel": dom, "achieved": issued_tf, "peak": peak_tf,
-                    "unit": "TFLOP/s", "frac": issued_tf / peak_tf, "traffic": traffic,
-                    "peak_source": pk["source"] + " (bf16/2 for tf32)",
-                    "note": "issued TF32 FLOP/s of the 3xTF32 GEMM (useful = 1/3); time = the kind's launches per step"}
-    else:
-        dom_gbs = kernels[dom].get("GBps")
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": pk["hbm_gbs"],
-                    "unit": "GB/s", "frac": (dom_gbs / pk["hbm_gbs"]) if dom_gbs else None,
-                    "traffic": traffic, "peak_source": pk["source"],
-                    "note": ("algorithmic bytes per step / CUDA-event time of the kind's launches in the step (on the launching stream); "
-                             "c1's per-kernel working set (<64 MB) is L2-resident within a step")}
-    # the on-chip pipe that bounds the CSR contraction kernels: the SDDMM converts
-    # one fp32 operand to fp64 per exact product on the XU pipe (16 lanes/clk/SM); the SpMMs read
-    # one 4-byte Ĩ_F/dZ operand per product from shared memory (128 B/clk/SM = 32 products/clk/SM)
-    pipe_roofline = None
-    g_ = layer.geometry
-    products = float(layer.nnz) * n * g_["t"]
-    clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
-    pipes = {"sddmm_dw": ("XU: F2F.F64.F32, one per exact product", 16.0),
-             "spmm_fwd": ("shared-memory pipe: 4 B per product", 32.0),
-             "spmm_bwd_data": ("shared-memory pipe: 4 B per product", 32.0)}
-    if dom in pipes and not dense:
-        name_, peak_ = pipes[dom]
-        # sddmm_dw's two launches per step (SDDMM + split_sum) are both counted: a lower bound
-        t_dom = prof[dom][0] / 3 * 1e-3
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ach = products / t_dom / sms / clk
-        pipe_roofline = {"kernel": dom, "pipe": name_, "unit": "products/clk/SM", "achieved": ach,
-                         "peak": peak_, "frac": ach / peak_,
-                         "note": "products = nnz·N·T per launch; time from the same CUDA events"}
+    kernels = kernel_table(prof, 3, cfg, layer, n, pk)
+    roofline = dominant_roofline(kernels, f"{cfg.name}:{cfg.sparsity}")
     line = {
         "metric": METRIC_FWD if fwd_only else METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
         "config": {"workload": workload_name(cfg, "fwd" if fwd_only else "fwd+bwd"), "global_batch": n * world,
-                   "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz,
-                   "path": ({"tc": "dense-tcgen05-3xtf32-fp64fold", "tc-fast": "dense-tcgen05-3xtf32-fast",
-                             "exact": "dense-exact-simt"}[args.dense or "tc"]) if dense else
-                           {"csr": "csr", "tc": "tcgen05-3xtf32-fp64fold on zero-filled W_F",
-                            "auto": "auto (tensor cores at density >= 8%, else csr)"}[args.contraction],
-                   "dw": {"sddmm": "masked-sddmm-exact", "tc": "tcgen05-3xtf32-fp64fold+mask-gather",
-                          "precise": "masked-sddmm-exact on fp32 hi+lo operands",
-                          "int8": "int8-tcgen05-exact-digit-products+mask-gather"}[args.dw],
-                   "l2_flush": "256 MB write between timed steps",
+                   "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz, "path": lb.path(),
+                   "dw": "exact: f64 digit kernels + int8 tcgen05 digit-pair GEMM (strict vs the f64 reference)",
+                   "l2_flush": "256 MB write between timed steps (inputs also exceed L2 at c2/c3)",
                    "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
         "ms_per_layer": ms_max,
         "roofline": roofline,
-        "pipe_roofline": pipe_roofline,
         "kernels": kernels,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item()), "mode": e2e_mode},
@@ -512,8 +578,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
         t, kind = cpu_fwd_bwd(cfg, img, w_f, go, n_img, threads)
         line["cpu_baseline"] = {"value": 3 * flops_per_image(cfg) * n_img / t / 1e9, "unit": "GFLOP/s",
                                 "cores": threads, "kind": kind,
-                                "sample": f"{n_img} of {cfg.n} images (one step's worth per thread) "
-                                          "through the reference's dense f64 fwd+bwd API"}
+                                "sample": f"{n_img} of {cfg.n} images (one per host thread) through the "
+                                          "reference's dense f64 per-image fwd+bwd API"}
+    lb.close()
+    del lb
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_sweep:
+        line["sweep"] = run_sweep(args, dev, local_rank, flush, pk)
     print(json.dumps(line), flush=True)
 
 
@@ -670,38 +741,81 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: re-launch this script as N ranks under
+    torch.distributed.run on 127.0.0.1 — the same command line the driver uses."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    print(f"# spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def run_dry(args, cfg, rank, world):
+    """--dry-run: the multi-rank plumbing of the GPU arm on CPU (gloo): every rank holds the
+    nnz-compact dW_F of the config, the step's one exchange (a sum all-reduce) runs, rank 0
+    checks the sum and prints one JSON line.  Exercised by tests/test_bench_cpu.py."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_08597_b200.dist import shard
+
+    _, w_f, _ = make_inputs(cfg, n=1)
+    nnz = int(np.count_nonzero(w_f))
+    dw = torch.full((nnz,), float(rank + 1))
+    if world > 1:
+        dist.all_reduce(dw)
+    want = world * (world + 1) / 2
+    ok = bool(torch.all(dw == want))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "backend": dist.get_backend() if world > 1 else None,
+                          "allreduce_ok": ok, "nnz": nnz, "shards": [shard(cfg.n * world, r, world) for r in range(world)]}),
+              flush=True)
+    if not ok:
+        raise SystemExit("all-reduce sum mismatch")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the metric's sparsity sweep (the 'sweep' key)")
+    ap.add_argument("--sweep-steps", type=int, default=10, help="timed steps per sweep point")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e through HostStep (whole-batch calls)")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
     ap.add_argument("--call-order", action="store_true",
                     help="forward then backward as two calls (default: one wino_forward_backward call "
                          "scheduled by data dependence)")
-    ap.add_argument("--separate-bwd", action="store_true",
-                    help="backward_weights then backward_input instead of the concurrent wino_backward")
     ap.add_argument("--contraction", default="csr", choices=["csr", "tc", "auto"],
                     help="sparse plan: CSR kernels (bitwise reference order) or tcgen05 on zero-filled W_F")
-    ap.add_argument("--dw", default="sddmm", choices=["sddmm", "tc", "precise", "int8"],
-                    help="sparse dW_F: exact masked SDDMM (default) or tensor-core GEMM + mask gather")
-    ap.add_argument("--dense", default=None, choices=["tc", "tc-fast", "exact"],
-                    help="dense path at 0%% sparsity: 'tc' (default: 3xTF32 tcgen05, per-k-block fp64 "
-                         "folding), 'tc-fast' (one TMEM chain), 'exact' (reference-order SIMT)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: the rank plumbing and the dW_F all-reduce over gloo (tests)")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" and not args.dry_run else args.warmup
     cfg = CONFIGS[args.config]
     if args.sparsity is not None:
         cfg = with_sparsity(cfg, args.sparsity)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, cfg, rank)
         return
@@ -709,10 +823,17 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dry_run:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if rank == 0:
+                print(f"# NCCL communicator: {dist.get_world_size()} ranks", file=sys.stderr, flush=True)
     try:
-        if args.config == "c4":
+        if args.dry_run:
+            run_dry(args, cfg, rank, world)
+        elif args.config == "c4":
             run_gpu_stack(args, cfg, rank, world, local_rank)
         else:
             run_gpu(args, cfg, rank, world, local_rank)

@@ -10,14 +10,14 @@ the reference's interfaces:
     autograd.WinogradConv2d        -- the same layer as a differentiable torch module
     io, infer_bench                -- WGT1 / checkpoints, the infer-bench CSV driver
 """
-from ._lib import (CapabilityError, ConsistencyError, CorruptFormatError, CudaError, ShapeError,
-                   WinoError)
+from ._lib import (CapabilityError, ConsistencyError, CorruptFormatError, CudaError, InvalidArgument,
+                   ShapeError, WinoError)
 from .api import conv_winograd, conv_winograd_grad, density, gen_transforms, lift, sparse_conv
 from .layer import (ForwardCache, PointwiseCsr, WinogradLayer, compress, make_geometry,
                     reconstruct, transforms)
 
 __all__ = [
-    "CapabilityError", "ConsistencyError", "CorruptFormatError", "CudaError", "ShapeError",
+    "CapabilityError", "ConsistencyError", "CorruptFormatError", "CudaError", "InvalidArgument", "ShapeError",
     "WinoError", "conv_winograd", "conv_winograd_grad", "density", "gen_transforms", "lift",
     "sparse_conv", "ForwardCache", "PointwiseCsr", "WinogradLayer", "compress", "make_geometry",
     "reconstruct", "transforms",

@@ -1176,6 +1176,7 @@ int wino_set_weights(wino_plan* p, const double* w_f, double zero_tol, int dense
 int wino_get_csr(const wino_plan* p, uint64_t* nnz, uint64_t* row_ptr, uint64_t* col_idx, float* values) {
     if (!p || !nnz) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (!p->has_weights) return set_err(WINO_CONSISTENCY_ERROR, "plan holds no CSR weights");
+    CUDA_TRY(cudaSetDevice(p->device));
     const int K = p->K, P2 = p->P2;
     for (int s = 0; s < P2; ++s) nnz[s] = (uint64_t)p->slice_nnz[s];
     if (row_ptr)
@@ -1207,6 +1208,7 @@ int wino_weight_values(wino_plan* p, float** values_dev) {
 int wino_values_updated(wino_plan* p, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
     Launch L(p, st, K_MISC);
     wino::refresh_values_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_cv, p->d_cvT, p->d_vals,
@@ -1611,6 +1613,7 @@ int wino_allreduce_dw(wino_plan* p, void* nccl_comm, float* grad_w, int64_t coun
     if (!nccl_comm || (!grad_w && count != 0)) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (count < 0) count = p->dense ? (int64_t)p->P2 * p->K * p->C : p->nnz;
     if (count == 0) return WINO_OK;
+    CUDA_TRY(cudaSetDevice(p->device));
     std::call_once(g_nccl_once, resolve_nccl);
     if (!g_nccl_allreduce) return set_err(WINO_CAPABILITY_ERROR, "allreduce_dw: libnccl.so.2 not found");
     const int r = g_nccl_allreduce(grad_w, grad_w, (size_t)count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, nccl_comm,
@@ -1623,6 +1626,7 @@ int wino_allreduce_dw(wino_plan* p, void* nccl_comm, float* grad_w, int64_t coun
 int wino_backward_input(wino_plan* p, const wino_cache* c, float* grad_input, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(p->device));
     if (!c) return set_err(WINO_INVALID_ARGUMENT, "null cache");
     if (c->plan != p)
         return set_err(WINO_CONSISTENCY_ERROR, "forward cache does not match the given geometry");
@@ -1638,6 +1642,7 @@ int wino_update_weights(wino_plan* p, const float* grad_w, const wino_update* u,
     if (!grad_w || !u) return set_err(WINO_INVALID_ARGUMENT, "null argument");
     if (u->norm != 1 && u->norm != 2) return set_err(WINO_INVALID_ARGUMENT, "norm must be 1 or 2");
     if (p->nnz == 0) return WINO_OK;
+    CUDA_TRY(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
     wino::UpdateParams up{u->lr, u->scale, u->lambda, u->eps, u->beta, u->norm, u->prune};
     if (u->norm == 2 && u->lambda != 0.0) {  // ‖w‖₂ of the layer before the step (train.cpp:264)
@@ -1665,6 +1670,7 @@ int wino_sgd_step(wino_plan* p, const float* grad_w, float lr, float scale, floa
 
 int wino_update_status(wino_plan* p, int64_t* nonfinite) {
     if (!p || !nonfinite) return set_err(WINO_INVALID_ARGUMENT, "null argument");
+    CUDA_TRY(cudaSetDevice(p->device));
     unsigned long long n = 0;
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpy(&n, p->d_nonfinite, sizeof(n), cudaMemcpyDeviceToHost));
@@ -1693,6 +1699,7 @@ int wino_recompress(wino_plan* p, double zero_tol) {
 
 int wino_set_option(wino_plan* p, int option, int value) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    CUDA_TRY(cudaSetDevice(p->device));
     if (option == WINO_OPT_CONTRACTION) {
         if (value < 0 || value > 2) return set_err(WINO_INVALID_ARGUMENT, "contraction must be 0, 1 or 2");
         if (value == 1 && (p->C % 4 || p->K % 4))

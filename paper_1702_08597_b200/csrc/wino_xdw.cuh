@@ -139,7 +139,7 @@ __device__ __forceinline__ void store_digit_groups(const uint32_t* slo, const ui
 // digit columns [col0, col0 + ncols_pad).  Block = 256 consecutive (c, column) items; the f64
 // transform is the reference's (layer.cpp:55-59 with f64 TransformSet values).
 template <int M, int P, class CF>
-__global__ void __launch_bounds__(kTileItems)
+__global__ void __launch_bounds__(kTileItems, (P <= 6) ? 2 : 1)
 input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int* __restrict__ Eout,
                     const unsigned* __restrict__ amax, const CoefsD cf, const Norms nrm, int C, int H, int W,
                     int pad, int tiles_x, int T, int ncols, int ncols_pad, int64_t NTd, int64_t plane, int col0) {
@@ -175,23 +175,22 @@ input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int*
             for (int k = 0; k < P; ++k) d[i][k] = 0.f;
     }
     const double amx = valid ? (double)__uint_as_float(__ldg(amax + c)) : 0.0;
-    double tmp[P][P];
+    // row i of B1ᵀ·d first (P doubles live), then its P outputs: keeps the f64 working set small
 #pragma unroll
-    for (int i = 0; i < P; ++i)
+    for (int i = 0; i < P; ++i) {
+        double tmp[P];
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cf, k * P + i), (double)d[k][l]);
-            tmp[i][l] = acc;
+            tmp[l] = acc;
         }
-#pragma unroll
-    for (int i = 0; i < P; ++i)
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cf, k * P + l), tmp[i][k]);
+            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cf, k * P + l), tmp[k]);
             const int s = i * P + l;
             const int E = bound_exp(nrm.v[s] * amx);
             uint32_t lo, hi;
@@ -200,6 +199,7 @@ input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int*
             shi[s * kTileItems + threadIdx.x] = (uint8_t)hi;
             if (valid && j == 0) Eout[s * C + c] = E;
         }
+    }
     __syncthreads();
     store_digit_groups(slo, shi, P2, C, ncols_pad, items, dig, NTd, plane, col0);
 }
@@ -207,7 +207,7 @@ input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int*
 // dZ digits of one segment from dO (ψ⁻¹ gather, zero at padded positions, optional ReLU mask):
 // dZ = A1·dÕ·A2ᵀ in f64 (layer.cpp:107-116).
 template <int M, int P, bool MASK, class CF>
-__global__ void __launch_bounds__(kTileItems)
+__global__ void __launch_bounds__(kTileItems, (P <= 6) ? 2 : 1)
 grad_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out, int8_t* __restrict__ dig,
                    int* __restrict__ Eout, const unsigned* __restrict__ amax, const CoefsD cf, const Norms nrm,
                    int K, int Ho, int Wo, int tiles_x, int T, int ncols, int ncols_pad, int64_t NTd, int64_t plane,
@@ -246,23 +246,21 @@ grad_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_
         }
     }
     const double amx = valid ? (double)__uint_as_float(__ldg(amax + k)) : 0.0;
-    double m1[P][M];
 #pragma unroll
-    for (int i = 0; i < P; ++i)
+    for (int i = 0; i < P; ++i) {
+        double m1[M];  // row i of A1·dÕ
 #pragma unroll
         for (int x = 0; x < M; ++x) {
             double acc = 0.0;
 #pragma unroll
             for (int y = 0; y < M; ++y) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cf, i * M + y), (double)d[y][x]);
-            m1[i][x] = acc;
+            m1[x] = acc;
         }
-#pragma unroll
-    for (int i = 0; i < P; ++i)
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
-            for (int x = 0; x < M; ++x) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cf, l * M + x), m1[i][x]);
+            for (int x = 0; x < M; ++x) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cf, l * M + x), m1[x]);
             const int s = i * P + l;
             const int E = bound_exp(nrm.v[s] * amx);
             uint32_t lo, hi;
@@ -271,6 +269,7 @@ grad_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_
             shi[s * kTileItems + threadIdx.x] = (uint8_t)hi;
             if (valid && j == 0) Eout[s * K + k] = E;
         }
+    }
     __syncthreads();
     store_digit_groups(slo, shi, P2, K, ncols_pad, items, dig, NTd, plane, col0);
 }

@@ -6,8 +6,12 @@
 //   winograd_forward / _backward_weights / _backward_input : a dense plan in the exact
 //       (reference-order SIMT) mode; f64 host tensors are cast to fp32 at the edge, as the
 //       reference's own f32 path casts them (sparse.cpp:99-100, 181)
-//   sparse_forward<float>  : a CSR plan from the caller's PointwiseCsr (validated), batched
+//   sparse_forward<float>, sparse_forward<double> : a CSR plan from the caller's PointwiseCsr
+//       (validated), batched; the B200 computes in fp32 (f64 values cast at the edge)
 //   lift_spatial_weights   : G1·W·G2ᵀ on the host (tiny)
+//   OpCounter              : filled analytically, as the reference counts — K·C·T·p·q
+//       multiplications and additions per winograd_forward (layer.cpp:72-77), nnz·T per slice and
+//       image in sparse_forward (sparse.cpp:65-68, merged over workers at :247-251)
 //
 // ForwardCache has no field for device state, so the shim keeps the device plan + cache of each
 // ForwardCache in a side table keyed by its address (a cache is never shared across threads,
@@ -140,7 +144,7 @@ Tensor lift_spatial_weights(const Tensor& w, const TransformSet& tset) {
 }
 
 Tensor winograd_forward(const Tensor& img, const Tensor& w_f, const TransformSet& tset, const TileGeometry& geom,
-                        ForwardCache* cache, OpCounter* /*counter*/) {
+                        ForwardCache* cache, OpCounter* counter) {
     ++shim_gpu_calls;
     if (w_f.rank() != 4 || w_f.extent(2) != tset.p || w_f.extent(3) != tset.q)
         throw ShapeError("winograd_forward: weights " + shape_str(w_f.shape()) +
@@ -160,6 +164,11 @@ Tensor winograd_forward(const Tensor& img, const Tensor& w_f, const TransformSet
     check(wino_forward(dc->plan->plan, 1, in.p, out.p, dc->cache, 0, nullptr));
     Tensor o({kn, geom.h_o, geom.w_o});
     out.download(o.data());
+    if (counter) {  // layer.cpp:72-77
+        const std::uint64_t n = static_cast<std::uint64_t>(kn) * geom.c * geom.t * geom.p * geom.q;
+        counter->multiplications += n;
+        counter->additions += n;
+    }
     if (cache) {
         cache->k = kn;
         cache->c = geom.c;
@@ -210,10 +219,10 @@ Tensor winograd_backward_input(const ForwardCache& cache, const Tensor& w_f, con
     return gi;
 }
 
-// Explicit specialization: overrides the template instantiation sparse.cpp emits for float.
-template <>
-Tensor sparse_forward<float>(const Tensor& batch, const PointwiseCsr<float>& csr, const TransformSet& tset,
-                             const TileGeometry& geom, unsigned /*workers*/, OpCounter* /*counter*/) {
+namespace {
+template <typename T>
+Tensor sparse_forward_gpu(const Tensor& batch, const PointwiseCsr<T>& csr, const TransformSet& tset,
+                          const TileGeometry& geom, OpCounter* counter) {
     ++shim_gpu_calls;
     if (batch.rank() != 4 || batch.extent(1) != geom.c || batch.extent(2) != geom.h_i || batch.extent(3) != geom.w_i)
         throw ShapeError("sparse_forward: batch " + shape_str(batch.shape()) + " does not match the geometry");
@@ -223,18 +232,22 @@ Tensor sparse_forward<float>(const Tensor& batch, const PointwiseCsr<float>& csr
     auto plan = make_plan(tset, geom, kn);
     if (csr.slices.size() != p2) throw CorruptFormatError("sparse_forward: expected p*q CSR slices");
     std::vector<std::vector<uint64_t>> rp(p2), ci(p2);
+    std::vector<std::vector<float>> vals(p2);
     std::vector<const uint64_t*> prp(p2), pci(p2);
     std::vector<const float*> pv(p2);
     std::vector<uint64_t> nnz(p2);
+    std::uint64_t nnz_total = 0;
     for (size_t s = 0; s < p2; ++s) {
         const auto& sl = csr.slices[s];
         rp[s].assign(sl.row_ptr.begin(), sl.row_ptr.end());
         ci[s].assign(sl.col_idx.begin(), sl.col_idx.end());
+        vals[s].assign(sl.values.begin(), sl.values.end());  // f64 values: cast at the edge
         if (rp[s].size() != kn + 1) throw CorruptFormatError("sparse_forward: row_ptr length != K+1");
         prp[s] = rp[s].data();
         pci[s] = ci[s].data();
-        pv[s] = sl.values.data();
+        pv[s] = vals[s].data();
         nnz[s] = sl.values.size();
+        nnz_total += nnz[s];
     }
     check(wino_set_weights_csr(plan->plan, prp.data(), pci.data(), pv.data(), nnz.data()));
     DevBuf in(batch.size()), out(n * kn * geom.h_o * geom.w_o);
@@ -242,7 +255,25 @@ Tensor sparse_forward<float>(const Tensor& batch, const PointwiseCsr<float>& csr
     check(wino_forward(plan->plan, (int)n, in.p, out.p, nullptr, 0, nullptr));
     Tensor o({n, kn, geom.h_o, geom.w_o});
     out.download(o.data());
+    if (counter) {  // spmdm per slice and image (sparse.cpp:65-68), summed over the batch
+        const std::uint64_t c = nnz_total * geom.t * n;
+        counter->multiplications += c;
+        counter->additions += c;
+    }
     return o;
+}
+}  // namespace
+
+// Explicit specializations: override the template instantiations sparse.cpp emits.
+template <>
+Tensor sparse_forward<float>(const Tensor& batch, const PointwiseCsr<float>& csr, const TransformSet& tset,
+                             const TileGeometry& geom, unsigned /*workers*/, OpCounter* counter) {
+    return sparse_forward_gpu(batch, csr, tset, geom, counter);
+}
+template <>
+Tensor sparse_forward<double>(const Tensor& batch, const PointwiseCsr<double>& csr, const TransformSet& tset,
+                              const TileGeometry& geom, unsigned /*workers*/, OpCounter* counter) {
+    return sparse_forward_gpu(batch, csr, tset, geom, counter);
 }
 
 }  // namespace wino

@@ -33,5 +33,27 @@ def test_bench_cli_parses():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--help"], capture_output=True, text=True,
                          timeout=120, cwd=ROOT)
     assert out.returncode == 0
-    for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--dw", "--contraction"):
+    for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--contraction", "--no-sweep"):
         assert flag in out.stdout
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself as 2 ranks under
+    torch.distributed.run (127.0.0.1) — the same code path as the driver's multi-GPU launch; the
+    dry run takes the GPU arm's rank plumbing and its one dW_F all-reduce over gloo."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run", "--config", "c1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "spawning 2 ranks" in out.stderr
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["backend"] == "gloo" and d["allreduce_ok"]
+    assert d["shards"] == [[0, 32], [32, 32]]
+
+
+def test_world_size_mismatch_fails():
+    env = dict(__import__("os").environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--dry-run"], capture_output=True,
+                         text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr

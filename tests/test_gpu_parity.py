@@ -175,7 +175,7 @@ def test_densities_against_f64_oracle(sparsity):
     assert_parity(r["dw"][mask], gw[mask], "dW on mask")
 
 
-@pytest.mark.parametrize("mode", ["exact", "tc", "tc-fast"])
+@pytest.mark.parametrize("mode", ["exact", "tc"])
 def test_dense_plan_against_f64_oracle(mode):
     cfg = with_sparsity(CONFIGS["c0"], 0.0)
     img, w_f, go = make_inputs(cfg, n=2)
@@ -223,30 +223,21 @@ def _f64_batched(img, w_f, go, pad, m=4):
 
 
 def test_c1_full_batch_parity():
-    """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%).
-
-    O and dI: every element within |d| <= 1e-5 + 1e-4·|ref| of the f64 reference.
-    dW_F: a 512-term dot product with heavy cancellation.  Its accuracy floor with fp32
-    Ĩ_F/dZ storage (exact f64 dot of the stored operands) already misses the strict bound on
-    ~5e-5 of the surviving entries (19/353,647 here; SURVEY §8a measured the same effect).
-    So dW_F must (a) match that floor within the strict bound elementwise — the kernel adds
-    no error of its own — and (b) miss the strict bound vs the reference on no entry the
-    floor does not also miss."""
+    """BASELINE configs[1] at its full size (N=32, C=256, K=384, H=13, 90%): O, dI and dW_F (every
+    surviving entry) within |d| <= 1e-5 + 1e-4·|ref| of the reference's f64 layer — zero misses.
+    dW_F is a 512-term dot product with heavy cancellation; an fp32-operand dW_F misses the bound
+    on ~5e-5 of the entries, the exact digit GEMM (wino_xdw.cuh) on none, with a margin of ~75x."""
     cfg = CONFIGS["c1"]
     img, w_f, go = make_inputs(cfg)
     r = run_layer(img, w_f, go, 4, 1, dense=False)
     o, dw, di = _f64_batched(img.astype(np.float64), w_f, go.astype(np.float64), 1)
     assert_parity(r["o"], o, "c1 O")
     assert_parity(r["di"], di, "c1 dI")
-    csr = wo.compress(w_f)
-    floor = _floor_dw(img, go, csr)
-    assert_parity(r["dw_raw"], floor, "c1 dW_F vs exact dot of the stored fp32 operands")
     mask = w_f != 0
-    got_bad = np.abs(r["dw"][mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
-    floor_dense = r["layer"].compact_to_dense(floor)
-    floor_bad = np.abs(floor_dense[mask] - dw[mask]) > 1e-5 + 1e-4 * np.abs(dw[mask])
-    assert not np.any(got_bad & ~floor_bad), "dW_F misses the tolerance where the fp32 floor does not"
-    assert got_bad.mean() <= 1e-4, f"strict-tolerance misses {got_bad.mean():.2e}"
+    assert_parity(r["dw"][mask], dw[mask], "c1 dW_F (every surviving entry)")
+    worst = np.max(np.abs(r["dw"][mask] - dw[mask]) / (1e-5 + 1e-4 * np.abs(dw[mask])))
+    assert worst < 0.1, f"dW_F margin only {1 / worst:.1f}x"
+    assert np.all(r["dw"][~mask] == 0)
     # and bitwise against the f32 mirror (reference association order) for the forward
     mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
     assert np.array_equal(r["o"], mir["o"])
@@ -298,7 +289,7 @@ def test_tensor_core_contraction_follows_updates():
     assert np.array_equal(out, fresh.forward(dev(img)).cpu().numpy())
 
 
-@pytest.mark.parametrize("mode", ["sparse", "dense-tc", "precise"])
+@pytest.mark.parametrize("mode", ["sparse", "dense-tc"])
 def test_fused_backward_equals_separate_calls(mode):
     """wino_backward (dW on a side stream, concurrent with dI) == backward_weights + backward_input."""
     cfg = CONFIGS["c0"]
@@ -307,8 +298,6 @@ def test_fused_backward_equals_separate_calls(mode):
         w_f = np.where(w_f == 0, 0.01, w_f)
     layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
     layer.set_weights(w_f, dense=True if mode == "dense-tc" else False)
-    if mode == "precise":
-        layer.set_dw_mode("precise")
     cache = layer.new_cache(3)
     x, g = dev(img), dev(go)
     o = layer.forward(x, cache, relu=True)
@@ -328,69 +317,90 @@ def test_determinism_and_repeatability():
         assert np.array_equal(a[key], b[key]), key
 
 
-@pytest.mark.slow
-def test_c3_sparse_sampled_parity():
-    """configs[3] (N=64, C=K=256, H=56) at 90%: full-size run, oracle on sampled images."""
+def _f64_slices(img, go, slices, pad=1, m=4, chunk=8):
+    """f64 Ĩ_F[s] (C×N·T) and dZ[s] (K×N·T) of selected slices over the whole batch (layer.cpp:55-59,
+    107-116 in f64), built in image chunks to bound host memory."""
+    n, c, h, w = img.shape
+    k = go.shape[1]
+    g = wo.padded_geometry(c, h, w, pad, m)
+    a, b, _ = wo.transforms(m)
+    p = g.p
+    vs = {s: np.empty((c, n * g.t)) for s in slices}
+    zs = {s: np.empty((k, n * g.t)) for s in slices}
+    for n0 in range(0, n, chunk):
+        n1 = min(n, n0 + chunk)
+        imgp = np.zeros((n1 - n0, c, g.h_ip, g.w_ip))
+        imgp[:, :, pad:pad + h, pad:pad + w] = img[n0:n1]
+        til = np.stack([imgp[:, :, (t // g.tiles_x) * m:(t // g.tiles_x) * m + p,
+                             (t % g.tiles_x) * m:(t % g.tiles_x) * m + p] for t in range(g.t)], axis=2)
+        full = np.zeros((n1 - n0, k, g.h_op, g.w_op))
+        full[:, :, :g.h_o, :g.w_o] = go[n0:n1]
+        dot = full.reshape(n1 - n0, k, g.tiles_y, m, g.tiles_x, m)
+        for s in slices:
+            i, j = divmod(s, p)
+            vs[s][:, n0 * g.t:n1 * g.t] = np.einsum("k,nctkl,l->cnt", b[:, i], til, b[:, j]).reshape(c, -1)
+            zs[s][:, n0 * g.t:n1 * g.t] = np.einsum("y,nkaybx,x->knab", a[i], dot, a[j]).reshape(k, -1)
+    return vs, zs
+
+
+C3_SLICES = [0, 7, 20, 35]  # corner, interior and the largest-coefficient slice (5,5)
+
+
+@pytest.fixture(scope="module")
+def c3_ref():
+    """configs[3] inputs (the same I and dO at every sparsity) and the f64 Ĩ_F / dZ of C3_SLICES."""
     cfg = CONFIGS["c3"]
-    img, w_f, go = make_inputs(cfg)
-    r = run_layer(img, w_f, go, 4, 1, dense=False)
+    img, _, go = make_inputs(cfg)
+    vs, zs = _f64_slices(img.astype(np.float64), go.astype(np.float64), C3_SLICES)
+    return img, go, vs, zs
+
+
+def _check_c3(r, w_f, img, go, vs, zs, what):
     sub = [0, 37]
     o, _, di = _f64_batched(img[sub].astype(np.float64), w_f, go[sub].astype(np.float64), 1)
-    assert_parity(r["o"][sub], o, "c3 O (sampled images)")
-    assert_parity(r["di"][sub], di, "c3 dI (sampled images)")
-    # dW needs the whole batch: check sampled rows of every slice against an f64 dot product
-    v, g = wo.input_transform_f32(img, 4, 1)
-    dz = wo.grad_z_f32(go, g, 4)
-    csr = wo.compress(w_f)
-    off = 0
+    assert_parity(r["o"][sub], o, f"{what} O (sampled images)")
+    assert_parity(r["di"][sub], di, f"{what} dI (sampled images)")
+    p = w_f.shape[2]
     worst = 0.0
-    for s in range(36):
-        n = len(csr.values[s])
-        e = np.arange(0, n, 97)
-        rows = np.repeat(np.arange(cfg.k), np.diff(csr.row_ptr[s]))[e]
-        cols = csr.col_idx[s][e]
-        ref_ = np.einsum("et,et->e", dz[s][rows].astype(np.float64), v[s][cols].astype(np.float64))
-        got = r["dw_raw"][off + e]
-        worst = max(worst, float(np.max(np.abs(got - ref_) / (1e-5 + 1e-4 * np.abs(ref_)))))
-        off += n
-    assert worst <= 1.0, f"c3 dW sampled: worst error / tolerance = {worst:.3f}"
+    for s in C3_SLICES:
+        i, j = divmod(s, p)
+        ref_ = zs[s] @ vs[s].T                     # f64 dW_F(:,:,i,j), layer.cpp:118-128
+        mask = w_f[:, :, i, j] != 0 if not r["layer"].is_dense else np.ones(ref_.shape, bool)
+        got = r["dw"][:, :, i, j]
+        assert_parity(got[mask], ref_[mask], f"{what} dW_F slice {s} (every surviving entry)")
+        worst = max(worst, float(np.max(np.abs(got[mask] - ref_[mask]) / (1e-5 + 1e-4 * np.abs(ref_[mask])))))
+        assert np.all(got[~mask] == 0)
+    return worst
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("mode", ["tc", "tc-fast"])
-def test_c3_dense_tensor_core_parity(mode):
-    """configs[3] at 0% sparsity: the dense plan runs the 3xTF32 tcgen05 GEMMs.  Their products
-    carry ~1e-6·Σ|w·x| error (tensor-core TF32 accumulation), so the strict elementwise bound is
-    checked as a miss fraction next to a normwise bound; the dense CSR fallback
-    (WINO_DENSE_NO_TC=1) is the exact-order alternative."""
-    cfg = with_sparsity(CONFIGS["c3"], 0.0)
-    img, w_f, go = make_inputs(cfg)
-    r = run_layer(img, w_f, go, 4, 1, dense=mode)
+@pytest.mark.parametrize("sparsity,contraction", [(0.5, "csr"), (0.8, "csr"), (0.9, "csr"), (0.95, "csr"),
+                                                  (0.5, "auto"), (0.8, "auto"), (0.9, "auto")])
+def test_c3_sweep_parity(sparsity, contraction, c3_ref):
+    """configs[3] (N=64, C=K=256, H=56) at every BASELINE sparsity, CSR and 'auto' contraction:
+    O and dI on sampled images, dW_F on EVERY surviving entry of sampled slices, all against the
+    reference's f64 layer (sparse.cpp:189-253 forward, layer.cpp:98-171 backward on the mask)."""
+    img, go, vs, zs = c3_ref
+    _, w_f, _ = make_inputs(with_sparsity(CONFIGS["c3"], sparsity))
+    r = run_layer(img, w_f, go, 4, 1, dense=False, contraction=contraction if contraction != "csr" else None)
+    worst = _check_c3(r, w_f, img, go, vs, zs, f"c3 {sparsity:.0%} {contraction}")
+    print(f"c3 {sparsity:.0%} {contraction}: dW worst error / tolerance {worst:.3g}")
+    if contraction == "csr":  # the CSR forward is bitwise the reference's f32 order: check 2 images
+        mir = wo.layer_f32(img[:2], wo.compress(w_f), None, m=4, pad=1)
+        assert np.array_equal(r["o"][:2], mir["o"])
+
+
+@pytest.mark.slow
+def test_c3_dense_tensor_core_parity(c3_ref):
+    """configs[3] at 0% sparsity: the dense plan (3xTF32 tcgen05 Z / dĨ_F, compensated fold per
+    k-block; exact int8 digit GEMM for dW_F): O and dI on sampled images and dW_F on every entry
+    of sampled slices within the strict bound of the f64 reference."""
+    img, go, vs, zs = c3_ref
+    _, w_f, _ = make_inputs(with_sparsity(CONFIGS["c3"], 0.0))
+    r = run_layer(img, w_f, go, 4, 1, dense="tc")
     assert r["layer"].is_dense
-    sub = [0, 37]
-    o, _, di = _f64_batched(img[sub].astype(np.float64), w_f, go[sub].astype(np.float64), 1)
-    fo, fi = fail_fraction(r["o"][sub], o), fail_fraction(r["di"][sub], di)
-    no = np.abs(r["o"][sub] - o).max() / np.abs(o).max()
-    ni = np.abs(r["di"][sub] - di).max() / np.abs(di).max()
-    print(f"dense c3 [{mode}]: O miss {fo:.2e} norm {no:.1e}; dI miss {fi:.2e} norm {ni:.1e}")
-    assert no < 1e-5 and ni < 1e-5
-    if mode == "tc":  # per-k-block fp64 folding: at the fp32 level, like the exact path
-        assert fo == 0.0 and fi == 0.0
-    else:
-        assert fo < 1e-3 and fi < 1e-3
-    # dW: full K×C×36 from the whole batch, sampled against an f64 dot of the fp32 operands
-    v, g = wo.input_transform_f32(img, 4, 1)
-    dz = wo.grad_z_f32(go, g, 4)
-    rng = np.random.default_rng(0)
-    ks, cs, ss = rng.integers(0, 256, 400), rng.integers(0, 256, 400), rng.integers(0, 36, 400)
-    ref_ = np.einsum("et,et->e", dz[ss, ks].astype(np.float64), v[ss, cs].astype(np.float64))
-    got = r["dw"][ks, cs, ss // 6, ss % 6]
-    nw = np.abs(got - ref_).max() / np.abs(ref_).max()
-    print(f"dense c3 [{mode}]: dW miss {fail_fraction(got, ref_):.2e} norm {nw:.1e}")
-    if mode == "tc":
-        assert nw < 1e-6 and fail_fraction(got, ref_) < 1e-2
-    else:
-        assert nw < 5e-5  # one fp32 TMEM chain over n·T = 12544 terms
+    worst = _check_c3(r, w_f, img, go, vs, zs, "c3 dense")
+    print(f"c3 dense: dW worst error / tolerance {worst:.3g}")
 
 
 def test_relu_flags_and_sgd():
@@ -546,8 +556,8 @@ def test_pipelined_host_step_is_bitwise_the_whole_batch(name, n, chunks, relu):
     for _ in range(2):
         ps(h[0], h[1], *outs)
     torch.cuda.synchronize()
-    for got, w in zip(outs, want):
-        assert np.array_equal(got.numpy(), w)
+    _check_pipelined(outs, want)
+    first = [t.numpy().copy() for t in outs]
     # and captured as one CUDA graph (copies + kernels on three streams)
     from paper_1702_08597_b200.graph import GraphedStep
 
@@ -555,8 +565,18 @@ def test_pipelined_host_step_is_bitwise_the_whole_batch(name, n, chunks, relu):
         t.zero_()
     GraphedStep(lambda: ps(h[0], h[1], *outs)).replay()
     torch.cuda.synchronize()
-    for got, w in zip(outs, want):
+    for got, w in zip(outs, first):
         assert np.array_equal(got.numpy(), w)
+
+
+def _check_pipelined(outs, want):
+    """O and dI bitwise the whole-batch calls.  dW_F: each image chunk is its own digit-exponent
+    segment (its max|I| / max|dO| are known when its range runs), so the digits round differently
+    than with the whole batch's exponents — both within ~2% of north_star's tolerance of the f64
+    value (c1), so they agree within a tolerance 10x tighter than north_star's."""
+    assert np.array_equal(outs[0].numpy(), want[0])
+    assert np.array_equal(outs[2].numpy(), want[2])
+    assert_parity(outs[1].numpy(), want[1], "pipelined dW_F vs whole batch", rtol=1e-5, atol=1e-6)
 
 
 def test_range_calls_validate():
@@ -580,7 +600,7 @@ def test_range_calls_validate():
 
 
 def test_auto_contraction_follows_density():
-    """contraction 'auto': tensor cores (incl. the tc dW) at density >= the threshold, the CSR path
+    """contraction 'auto': tensor cores at density >= the threshold, the CSR path
     below it (bitwise the default forward), re-decided when the weights change."""
     cfg = CONFIGS["c0"]
     img, w_f, go = make_inputs(with_sparsity(cfg, 0.5), n=2)
@@ -595,7 +615,7 @@ def test_auto_contraction_follows_density():
     assert_parity(o, o64, "auto O (tensor cores)")
     assert_parity(di, di64, "auto dI (tensor cores)")
     mask = w_f != 0
-    assert fail_fraction(layer.compact_to_dense(dw.astype(np.float64))[mask], dw64[mask]) < 1e-2
+    assert_parity(layer.compact_to_dense(dw.astype(np.float64))[mask], dw64[mask], "auto dW_F")
     # below the threshold: the CSR kernels, bitwise the reference order
     layer.set_auto_density(0.9)
     o2 = layer.forward(dev(img)).cpu().numpy()
@@ -603,7 +623,7 @@ def test_auto_contraction_follows_density():
     assert np.array_equal(o2, mir["o"])
 
 
-@pytest.mark.parametrize("mode", ["csr", "tc", "dense", "int8"])
+@pytest.mark.parametrize("mode", ["csr", "tc", "dense"])
 def test_forward_backward_equals_two_calls(mode):
     """wino_forward_backward (dI chain and dW_F overlapping the forward) is bitwise forward +
     backward on every plan kind."""
@@ -613,8 +633,6 @@ def test_forward_backward_equals_two_calls(mode):
     layer.set_weights(w_f, dense=(mode == "dense"))
     if mode == "tc":
         layer.set_contraction("tc")
-    if mode == "int8":
-        layer.set_dw_mode("int8")
     x, g = dev(img), dev(go)
     c1 = layer.new_cache(cfg.n)
     o1 = layer.forward(x, c1)
@@ -628,11 +646,12 @@ def test_forward_backward_equals_two_calls(mode):
     assert torch.equal(layer.backward_input(c2), i1)
 
 
-@pytest.mark.parametrize("mode", ["dense", "tc", "int8", "fb"])
+@pytest.mark.parametrize("mode", ["dense", "tc", "csr", "fb"])
 def test_ragged_tile_shapes(mode):
     """C, K and N·T that fill no tcgen05 tile evenly (C = 136, K = 200, 3 images of 9×9 → N·T = 27):
     partial M, N and reduction blocks in the warp-specialised GEMM (TMA zero-fill, clipped TMA
-    stores), partial int8 digit blocks and a partial 48-column tile, against the f64 reference."""
+    stores) and in the int8 digit GEMM (partial 128-row / 64-row tiles, a padded 64-column
+    segment), every output element within the strict bound of the f64 reference."""
     from paper_1702_08597_b200.synth import LayerConfig
 
     cfg = LayerConfig("ragged", 3, 136, 200, 9, 0.0 if mode == "dense" else 0.7)
@@ -641,9 +660,6 @@ def test_ragged_tile_shapes(mode):
     layer.set_weights(w_f, dense=(mode == "dense"))
     if mode == "tc":
         layer.set_contraction("tc")
-        layer.set_dw_mode("tc")
-    if mode == "int8":
-        layer.set_dw_mode("int8")
     cache = layer.new_cache(cfg.n)
     x, g = dev(img), dev(go)
     if mode == "fb":
@@ -656,32 +672,27 @@ def test_ragged_tile_shapes(mode):
     assert_parity(o, o64, f"{mode} O")
     assert_parity(di, di64, f"{mode} dI")
     dwd = dw if mode == "dense" else layer.compact_to_dense(dw.astype(np.float64))
-    mask = w_f != 0
-    assert fail_fraction(np.asarray(dwd)[mask], dw64[mask]) < 1e-3, f"{mode} dW_F"
-    if mode == "int8":  # the exact-product SDDMM on the same operands, within one rounding
-        layer.set_dw_mode("sddmm")
-        ref = layer.backward_weights(g, cache).cpu().numpy()
-        assert_parity(dw, ref, "int8 dW_F vs SDDMM")
+    mask = w_f != 0 if mode != "dense" else np.ones(w_f.shape, bool)
+    assert_parity(np.asarray(dwd)[mask], dw64[mask], f"{mode} dW_F")
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("tmem", [False, True])
-def test_c2_shape_forward_bitwise(tmem, monkeypatch):
-    """configs[2]'s layer shape (C = K = 512, H = W = 28, 90%) on 2 images: the SpMM takes its
-    2-wide-t variant (a 512-row X chunk does not fit shared memory at 4-wide) — or, with
-    WINO_SPMM_TMEM=1, the tensor-memory SpMM in 4 passes — and the forward stays bitwise the f32
-    mirror of the reference's sparse_forward<float>."""
-    from paper_1702_08597_b200.synth import LayerConfig
-
-    if tmem:
-        monkeypatch.setenv("WINO_SPMM_TMEM", "1")
-    cfg = CONFIGS["c2"]
-    img, w_f, _ = make_inputs(LayerConfig("c2", 2, cfg.c, cfg.k, cfg.h, 0.9))
+@pytest.mark.parametrize("sparsity", [0.8, 0.9, 0.95])
+def test_c2_forward_bitwise(sparsity):
+    """configs[2] at its full size (N=64, C=K=512, H=W=28) at 80/90/95%: the SpMM takes its
+    2-wide-t variant (a 512-row X chunk does not fit shared memory at 4-wide); the forward of 8
+    sampled images is bitwise the f32 mirror of the reference's sparse_forward<float>
+    (sparse.cpp:189-253) and within the strict bound of the f64 layer."""
+    cfg = with_sparsity(CONFIGS["c2"], sparsity)
+    img, w_f, _ = make_inputs(cfg)
     layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.h, pad=1, m=4)
     layer.set_weights(w_f, dense=False)
     o = layer.forward(dev(img)).cpu().numpy()
-    mir = wo.layer_f32(img, wo.compress(w_f), None, m=4, pad=1)
-    assert np.array_equal(o, mir["o"])
+    sub = [0, 9, 18, 27, 36, 45, 54, 63]
+    mir = wo.layer_f32(img[sub], wo.compress(w_f), None, m=4, pad=1)
+    assert np.array_equal(o[sub], mir["o"])
+    o64, _, _ = _f64_batched(img[sub[:2]].astype(np.float64), w_f, np.zeros((2, cfg.k, cfg.h, cfg.h)), 1)
+    assert_parity(o[sub[:2]], o64, f"c2 {sparsity:.0%} O")
 
 
 @pytest.mark.parametrize("name", LAYER_CASES)
@@ -701,3 +712,54 @@ def test_forward_backward_golden(name):
     assert torch.equal(o1, o2) and torch.equal(w1, w2) and torch.equal(i1, i2)
     if "o_sparse_f32" in d:
         assert np.array_equal(o2.cpu().numpy(), d["o_sparse_f32"])
+
+
+
+@pytest.mark.slow
+def test_c4_stack_layers_against_reference():
+    """configs[4]'s layer stack (4 layers, C=K=256, H=W=28, 90% fixed masks, ReLU between layers)
+    at 64 images per GPU (the 8-GPU shard of the global batch of 512): every layer's forward is
+    bitwise the f32 mirror of the reference's sparse_forward<float> applied to the previous
+    layer's fp32 output (ReLU fused, train.cpp:76-83); every layer's dW_F (every surviving entry)
+    and dI within the strict bound of the f64 layer on the same fp32 inputs and the
+    relu-masked incoming gradient (train.cpp:189-211)."""
+    from paper_1702_08597_b200.stack import WinogradStack
+    from paper_1702_08597_b200.synth import LayerConfig, Stream
+
+    cfg = CONFIGS["c4"]
+    n = 64
+    weights = [make_inputs(LayerConfig("c4", 1, cfg.c, cfg.k, cfg.h, cfg.sparsity, seed=cfg.seed), layer=l)[1]
+               for l in range(4)]
+    img = Stream(cfg.seed, "c4/I").normal((n, cfg.c, cfg.h, cfg.w)).astype(np.float32)
+    go = Stream(cfg.seed, "c4/dO").normal((n, cfg.k, cfg.h, cfg.w)).astype(np.float32)
+    st = WinogradStack(weights, cfg.c, cfg.h, cfg.w, pad=1, m=4, n_max=n)
+    st.forward(dev(img))
+    st.backward(dev(go), serial=True)
+    torch.cuda.synchronize()
+    ins = [img] + [st.outs[i].cpu().numpy() for i in range(3)]
+    grads = [g.cpu().numpy().astype(np.float64) for g in st.grads]
+    g_in = go
+    for i in range(3, -1, -1):
+        lay, w_f = st.layers[i], weights[i]
+        out = st.outs[i].cpu().numpy()
+        if i in (0, 3):  # the mirror of the reference's f32 order, bitwise (two layers: host time)
+            mir = wo.layer_f32(ins[i][:4], wo.compress(w_f), None, m=4, pad=1)
+            assert np.array_equal(out[:4], np.maximum(mir["o"], 0)), f"layer {i} forward"
+        dO = g_in * (out > 0)                            # relu-mask backward, train.cpp:193
+        o64, dw64, di64 = _f64_batched(ins[i].astype(np.float64), w_f, dO.astype(np.float64), 1)
+        assert_parity(out, np.maximum(o64, 0), f"layer {i} O")
+        mask = w_f != 0
+        assert_parity(lay.compact_to_dense(grads[i])[mask], dw64[mask], f"layer {i} dW_F")
+        if i > 0:
+            g_in = st.dis[i].cpu().numpy()
+            assert_parity(g_in, di64, f"layer {i} dI")
+
+
+def test_dw_mode_option():
+    """dW_F has one mode ('exact'); the round-1 mode names are rejected."""
+    layer = wb.WinogradLayer(16, 16, 12, 12, pad=1, m=4)
+    layer.set_weights(make_inputs(CONFIGS["c0"])[1])
+    layer.set_dw_mode("exact")
+    for bad in ("sddmm", "tc", "precise", "int8"):
+        with pytest.raises(wb.InvalidArgument):
+            layer.set_dw_mode(bad)
