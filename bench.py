@@ -209,8 +209,9 @@ def capture(step, args):
 
 def kernel_work(cfg, layer, n):
     """Algorithmic HBM bytes and tensor-pipe operations per STEP of each kernel
-    kind.  dw_digits: the two digit kernels (I -> Ĩ_F digits, dO -> dZ digits: 5 int8 digits per
-    value); dw_gemm_i8: 15 exact digit-pair MACs per (k, c, column) on tcgen05 kind::i8."""
+    kind.  input_transform / grad_z: K1 / K4 fused with the exact dW_F digits (5 int8 digits per
+    value of Ĩ_F / dZ besides the fp32 value); amax: the max|I| / max|dO| pre-pass; dw_gemm_i8: 15
+    exact digit-pair MACs per (k, c, column) on tcgen05 kind::i8."""
     g = layer.geometry
     nt = n * g["t"]
     ntd = -(-nt // 64) * 64
@@ -223,12 +224,14 @@ def kernel_work(cfg, layer, n):
     nnz = layer.nnz
     Wb = 8 * nnz + 4 * p2 * (cfg.k + 1)
     Wt = 8 * nnz + 4 * p2 * (cfg.c + 1)
-    dig = 5 * p2 * (cfg.c + cfg.k) * ntd
+    dig_v, dig_z = 5 * p2 * cfg.c * ntd, 5 * p2 * cfg.k * ntd
+    dig = dig_v + dig_z
     dense_w = 2 * 4 * p2 * cfg.k * cfg.c  # tf32 hi/lo weight operands
+    fwd_only = not cfg.backward
     return {
-        "input_transform": {"bytes": I + V}, "spmm_fwd": {"bytes": V + Z + Wb},
-        "output_transform": {"bytes": Z + O}, "grad_z": {"bytes": O + Z},
-        "dw_digits": {"bytes": I + O + dig},
+        "input_transform": {"bytes": I + V + (0 if fwd_only else dig_v)}, "spmm_fwd": {"bytes": V + Z + Wb},
+        "output_transform": {"bytes": Z + O}, "grad_z": {"bytes": O + Z + dig_z},
+        "amax": {"bytes": I + O},
         "dw_gemm_i8": {"bytes": dig, "ops": 2.0 * 15 * p2 * cfg.k * cfg.c * ntd, "pipe": "int8"},
         "dw_reduce": {"bytes": 8 * p2 * cfg.k * cfg.c + (nnz * 12 if not layer.is_dense else 4 * nnz)},
         "spmm_bwd_data": {"bytes": Z + Wt + V}, "input_grad": {"bytes": V + I},

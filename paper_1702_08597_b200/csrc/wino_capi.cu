@@ -138,10 +138,12 @@ int make_geometry(int64_t c, int64_t h_i, int64_t w_i, int m, int r, wino_geomet
     return WINO_OK;
 }
 
-enum Kind { K_INPUT = 0, K_SPMM, K_OUTPUT, K_GRADZ, K_DW_DIGITS, K_DW_GEMM, K_DW_REDUCE, K_SPMM_T, K_INGRAD,
+// input_transform / grad_z: K1 / K4, in training steps fused with the exact dW_F digits;
+// amax: the per-(segment, row) max|I| / max|dO| pre-pass that bounds the digit exponents.
+enum Kind { K_INPUT = 0, K_SPMM, K_OUTPUT, K_GRADZ, K_AMAX, K_DW_GEMM, K_DW_REDUCE, K_SPMM_T, K_INGRAD,
             K_DENSE_FWD, K_DENSE_DV, K_SGD, K_MISC, K_NKINDS };
 const char* kKindNames[K_NKINDS] = {"input_transform", "spmm_fwd",      "output_transform", "grad_z",
-                                    "dw_digits",       "dw_gemm_i8",    "dw_reduce",        "spmm_bwd_data",
+                                    "amax",            "dw_gemm_i8",    "dw_reduce",        "spmm_bwd_data",
                                     "input_grad",      "dense_fwd_tc",  "dense_dv_tc",      "sgd",
                                     "misc"};
 
@@ -436,18 +438,16 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
     }
 }
 
-// stage 0: K1 (Ĩ_F; with amax also the per-(segment, channel) max|I| of the exact dW_F digits);
+// stage 0: K1 (Ĩ_F only: inference; training steps run K1 fused with the dW_F digits);
 // stage 1: K3 (O)
 template <int M, int P, class CF>
 int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, float* V, float* Z, int n,
-                   int64_t NT, int64_t NTs, int flags, int stage, int64_t NTr, unsigned* amax = nullptr,
-                   int seg_imgs = 1) {
+                   int64_t NT, int64_t NTs, int flags, int stage, int64_t NTr) {
     const wino_geometry& g = p->g;
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
         wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTr, 256, p->sm_count), 256, 0, st>>>(
-            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr, amax,
-            seg_imgs);
+            in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr);
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
@@ -458,24 +458,6 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, f
     else
         wino::output_transform_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(
             Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);
-    return L.done();
-}
-
-// K4: dZ (+ max|dO| per (segment, k) with amax)
-template <int M, int P, class CF>
-int launch_grad_z(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, float* DZ,
-                  int64_t NT, int64_t NTs, bool mask, int64_t NTr, unsigned* amax = nullptr, int seg_imgs = 1) {
-    const wino_geometry& g = p->g;
-    Launch L(p, st, K_GRADZ);
-    const int grid = grid_for((int64_t)p->K * NTr, 256, p->sm_count);
-    if (mask)
-        wino::grad_z_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
-                                                              (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                              (int)NT, (int)NTs, (int)NTr, amax, seg_imgs);
-    else
-        wino::grad_z_kernel<M, P, false, CF><<<grid, 256, 0, st>>>(dO, relu, DZ, p->cf, p->K, (int)g.h_o,
-                                                               (int)g.w_o, (int)g.tiles_x, (int)g.t,
-                                                               (int)NT, (int)NTs, (int)NTr, amax, seg_imgs);
     return L.done();
 }
 
@@ -651,54 +633,77 @@ int find_segments(const wino_cache* c, int n0, int n1, int* g0, int* g1) {
     return WINO_OK;
 }
 
-// Ĩ_F digits of segments [g0, g1); `in` holds images from n_base on (amax_v filled by K1)
+// max|x| per (segment, row) over images [0, n) of x = [n][R][HW] (segments of seg_images(p)
+// images from amax[0]); mask: of dO·[relu > 0]
+int launch_amax(wino_plan* p, cudaStream_t st, const float* x, const float* relu, bool mask, unsigned* amax, int R,
+                int64_t HW, int n) {
+    const int64_t planes = (int64_t)n * R;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((planes + 7) / 8, (int64_t)p->sm_count * 16));
+    Launch L(p, st, K_AMAX);
+    if (mask)
+        wino::xdw::plane_amax_kernel<true><<<grid, 256, 0, st>>>(x, relu, amax, R, (int)HW, seg_images(p), (int)planes);
+    else
+        wino::xdw::plane_amax_kernel<false><<<grid, 256, 0, st>>>(x, nullptr, amax, R, (int)HW, seg_images(p),
+                                                                  (int)planes);
+    return L.done();
+}
+
+// K1 fused with the Ĩ_F digits, segments [g0, g1) of the cache: `in` holds images from n_base on,
+// V points at image n_base's first column (row stride NTs), `owned` = V columns this call writes
+// (from image n_base on; beyond the last image: the batch's zero padding).
 template <int M, int P, class CF>
-int launch_input_digits(wino_plan* p, cudaStream_t st, const float* in, int n_base, wino_cache* c, int g0,
-                        int g1) {
+int launch_input_fused(wino_plan* p, cudaStream_t st, const float* in, float* V, int64_t NTs, int64_t owned,
+                       int n_base, wino_cache* c, int g0, int g1) {
     namespace x = wino::xdw;
     const int64_t T = p->g.t;
-    const size_t smem = (size_t)P * P * x::kTileItems * 5;
-    auto kern = x::input_digits_kernel<M, P, CF>;
-    set_smem_attr(kern, (int)std::max<size_t>(smem, 48 * 1024));
+    constexpr int smem = x::digit_smem_bytes<P * P>();
+    auto kern = x::input_transform_digits_kernel<M, P, CF>;
+    set_smem_attr(kern, smem);
     const int64_t plane = (int64_t)p->P2 * p->C * c->NTd;
     for (int g = g0; g < g1; ++g) {
         const DwSeg& sg = c->segs[g];
-        const int64_t items = (int64_t)p->C * sg.ncols_pad;
-        Launch L(p, st, K_DW_DIGITS);
-        kern<<<(unsigned)((items + x::kTileItems - 1) / x::kTileItems), x::kTileItems, smem, st>>>(
-            in + (int64_t)(sg.n0 - n_base) * p->C * p->H * p->W, c->dig_v, c->e_v + (int64_t)g * p->P2 * p->C,
-            c->amax_v + (int64_t)g * p->C, p->cfd, p->nrm_v, p->C, p->H, p->W, p->pad, (int)p->g.tiles_x, (int)T,
-            (int)((sg.n1 - sg.n0) * T), (int)sg.ncols_pad, c->NTd, plane, (int)sg.col0);
+        const int64_t ncols = (int64_t)(sg.n1 - sg.n0) * T, voff = (int64_t)(sg.n0 - n_base) * T;
+        const int64_t vcols = g == g1 - 1 ? owned - voff : ncols;
+        const int64_t cols = std::max(vcols, sg.ncols_pad);
+        Launch L(p, st, K_INPUT);
+        kern<<<dim3((unsigned)((cols + x::kTileItems - 1) / x::kTileItems), (unsigned)p->C), x::kTileItems, smem, st>>>(
+            in + (int64_t)(sg.n0 - n_base) * p->C * p->H * p->W, V + voff, c->dig_v,
+            c->e_v + (int64_t)g * p->P2 * p->C, c->amax_v + (int64_t)g * p->C, p->cf, p->cfd, p->nrm_v, p->C, p->H,
+            p->W, p->pad, (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
+            (int)sg.col0);
         int rc = L.done();
         if (rc) return rc;
     }
     return WINO_OK;
 }
 
-// dZ digits of segments [g0, g1); dO (and relu) hold images from n_base on (amax_z filled by K4)
+// K4 fused with the dZ digits, segments [g0, g1): dO (and relu) hold images from n_base on, DZ
+// points at image n_base's first column, `owned` as launch_input_fused
 template <int M, int P, class CF>
-int launch_grad_digits(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, bool mask, int n_base,
-                       wino_cache* c, int g0, int g1) {
+int launch_grad_fused(wino_plan* p, cudaStream_t st, const float* dO, const float* relu, bool mask, float* DZ,
+                      int64_t NTs, int64_t owned, int n_base, wino_cache* c, int g0, int g1) {
     namespace x = wino::xdw;
     const int64_t T = p->g.t, HW = p->g.h_o * p->g.w_o;
-    const size_t smem = (size_t)P * P * x::kTileItems * 5;
+    constexpr int smem = x::digit_smem_bytes<P * P>();
     const int64_t plane = (int64_t)p->P2 * p->K * c->NTd;
     for (int g = g0; g < g1; ++g) {
         const DwSeg& sg = c->segs[g];
-        const int64_t items = (int64_t)p->K * sg.ncols_pad;
+        const int64_t ncols = (int64_t)(sg.n1 - sg.n0) * T, voff = (int64_t)(sg.n0 - n_base) * T;
+        const int64_t vcols = g == g1 - 1 ? owned - voff : ncols;
+        const int64_t cols = std::max(vcols, sg.ncols_pad);
         const int64_t off = (int64_t)(sg.n0 - n_base) * p->K * HW;
-        const unsigned blocks = (unsigned)((items + x::kTileItems - 1) / x::kTileItems);
-        Launch L(p, st, K_DW_DIGITS);
+        const dim3 grid((unsigned)((cols + x::kTileItems - 1) / x::kTileItems), (unsigned)p->K);
+        Launch L(p, st, K_GRADZ);
         auto go = [&](auto kern) {
-            set_smem_attr(kern, (int)std::max<size_t>(smem, 48 * 1024));
-            kern<<<blocks, x::kTileItems, smem, st>>>(
-                dO + off, relu ? relu + off : nullptr, c->dig_z, c->e_z + (int64_t)g * p->P2 * p->K,
-                c->amax_z + (int64_t)g * p->K, p->cfd, p->nrm_z, p->K, (int)p->g.h_o, (int)p->g.w_o,
-                (int)p->g.tiles_x, (int)T, (int)((sg.n1 - sg.n0) * T), (int)sg.ncols_pad, c->NTd, plane,
+            set_smem_attr(kern, smem);
+            kern<<<grid, x::kTileItems, smem, st>>>(
+                dO + off, relu ? relu + off : nullptr, DZ + voff, c->dig_z, c->e_z + (int64_t)g * p->P2 * p->K,
+                c->amax_z + (int64_t)g * p->K, p->cf, p->cfd, p->nrm_z, p->K, (int)p->g.h_o, (int)p->g.w_o,
+                (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
                 (int)sg.col0);
         };
-        if (mask) go(x::grad_digits_kernel<M, P, true, CF>);
-        else go(x::grad_digits_kernel<M, P, false, CF>);
+        if (mask) go(x::grad_z_digits_kernel<M, P, true, CF>);
+        else go(x::grad_z_digits_kernel<M, P, false, CF>);
         int rc = L.done();
         if (rc) return rc;
     }
@@ -1312,19 +1317,17 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         V = p->d_dv;  // inference: the backward scratch doubles as Ĩ_F
     }
     if ((rc = ensure(&p->d_z, &p->z_cap, (size_t)p->P2 * p->K * NTs))) return rc;
-    unsigned* amax = nullptr;
-    int nseg = 0;
-    if (cache) {
+    if (cache) {  // training: K1 fused with the exact dW_F digits of Ĩ_F
         cache->has_fwd = false;
         if ((rc = plan_segments(p, cache, 0, n, true))) return rc;
-        nseg = (int)cache->segs.size();
-        if ((rc = zero_rows(cache->amax_v, 0, nseg, p->C, st))) return rc;
-        amax = cache->amax_v;
-    }
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, p->d_z, n, NT, NTs, flags, 0, NTs, amax,
-                          seg_images(p))))
+        const int nseg = (int)cache->segs.size();
+        if ((rc = zero_rows(cache->amax_v, 0, nseg, p->C, st)) ||
+            (rc = launch_amax(p, st, input, nullptr, false, cache->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
+            (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, V, NTs, NTs, 0, cache, 0, nseg)))
+            return rc;
+    } else if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, p->d_z, n, NT, NTs, flags, 0, NTs))) {
         return rc;
-    if (cache && (rc = DISPATCH_MP(p, launch_input_digits, p, st, input, 0, cache, 0, nseg))) return rc;
+    }
     if (p->tc_ready && (p->dense || p->contraction == 1))
         rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, V, p->d_z, p->K, p->C, NTs);
     else
@@ -1354,28 +1357,24 @@ static int bwd_check(wino_plan* p, const float* grad_output, const float* relu_o
     return WINO_OK;
 }
 
-// K4: dZ = A1·dÕ·A2ᵀ into the cache, with the per-segment max|dO| of the dZ digits
+// K4: dZ = A1·dÕ·A2ᵀ into the cache fused with its exact dW_F digits (after the max|dO| pre-pass)
 static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, int flags,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool zero = true) {
     const bool mask = (flags & WINO_BWD_RELU_MASK) != 0;
-    const int64_t NT = (int64_t)c->n * p->g.t, NTs = c->NTs;
-    int rc = zero_rows(c->amax_z, 0, (int)c->segs.size(), p->K, st);
-    if (rc) return rc;
+    const int nseg = (int)c->segs.size();
     c->z_segs = 0;
-    return DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, c->DZ, NT, NTs, mask, NTs, c->amax_z,
-                       seg_images(p));
+    int rc;
+    if ((zero && (rc = zero_rows(c->amax_z, 0, nseg, p->K, st))) ||
+        (rc = launch_amax(p, st, grad_output, relu_out, mask, c->amax_z, p->K, p->g.h_o * p->g.w_o, c->n)) ||
+        (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, c->DZ, c->NTs, c->NTs, 0, c, 0,
+                          nseg)))
+        return rc;
+    c->z_segs = nseg;
+    return WINO_OK;
 }
 
-// dZ digits of the whole batch, then dW_F (exact, wino_xdw.cuh)
-static int bwd_dw(wino_plan* p, wino_cache* c, const float* grad_output, const float* relu_out, int flags,
-                  float* grad_w, cudaStream_t st) {
-    const int nseg = (int)c->segs.size();
-    int rc = DISPATCH_MP(p, launch_grad_digits, p, st, grad_output, relu_out, (flags & WINO_BWD_RELU_MASK) != 0, 0,
-                         c, 0, nseg);
-    if (rc) return rc;
-    c->z_segs = nseg;
-    return launch_xdw(p, st, c, grad_w);
-}
+// dW_F from the digits of Ĩ_F and dZ (exact, wino_xdw.cuh)
+static int bwd_dw(wino_plan* p, wino_cache* c, float* grad_w, cudaStream_t st) { return launch_xdw(p, st, c, grad_w); }
 
 // dĨ_F = W_Fᵀ·dZ and dI = Σ_φ B1·dĨ_F·B2ᵀ
 static int bwd_input(wino_plan* p, const wino_cache* c, float* grad_input, cudaStream_t st) {
@@ -1397,7 +1396,7 @@ int wino_backward_weights(wino_plan* p, const float* grad_output, const float* r
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
     c->has_grad_z = true;
-    return bwd_dw(p, c, grad_output, relu_out, flags, grad_w, st);
+    return bwd_dw(p, c, grad_w, st);
 }
 
 int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out, wino_cache* c, float* grad_w,
@@ -1408,13 +1407,13 @@ int wino_backward(wino_plan* p, const float* grad_output, const float* relu_out,
     if ((rc = bwd_grad_z(p, grad_output, relu_out, c, flags, st))) return rc;
     c->has_grad_z = true;
     if (!grad_input)  // no dI wanted (the first layer of a stack, train.cpp:201): dW only
-        return bwd_dw(p, c, grad_output, relu_out, flags, grad_w, st);
+        return bwd_dw(p, c, grad_w, st);
     if ((rc = ensure_streams(p))) return rc;
     // dW (side stream) and dĨ_F -> dI (caller's stream) only share the read-only dZ / dO
     CUDA_TRY(cudaEventRecord(p->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     JoinGuard join{p, st, true, false};
-    if ((rc = bwd_dw(p, c, grad_output, relu_out, flags, grad_w, p->side))) return rc;
+    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
     return bwd_input(p, c, grad_input, st);
 }
 
@@ -1452,22 +1451,19 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     CUDA_TRY(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     JoinGuard join{p, st, true, true};
-    // side2: dZ, then dĨ_F = W_Fᵀ·dZ and dI
-    if ((rc = DISPATCH_MP(p, launch_grad_z, p, p->side2, grad_output, nullptr, c->DZ, NT, NTs, false, NTs,
-                          c->amax_z, seg_images(p))))
-        return rc;
+    // side2: dZ and its digits, then dĨ_F = W_Fᵀ·dZ and dI
+    if ((rc = bwd_grad_z(p, grad_output, nullptr, c, 0, p->side2, false))) return rc;
     CUDA_TRY(cudaEventRecord(p->ev_dz, p->side2));
     if ((rc = bwd_input(p, c, grad_input, p->side2))) return rc;
-    // caller's stream: Ĩ_F, then Z = W_F·Ĩ_F and O
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, c->V, p->d_z, n, NT, NTs, 0, 0, NTs,
-                          c->amax_v, seg_images(p))))
+    // caller's stream: Ĩ_F and its digits, then Z = W_F·Ĩ_F and O
+    if ((rc = launch_amax(p, st, input, nullptr, false, c->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
+        (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, c->V, NTs, NTs, 0, c, 0, nseg)))
         return rc;
     CUDA_TRY(cudaEventRecord(p->ev_v, st));
-    // side: the dW_F chain once K1 and K4 have the segment maxima
+    // side: the dW_F GEMM once both digit sets exist
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_v, 0));
-    if ((rc = DISPATCH_MP(p, launch_input_digits, p, p->side, input, 0, c, 0, nseg))) return rc;
     CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_dz, 0));
-    if ((rc = bwd_dw(p, c, grad_output, nullptr, 0, grad_w, p->side))) return rc;
+    if ((rc = bwd_dw(p, c, grad_w, p->side))) return rc;
     if (p->tc_ready && (p->dense || p->contraction == 1))
         rc = launch_tc_gemm(p, st, K_DENSE_FWD, p->map_wh, p->map_wl, c->V, p->d_z, p->K, p->C, NTs);
     else
@@ -1524,10 +1520,10 @@ int wino_forward_range(wino_plan* p, int n_total, int n0, int n1, const float* i
     if ((rc = zero_rows(cache->amax_v, g0, g1, p->C, st))) return rc;
     float* V = cache->V + r.a;
     float* Z = p->d_z + r.a;
-    if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, Z, n1 - n0, r.NT, r.NTs, flags, 0, r.NTr,
-                          cache->amax_v + (int64_t)g0 * p->C, seg_images(p))))
+    if ((rc = launch_amax(p, st, input, nullptr, false, cache->amax_v + (int64_t)g0 * p->C, p->C,
+                          (int64_t)p->H * p->W, n1 - n0)) ||
+        (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, V, r.NTs, r.NTr, n0, cache, g0, g1)))
         return rc;
-    if ((rc = DISPATCH_MP(p, launch_input_digits, p, st, input, n0, cache, g0, g1))) return rc;
     if ((rc = launch_spmm(p, st, K_SPMM, p->d_rowptr, p->d_cv, p->h_rowptr, V, Z, p->K, p->C, r.NT, r.NTs, r.NTr)))
         return rc;
     if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, Z, n1 - n0, r.NT, r.NTs, flags, 1, r.NTr)))
@@ -1561,11 +1557,11 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
     if (n0 == 0) c->z_segs = 0;
     if (g0 != c->z_segs)
         return set_err(WINO_CONSISTENCY_ERROR, "backward image ranges of a batch must be issued in order from image 0");
-    if ((rc = zero_rows(c->amax_z, g0, g1, p->K, st))) return rc;
-    if ((rc = DISPATCH_MP(p, launch_grad_z, p, st, grad_output, relu_out, DZ, r.NT, r.NTs, mask, r.NTr,
-                          c->amax_z + (int64_t)g0 * p->K, seg_images(p))))
+    if ((rc = zero_rows(c->amax_z, g0, g1, p->K, st)) ||
+        (rc = launch_amax(p, st, grad_output, relu_out, mask, c->amax_z + (int64_t)g0 * p->K, p->K,
+                          p->g.h_o * p->g.w_o, n1 - n0)) ||
+        (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, DZ, r.NTs, r.NTr, n0, c, g0, g1)))
         return rc;
-    if ((rc = DISPATCH_MP(p, launch_grad_digits, p, st, grad_output, relu_out, mask, n0, c, g0, g1))) return rc;
     if ((rc = launch_spmm(p, st, K_SPMM_T, p->d_colptr, p->d_cvT, p->h_colptr, DZ, DV, p->C, p->K, r.NT, r.NTs,
                           r.NTr)))
         return rc;

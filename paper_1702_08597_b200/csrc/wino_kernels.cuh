@@ -77,20 +77,6 @@ struct CoefsD {
     double b[kMaxP * kMaxP];  // b1: p×p row-major
 };
 
-// atomicMax of a non-negative float's bits into amax[key] (key < 0: nothing), one atomic per warp
-// when the active lanes share the key (the common case: consecutive tiles of one channel).
-__device__ __forceinline__ void block_max_atomic(unsigned* amax, int key, unsigned mx) {
-    const unsigned am = __activemask();
-    const int leader = __ffs(am) - 1;
-    const int k0 = __shfl_sync(am, key, leader);
-    if (__all_sync(am, key == k0)) {
-        const unsigned r = __reduce_max_sync(am, mx);
-        if (k0 >= 0 && (int)(threadIdx.x & 31) == leader) atomicMax(amax + k0, r);
-    } else if (key >= 0) {
-        atomicMax(amax + key, mx);
-    }
-}
-
 // ---------------------------------------------------------------------------------
 // K1: φ gather (pad folded in) + Ĩ_F = B1ᵀ·d·B2   (transforms.cpp:196-210, sparse.cpp:94-120)
 // One thread per (c, nt); consecutive threads = consecutive tiles -> coalesced stores.
@@ -98,12 +84,9 @@ __device__ __forceinline__ void block_max_atomic(unsigned* amax, int key, unsign
 template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
-                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr,
-                       unsigned* __restrict__ amax = nullptr, int seg_imgs = 1) {
-    // columns [0, NTr) of V rows with stride NTs (a column range of the batch when V and `in` are
-    // offset to its first image); columns ≥ NT are the zero padding.
-    // amax != nullptr: also max|I| over the pixels each (segment, c) reads, segment = n / seg_imgs
-    // (the exponent bound of the exact dW_F digits, wino_xdw.cuh), as float bits via atomicMax
+                       int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr) {
+    // columns [0, NTr) of V rows with stride NTs; columns ≥ NT are the zero padding.  (Training
+    // steps run the same product fused with the exact dW_F digits, wino_xdw.cuh.)
     const int64_t plane = (int64_t)C * NTs;
     const int64_t items = (int64_t)C * NTr;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
@@ -111,7 +94,6 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
         const int c = (int)(gid / NTr);
         const int nt = (int)(gid - (int64_t)c * NTr);
         float d[P][P];
-        int key = -1;
         if (nt < NT) {
             const int n = nt / T, t = nt - n * T;
             const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -127,20 +109,11 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                     d[i][j] = (yok && (unsigned)x < (unsigned)W) ? __ldg(src + y * W + x) : 0.f;
                 }
             }
-            if (amax) key = (n / seg_imgs) * C + c;
         } else {
 #pragma unroll
             for (int i = 0; i < P; ++i)
 #pragma unroll
                 for (int j = 0; j < P; ++j) d[i][j] = 0.f;
-        }
-        if (amax) {
-            unsigned mx = 0;
-#pragma unroll
-            for (int i = 0; i < P; ++i)
-#pragma unroll
-                for (int j = 0; j < P; ++j) mx = max(mx, __float_as_uint(d[i][j]) & 0x7fffffffu);
-            block_max_atomic(amax, key, mx);
         }
         float tmp[P][P];
 #pragma unroll
@@ -213,80 +186,8 @@ output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, cons
     }
 }
 
-// ---------------------------------------------------------------------------------
-// K4: dZ = A1·dÕ·A2ᵀ with ψ⁻¹ gather, zero at padded positions, optional ReLU mask
-//     (layer.cpp:107-116, transforms.cpp:228-241, train.cpp:193)
-// One thread per (k, nt < NTs); padding columns nt ≥ NT are written as zeros.
-// ---------------------------------------------------------------------------------
-template <int M, int P, bool MASK, class CF>
-__global__ void __launch_bounds__(256)
-grad_z_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out,
-              float* __restrict__ DZ, const Coefs cf, int K, int Ho, int Wo, int tiles_x, int T,
-              int NT, int NTs, int NTr, unsigned* __restrict__ amax = nullptr, int seg_imgs = 1) {
-    // amax != nullptr: also max|dO| (after the mask) per (segment, k), as input_transform_kernel
-    const int64_t plane = (int64_t)K * NTs;
-    const int64_t items = (int64_t)K * NTr;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
-         gid += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(gid / NTr);
-        const int nt = (int)(gid - (int64_t)k * NTr);
-        float d[M][M];
-        int key = -1;
-        if (nt < NT) {
-            const int n = nt / T, t = nt - n * T;
-            const int ty = t / tiles_x, tx = t - ty * tiles_x;
-            const int64_t base = ((int64_t)n * K + k) * Ho * Wo;
-            if (amax) key = (n / seg_imgs) * K + k;
-#pragma unroll
-            for (int y = 0; y < M; ++y) {
-                const int oy = ty * M + y;
-#pragma unroll
-                for (int x = 0; x < M; ++x) {
-                    const int ox = tx * M + x;
-                    float v = 0.f;
-                    if (oy < Ho && ox < Wo) {
-                        const int64_t o = base + oy * Wo + ox;
-                        v = __ldg(dO + o);
-                        if (MASK) v = __fmul_rn(v, __ldg(relu_out + o) > 0.f ? 1.f : 0.f);
-                    }
-                    d[y][x] = v;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int y = 0; y < M; ++y)
-#pragma unroll
-                for (int x = 0; x < M; ++x) d[y][x] = 0.f;
-        }
-        if (amax) {
-            unsigned mx = 0;
-#pragma unroll
-            for (int y = 0; y < M; ++y)
-#pragma unroll
-                for (int x = 0; x < M; ++x) mx = max(mx, __float_as_uint(d[y][x]) & 0x7fffffffu);
-            block_max_atomic(amax, key, mx);
-        }
-        float m1[P][M];  // m1(i,x) = Σ_y a1(i,y)·d(y,x)
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-#pragma unroll
-            for (int x = 0; x < M; ++x) {
-                float acc = 0.f;
-#pragma unroll
-                for (int y = 0; y < M; ++y) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), d[y][x]);
-                m1[i][x] = acc;
-            }
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-#pragma unroll
-            for (int j = 0; j < P; ++j) {  // dz(i,j) = Σ_x m1(i,x)·a2(j,x)
-                float acc = 0.f;
-#pragma unroll
-                for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), m1[i][x]);
-                DZ[(int64_t)(i * P + j) * plane + (int64_t)k * NTs + nt] = acc;
-            }
-    }
-}
+// K4 (dZ = A1·dÕ·A2ᵀ, ψ⁻¹ gather, ReLU mask) runs fused with the exact dW_F digits:
+// grad_z_digits_kernel (wino_xdw.cuh).
 
 // ---------------------------------------------------------------------------------
 // K7: dI = Σ_φ B1·dĨ_F·B2ᵀ — fused B-transform + deterministic halo gather-sum

@@ -112,21 +112,82 @@ __device__ __forceinline__ void to_digits(double x, double scale, uint32_t& lo, 
     hi = ((uint32_t)(b >> 32) & 0xffu) ^ 0x80u;
 }
 
-// Block-wide copy-out of the staged digit words: item g0..g0+3 of the block (same row: ncols_pad
-// is a multiple of 4) -> one u32 per digit plane.
-__device__ __forceinline__ void store_digit_groups(const uint32_t* slo, const uint8_t* shi, int P2, int R,
-                                                   int ncols_pad, int64_t items, int8_t* __restrict__ dig,
-                                                   int64_t NTd, int64_t plane, int col0) {
-    for (int idx = threadIdx.x; idx < P2 * (kTileItems / 4); idx += blockDim.x) {
-        const int s = idx / (kTileItems / 4), g = idx - s * (kTileItems / 4);
-        const int64_t g0 = (int64_t)blockIdx.x * kTileItems + 4 * g;
-        if (g0 >= items) continue;
-        const int r = (int)(g0 / ncols_pad), j = (int)(g0 - (int64_t)r * ncols_pad);
+// max|x| per (segment, row) of x = [n][R][HW] images (MASK: of x·[relu > 0], the masked dO of
+// train.cpp:193): amax[(n / seg_imgs)·R + r] as float bits (atomicMax: non-negative floats order
+// as their bits).  One warp per (n, r) plane; the a-priori exponent bound of the digits.
+template <bool MASK>
+__global__ void __launch_bounds__(256)
+plane_amax_kernel(const float* __restrict__ x, const float* __restrict__ relu, unsigned* __restrict__ amax, int R,
+                  int HW, int seg_imgs, int n_planes) {
+    const int lane = threadIdx.x & 31;
+    for (int pl = blockIdx.x * 8 + (threadIdx.x >> 5); pl < n_planes; pl += gridDim.x * 8) {
+        const float* src = x + (int64_t)pl * HW;
+        const float* rl = MASK ? relu + (int64_t)pl * HW : nullptr;
+        unsigned mx = 0;
+        if ((HW & 3) == 0) {
+            const float4* s4 = reinterpret_cast<const float4*>(src);
+            const float4* r4 = reinterpret_cast<const float4*>(rl);
+#pragma unroll 4
+            for (int i = lane; i < (HW >> 2); i += 32) {
+                float4 v = __ldg(s4 + i);
+                if (MASK) {
+                    const float4 r = __ldg(r4 + i);
+                    v.x = r.x > 0.f ? v.x : 0.f;
+                    v.y = r.y > 0.f ? v.y : 0.f;
+                    v.z = r.z > 0.f ? v.z : 0.f;
+                    v.w = r.w > 0.f ? v.w : 0.f;
+                }
+                mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                                 max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+            }
+        } else {
+#pragma unroll 4
+            for (int i = lane; i < HW; i += 32) {
+                float v = __ldg(src + i);
+                if (MASK && !(__ldg(rl + i) > 0.f)) v = 0.f;
+                mx = max(mx, __float_as_uint(v) & 0x7fffffffu);
+            }
+        }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        const int n = pl / R, r = pl - n * R;
+        if (lane == 0) atomicMax(amax + (int64_t)(n / seg_imgs) * R + r, mx);
+    }
+}
+
+// Shared-memory staging of the digits: [P2][kTileItems] words (digits 0..3) + [P2][kTileItems]
+// bytes (digit 4) + the P2 per-slice scales.
+template <int P2>
+constexpr int digit_smem_bytes() {
+    return P2 * kTileItems * 5 + P2 * 8;
+}
+
+// Per-block prologue: the scale 2^(38-E) of each slice from the row's segment maximum (E written
+// once per (slice, row) by the row's first column block).
+__device__ __forceinline__ void slice_scales(double* ssc, const Norms& nrm, int P2, const unsigned* amax, int row,
+                                             int R, int* Eout) {
+    if ((int)threadIdx.x < P2) {
+        const double amx = (double)__uint_as_float(__ldg(amax + row));
+        const int E = bound_exp(nrm.v[threadIdx.x] * amx);
+        ssc[threadIdx.x] = pow2(kScaleBits - E);
+        if (blockIdx.x == 0) Eout[threadIdx.x * R + row] = E;
+    }
+}
+
+// Block-wide copy-out of the staged digits of row `row`, block columns [jb, jb + kTileItems)
+// (only those < ncols_pad): four columns of one slice per thread and step -> one u32 per plane.
+__device__ __forceinline__ void store_digit_rows(const uint32_t* slo, const uint8_t* shi, int P2, int R, int row,
+                                                 int jb, int ncols_pad, int8_t* __restrict__ dig, int64_t NTd,
+                                                 int64_t plane, int col0) {
+    constexpr int G = kTileItems / 4;
+    for (int idx = threadIdx.x; idx < P2 * G; idx += kTileItems) {
+        const int s = idx / G, g = idx - s * G;
+        const int col = jb + 4 * g;
+        if (col >= ncols_pad) continue;
         const uint4 w = *reinterpret_cast<const uint4*>(slo + s * kTileItems + 4 * g);
         const uint32_t h = *reinterpret_cast<const uint32_t*>(shi + s * kTileItems + 4 * g);
         const uint32_t t01 = __byte_perm(w.x, w.y, 0x5140), t23 = __byte_perm(w.z, w.w, 0x5140);
         const uint32_t u01 = __byte_perm(w.x, w.y, 0x7362), u23 = __byte_perm(w.z, w.w, 0x7362);
-        int8_t* dst = dig + ((int64_t)s * R + r) * NTd + col0 + j;
+        int8_t* dst = dig + ((int64_t)s * R + row) * NTd + col0 + col;
         *reinterpret_cast<uint32_t*>(dst) = __byte_perm(t01, t23, 0x5410);
         *reinterpret_cast<uint32_t*>(dst + plane) = __byte_perm(t01, t23, 0x7632);
         *reinterpret_cast<uint32_t*>(dst + 2 * plane) = __byte_perm(u01, u23, 0x5410);
@@ -135,25 +196,30 @@ __device__ __forceinline__ void store_digit_groups(const uint32_t* slo, const ui
     }
 }
 
-// Ĩ_F digits of one segment: images [0, ncols/T) of `in` (offset to the segment's first image),
-// digit columns [col0, col0 + ncols_pad).  Block = 256 consecutive (c, column) items; the f64
-// transform is the reference's (layer.cpp:55-59 with f64 TransformSet values).
+// K1 fused with the Ĩ_F digits of one exponent segment.  Grid (column blocks, C): c = blockIdx.y,
+// segment column j = n·T + t (`in` and V offset to the segment's first image).  From one φ gather:
+//   V(s, c, j)      fp32, bitwise K1 (the reference's f32 order, transforms.cpp:196-210), j < vcols
+//                   (columns >= ncols are the batch's zero padding);
+//   digits(s, c, j) the reference's f64 B1ᵀ·d·B2 (layer.cpp:55-59) as DIG digits, j < ncols_pad.
+// Row i of both products at a time keeps the working set at d plus one row.
 template <int M, int P, class CF>
 __global__ void __launch_bounds__(kTileItems, (P <= 6) ? 2 : 1)
-input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int* __restrict__ Eout,
-                    const unsigned* __restrict__ amax, const CoefsD cf, const Norms nrm, int C, int H, int W,
-                    int pad, int tiles_x, int T, int ncols, int ncols_pad, int64_t NTd, int64_t plane, int col0) {
+input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ V, int8_t* __restrict__ dig,
+                              int* __restrict__ Eout, const unsigned* __restrict__ amax, const Coefs cf,
+                              const CoefsD cfd, const Norms nrm, int C, int H, int W, int pad, int tiles_x, int T,
+                              int ncols, int vcols, int ncols_pad, int64_t NTs, int64_t NTd, int64_t plane,
+                              int col0) {
     constexpr int P2 = P * P;
     extern __shared__ __align__(16) uint32_t xdw_smem[];
     uint32_t* slo = xdw_smem;
     uint8_t* shi = reinterpret_cast<uint8_t*>(xdw_smem + P2 * kTileItems);
-    const int64_t items = (int64_t)C * ncols_pad;
-    const int64_t gid = (int64_t)blockIdx.x * kTileItems + threadIdx.x;
-    const bool valid = gid < items;
-    const int c = valid ? (int)(gid / ncols_pad) : 0;
-    const int j = valid ? (int)(gid - (int64_t)c * ncols_pad) : 0;
+    double* ssc = reinterpret_cast<double*>(shi + P2 * kTileItems);
+    const int c = blockIdx.y;
+    const int jb = blockIdx.x * kTileItems;
+    const int j = jb + threadIdx.x;
+    slice_scales(ssc, nrm, P2, amax, c, C, Eout);
     float d[P][P];
-    if (valid && j < ncols) {
+    if (j < ncols) {
         const int n = j / T, t = j - n * T;
         const int ty = t / tiles_x, tx = t - ty * tiles_x;
         const int y0 = ty * M - pad, x0 = tx * M - pad;
@@ -174,59 +240,76 @@ input_digits_kernel(const float* __restrict__ in, int8_t* __restrict__ dig, int*
 #pragma unroll
             for (int k = 0; k < P; ++k) d[i][k] = 0.f;
     }
-    const double amx = valid ? (double)__uint_as_float(__ldg(amax + c)) : 0.0;
-    // row i of B1ᵀ·d first (P doubles live), then its P outputs: keeps the f64 working set small
+    __syncthreads();  // scales
+    const bool vok = j < vcols;
+    float* vp = V + (int64_t)c * NTs + j;
+    const int64_t vplane = (int64_t)C * NTs;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        double tmp[P];
+        float t32[P];
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + i), d[k][l]);
+            t32[l] = acc;
+        }
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + l), t32[k]);
+            if (vok) vp[(int64_t)(i * P + l) * vplane] = acc;
+        }
+        double t64[P];
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cf, k * P + i), (double)d[k][l]);
-            tmp[l] = acc;
+            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cfd, k * P + i), (double)d[k][l]);
+            t64[l] = acc;
         }
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cf, k * P + l), tmp[k]);
+            for (int k = 0; k < P; ++k) acc = dmadd<CF>(acc, coef_bd<CF, M, P>(cfd, k * P + l), t64[k]);
             const int s = i * P + l;
-            const int E = bound_exp(nrm.v[s] * amx);
             uint32_t lo, hi;
-            to_digits(acc, pow2(kScaleBits - E), lo, hi);
+            to_digits(acc, ssc[s], lo, hi);
             slo[s * kTileItems + threadIdx.x] = lo;
             shi[s * kTileItems + threadIdx.x] = (uint8_t)hi;
-            if (valid && j == 0) Eout[s * C + c] = E;
         }
     }
     __syncthreads();
-    store_digit_groups(slo, shi, P2, C, ncols_pad, items, dig, NTd, plane, col0);
+    store_digit_rows(slo, shi, P2, C, c, jb, ncols_pad, dig, NTd, plane, col0);
 }
 
-// dZ digits of one segment from dO (ψ⁻¹ gather, zero at padded positions, optional ReLU mask):
-// dZ = A1·dÕ·A2ᵀ in f64 (layer.cpp:107-116).
+// K4 fused with the dZ digits of one exponent segment (grid (column blocks, K), k = blockIdx.y):
+// the ψ⁻¹ gather of dO (zero at padded positions, optional ReLU mask, train.cpp:193), then
+//   DZ(s, k, j)     fp32 A1·dÕ·A2ᵀ, bitwise the reference's f32 order (layer.cpp:107-116), j < vcols;
+//   digits(s, k, j) the same product in the reference's f64, j < ncols_pad.
 template <int M, int P, bool MASK, class CF>
 __global__ void __launch_bounds__(kTileItems, (P <= 6) ? 2 : 1)
-grad_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out, int8_t* __restrict__ dig,
-                   int* __restrict__ Eout, const unsigned* __restrict__ amax, const CoefsD cf, const Norms nrm,
-                   int K, int Ho, int Wo, int tiles_x, int T, int ncols, int ncols_pad, int64_t NTd, int64_t plane,
-                   int col0) {
+grad_z_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out, float* __restrict__ DZ,
+                     int8_t* __restrict__ dig, int* __restrict__ Eout, const unsigned* __restrict__ amax,
+                     const Coefs cf, const CoefsD cfd, const Norms nrm, int K, int Ho, int Wo, int tiles_x, int T,
+                     int ncols, int vcols, int ncols_pad, int64_t NTs, int64_t NTd, int64_t plane, int col0) {
     constexpr int P2 = P * P;
     extern __shared__ __align__(16) uint32_t xdw_smem[];
     uint32_t* slo = xdw_smem;
     uint8_t* shi = reinterpret_cast<uint8_t*>(xdw_smem + P2 * kTileItems);
-    const int64_t items = (int64_t)K * ncols_pad;
-    const int64_t gid = (int64_t)blockIdx.x * kTileItems + threadIdx.x;
-    const bool valid = gid < items;
-    const int k = valid ? (int)(gid / ncols_pad) : 0;
-    const int j = valid ? (int)(gid - (int64_t)k * ncols_pad) : 0;
+    double* ssc = reinterpret_cast<double*>(shi + P2 * kTileItems);
+    const int k = blockIdx.y;
+    const int jb = blockIdx.x * kTileItems;
+    const int j = jb + threadIdx.x;
+    slice_scales(ssc, nrm, P2, amax, k, K, Eout);
     float d[M][M];
 #pragma unroll
     for (int y = 0; y < M; ++y)
 #pragma unroll
         for (int x = 0; x < M; ++x) d[y][x] = 0.f;
-    if (valid && j < ncols) {
+    if (j < ncols) {
         const int n = j / T, t = j - n * T;
         const int ty = t / tiles_x, tx = t - ty * tiles_x;
         const int64_t base = ((int64_t)n * K + k) * Ho * Wo;
@@ -239,39 +322,55 @@ grad_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_
                 if (oy < Ho && ox < Wo) {
                     const int64_t o = base + oy * Wo + ox;
                     float v = __ldg(dO + o);
-                    if (MASK && !(__ldg(relu_out + o) > 0.f)) v = 0.f;
+                    if (MASK) v = __fmul_rn(v, __ldg(relu_out + o) > 0.f ? 1.f : 0.f);
                     d[y][x] = v;
                 }
             }
         }
     }
-    const double amx = valid ? (double)__uint_as_float(__ldg(amax + k)) : 0.0;
+    __syncthreads();  // scales
+    const bool vok = j < vcols;
+    float* zp = DZ + (int64_t)k * NTs + j;
+    const int64_t zplane = (int64_t)K * NTs;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        double m1[M];  // row i of A1·dÕ
+        float m32[M];  // row i of A1·dÕ
+#pragma unroll
+        for (int x = 0; x < M; ++x) {
+            float acc = 0.f;
+#pragma unroll
+            for (int y = 0; y < M; ++y) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), d[y][x]);
+            m32[x] = acc;
+        }
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            float acc = 0.f;
+#pragma unroll
+            for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, l * M + x), m32[x]);
+            if (vok) zp[(int64_t)(i * P + l) * zplane] = acc;
+        }
+        double m64[M];
 #pragma unroll
         for (int x = 0; x < M; ++x) {
             double acc = 0.0;
 #pragma unroll
-            for (int y = 0; y < M; ++y) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cf, i * M + y), (double)d[y][x]);
-            m1[x] = acc;
+            for (int y = 0; y < M; ++y) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cfd, i * M + y), (double)d[y][x]);
+            m64[x] = acc;
         }
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             double acc = 0.0;
 #pragma unroll
-            for (int x = 0; x < M; ++x) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cf, l * M + x), m1[x]);
+            for (int x = 0; x < M; ++x) acc = dmadd<CF>(acc, coef_ad<CF, M, P>(cfd, l * M + x), m64[x]);
             const int s = i * P + l;
-            const int E = bound_exp(nrm.v[s] * amx);
             uint32_t lo, hi;
-            to_digits(acc, pow2(kScaleBits - E), lo, hi);
+            to_digits(acc, ssc[s], lo, hi);
             slo[s * kTileItems + threadIdx.x] = lo;
             shi[s * kTileItems + threadIdx.x] = (uint8_t)hi;
-            if (valid && j == 0) Eout[s * K + k] = E;
         }
     }
     __syncthreads();
-    store_digit_groups(slo, shi, P2, K, ncols_pad, items, dig, NTd, plane, col0);
+    store_digit_rows(slo, shi, P2, K, k, jb, ncols_pad, dig, NTd, plane, col0);
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
