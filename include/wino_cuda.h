@@ -203,37 +203,32 @@ WINO_API int wino_update_status(wino_plan* plan, int64_t* nonfinite);
 WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
 
 /* Plan options.
- *   WINO_OPT_DW_MODE: how the sparse plan computes dW_F on the mask (layer.cpp:118-128):
- *     0 (default) masked SDDMM — exact fp64 products and accumulation of the fp32 operands;
- *     1 tensor cores — the accurate 3xTF32 tcgen05 GEMM over all K×C (per-k-block fp64
- *       folding, ~2e-7 of Σ|dz·x|), then the surviving entries gathered in CSR order.
- *       Faster whenever the density is above a few percent; requires C, K multiples of 4.
- *     2 precise — the forward also stores the fp32 residual of Ĩ_F (and backward_weights that of
- *       dZ), each recomputed in fp64 with the reference's coefficients; the SDDMM forms
- *       zh·xh + zh·xl + zl·xh exactly in fp64, so dW_F matches the reference's f64 layer on
- *       every element (no fp32-storage floor).  ~2× the SDDMM time and 2× the cache memory;
- *       caches created before the switch allocate their residual buffers on first use.
- *     3 int8 tensor cores — dZ and Ĩ_F split into 5 signed base-2^7 digits per value with one
- *       exponent per 128-long block, the 15 digit pairs of weight < 5 multiplied exactly on
- *       tcgen05 kind::i8 into int32 TMEM, blocks summed in fp64: the exact dot products of the
- *       stored fp32 operands like mode 0 (within one fp32 rounding of it), then the surviving
- *       entries gathered in CSR order.  Requires C, K multiples of 4; measured slower than
- *       mode 0 on the BASELINE shapes. */
+ *   WINO_OPT_DW_MODE: how dW_F (layer.cpp:118-128, on the mask of train.cpp:281-283) is computed.
+ *     0 (default, the only mode): exact — Ĩ_F and dZ recomputed in the reference's f64 by the
+ *       fused K1/K4 kernels and written as 5 balanced base-256 int8 digits (one exponent per
+ *       (segment, slice, row) from max|I| / max|dO|); the 15 high-weight digit pairs are
+ *       multiplied exactly on tcgen05 kind::i8 into int32 TMEM, combined and chunk-summed in fp64,
+ *       then gathered on the mask in CSR order.  Matches the reference's f64 layer within the
+ *       strict per-element bound (~2^-35 of Σ|products|).  Other values: WINO_INVALID_ARGUMENT. */
 #define WINO_OPT_DW_MODE 1
 /*   WINO_OPT_CONTRACTION: how a sparse plan runs Z = W_F·Ĩ_F and dĨ_F = W_Fᵀ·dZ:
  *     0 (default) the CSR kernels — the reference's association order, forward bitwise equal
  *       to sparse_forward<float>;
  *     1 tensor cores — the 3xTF32 tcgen05 GEMM (per-k-block fp64 folding) over the zero-filled
- *       W_F slices; fp32-level accuracy (within the north_star tolerance, not bitwise), faster
- *       than the SIMT CSR kernels above ~5-10% density.  Masked coordinates stay exactly zero
- *       (the operands are re-scattered from the CSR values on every update).
- *       Requires C, K multiples of 4.  dW_F still follows WINO_OPT_DW_MODE. */
-/*     2 auto — tensor cores (for Z, dĨ_F and, in dW mode 0, a tensor-core dW + mask gather) when
- *       the plan's density reaches WINO_OPT_AUTO_DENSITY per mille (default 80), else the CSR
- *       kernels; re-decided whenever the weights change.  Fastest across the density sweep, with
- *       fp32-level (not bitwise / floor-exact) results on the tensor-core side. */
+ *       W_F slices; fp32-level accuracy (within the north_star tolerance, not bitwise).  Masked
+ *       coordinates stay exactly zero (the operands are re-scattered from the CSR values on
+ *       every update).  Requires C, K multiples of 4.
+ *     2 auto — tensor cores when the plan's density reaches WINO_OPT_AUTO_DENSITY per mille
+ *       (default 80), else the CSR kernels; re-decided whenever the weights change. */
 #define WINO_OPT_CONTRACTION 2
 #define WINO_OPT_AUTO_DENSITY 3
+/*   WINO_OPT_SPMM_OPERANDS: where the CSR kernels keep their dense operand chunk (Ĩ_F / dZ):
+ *     0 (default) auto — tensor memory (tcgen05.ld, operand rows spread over the lane quarters
+ *       by stage, wino_spmm_tm.cuh) when 128 < rows <= 512, the density is >= 7% and the work
+ *       units fill the GPU twice; shared memory otherwise;
+ *     1 shared memory always; 2 tensor memory whenever 128 < rows <= 512.  All are bitwise the
+ *     reference's order. */
+#define WINO_OPT_SPMM_OPERANDS 4
 WINO_API int wino_set_option(wino_plan* plan, int option, int value);
 
 /* ---------------------------------------------------------------------------- */

@@ -132,6 +132,7 @@ SIGNATURES = {
 WINO_OPT_DW_MODE = 1
 WINO_OPT_CONTRACTION = 2
 WINO_OPT_AUTO_DENSITY = 3
+WINO_OPT_SPMM_OPERANDS = 4
 WINO_FWD_RELU = 1
 WINO_BWD_RELU_MASK = 1
 

@@ -19,6 +19,7 @@
 #include "wino_tmap.h"
 #include "wino_update.cuh"
 #include "wino_xdw.cuh"
+#include "wino_spmm_tm.cuh"
 
 namespace {
 
@@ -208,6 +209,19 @@ struct wino_plan {
     int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc when dense enough)
     int auto_permille = 80;    // auto: tensor cores at density >= this / 1000 (measured crossover 5-10%)
     int64_t* d_slice_off = nullptr;
+    // TMEM SpMM (wino_spmm_tm.cuh): the padded stage-segment streams of the CSR [0] and CSC [1],
+    // rebuilt whenever the structure changes, values refreshed by wino_values_updated
+    int spmm_operands = 0;  // WINO_OPT_SPMM_OPERANDS: 0 auto, 1 shared memory, 2 tensor memory
+    struct TmStream {        // the TMEM SpMM's padded stage-segment stream of one direction
+        int2* cv = nullptr;  // (TMEM column, value)
+        int* pidx = nullptr; // source entry (-1: pad)
+        int* bnd = nullptr;  // [P2][rows][S+1] segment starts
+        int* cnt = nullptr;  // [P2·rows + 1] scan scratch
+        size_t cap_cv = 0, cap_pidx = 0, cap_bnd = 0, cap_cnt = 0;
+        int64_t n = 0;       // stream length
+        int64_t max_slice = 0;
+        bool ready = false;
+    } tms[2];
     double* d_xpart = nullptr;  // exact dW_F: scaled fp64 products per accumulation chunk [chunk][P2][K][C]
     size_t xpart_cap = 0;
     // scratch
@@ -427,10 +441,86 @@ int launch_spmm_r(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, co
 // X, Y may point at column `a` of their rows (a column range of the batch): NT = valid columns
 // of the range, NTs = the row stride, NTr = columns the range owns (≥ NT on the batch's last range,
 // which also owns the zero padding).  The whole batch: NTr = NTs.
+bool tm_applies(const wino_plan* p, int ncols) { return p->spmm_operands != 1 && ncols > 128 && ncols <= 512; }
+
+// Build the TMEM SpMM stream of direction dir (0: CSR rows K over C columns, 1: CSC rows C over K)
+// for the current structure and values (device-synchronous: at weight-set time only).
+int build_tm_stream(wino_plan* p, int dir) {
+    namespace t = wino::tm;
+    auto& ts = p->tms[dir];
+    ts.ready = false;
+    const int nrows = dir ? p->C : p->K, ncols = dir ? p->K : p->C;
+    if (!(ncols > 128 && ncols <= 512) || p->nnz == 0) return WINO_OK;
+    const int S = t::stages_for(ncols);
+    const int* rowptr = dir ? p->d_colptr : p->d_rowptr;
+    const int2* cv = dir ? p->d_cvT : p->d_cv;
+    const int64_t rows = (int64_t)p->P2 * nrows;
+    int rc;
+    if ((rc = grow(&ts.cnt, &ts.cap_cnt, (size_t)rows + 1)) || (rc = grow(&ts.bnd, &ts.cap_bnd, (size_t)rows * (S + 1))))
+        return rc;
+    t::tm_count_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, nrows, p->P2, S, ts.cnt);
+    t::tm_scan_kernel<<<1, 1024>>>(ts.cnt, (int)rows);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<int> off((size_t)rows + 1);
+    CUDA_TRY(cudaMemcpy(off.data(), ts.cnt, off.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    ts.n = off.back();
+    ts.max_slice = 0;
+    for (int s = 0; s < p->P2; ++s)
+        ts.max_slice = std::max<int64_t>(ts.max_slice, off[(size_t)(s + 1) * nrows] - off[(size_t)s * nrows]);
+    if ((rc = grow(&ts.cv, &ts.cap_cv, (size_t)ts.n + 2)) || (rc = grow(&ts.pidx, &ts.cap_pidx, (size_t)ts.n + 2)))
+        return rc;
+    t::tm_fill_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, ts.cnt, nrows, p->P2, S, ts.cv, ts.pidx,
+                                                                 ts.bnd);
+    p->launches += 3;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    ts.ready = true;
+    return WINO_OK;
+}
+
+int build_tm_streams(wino_plan* p) {
+    int rc = build_tm_stream(p, 0);
+    return rc ? rc : build_tm_stream(p, 1);
+}
+
+// K2/K6 with the X chunk in TMEM (wino_spmm_tm.cuh)
+int launch_spmm_tm(wino_plan* p, cudaStream_t st, int kind, const float* X, float* Y, int nrows, int ncols,
+                   int64_t NTs, int64_t NTr) {
+    namespace t = wino::tm;
+    const int dir = kind == K_SPMM_T ? 1 : 0;
+    const auto& ts = p->tms[dir];
+    const int S = t::stages_for(ncols);
+    const int TW = 512 / S;
+    const int chunks = (int)((NTr + TW - 1) / TW);
+    const int units = chunks * p->P2;
+    // stage each slice's stream in shared memory when the largest slice fits
+    const int staged_smem = t::smem_bytes(S, nrows, ts.max_slice);
+    const bool staged = staged_smem <= p->max_smem;
+    const int smem = std::max(staged ? staged_smem : t::smem_fixed(S), t::kMinSmem);
+    const unsigned long long z = 0x8000000080000000ull;  // (-0.f, -0.f)
+    const int grid = std::min(units, p->sm_count);
+    Launch L(p, st, kind);
+    auto go = [&](auto kern) {
+        set_smem_attr(kern, smem);
+        kern<<<grid, t::THREADS, smem, st>>>(ts.cv, ts.bnd, X, Y, nrows, ncols, (int)NTs, (int)NTr, chunks, units, z);
+    };
+    if (S == 2) staged ? go(t::spmm_tmem_kernel<2, true>) : go(t::spmm_tmem_kernel<2, false>);
+    else staged ? go(t::spmm_tmem_kernel<4, true>) : go(t::spmm_tmem_kernel<4, false>);
+    return L.done();
+}
+
 int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs, int64_t NTr = -1) {
     if (NTr < 0) NTr = NTs;
+    // TMEM operands where they pay (measured): their per-(row, stage) and per-unit
+    // costs are fixed, so they win once a row has enough entries (density >= 7%) and the units
+    // fill the GPU at least twice; below that the shared-memory kernel is faster
+    const double density = (double)p->nnz / ((double)p->P2 * p->K * p->C);
+    const int64_t tm_units = (NTr + 512 / wino::tm::stages_for(ncols) - 1) / (512 / wino::tm::stages_for(ncols)) * p->P2;
+    if (tm_applies(p, ncols) && p->tms[kind == K_SPMM_T ? 1 : 0].ready &&
+        (p->spmm_operands == 2 || (density >= 0.07 && tm_units >= 2 * p->sm_count)))
+        return launch_spmm_tm(p, st, kind, X, Y, nrows, ncols, NTs, NTr);
     switch (spmm_r(ncols)) {
         case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
         case 2: return launch_spmm_r<2>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);
@@ -804,6 +894,9 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
         std::memcpy(&bits, &val[e], 4);
         cv[e] = make_int2(col[e], bits);
     }
+    // one zero pad entry: the shared-memory SpMM stages whole 16-byte (col, value) pairs
+    cv.push_back(make_int2(0, 0));
+    cvT.push_back(make_int2(0, 0));
     auto up = [&](auto** dptr, const auto& hv) -> int {
         using T = typename std::decay_t<decltype(hv)>::value_type;
         CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), std::max<size_t>(1, hv.size()) * sizeof(T)));
@@ -829,6 +922,8 @@ int upload_csr(wino_plan* p, const std::vector<int>& rowptr, const std::vector<i
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
+    int rc2 = build_tm_streams(p);
+    if (rc2) return rc2;
     if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
@@ -915,10 +1010,13 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     CUDA_TRY(cudaMemcpy(colptr.data(), p->d_colptr, colptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
     const int64_t nnz = rowptr.back();
     if ((rc = grow(&p->d_colidx, &p->cap_colidx, (size_t)nnz)) || (rc = grow(&p->d_vals, &p->cap_vals, (size_t)nnz)) ||
-        (rc = grow(&p->d_rowof, &p->cap_rowof, (size_t)nnz)) || (rc = grow(&p->d_cv, &p->cap_cv, (size_t)nnz)) ||
+        (rc = grow(&p->d_rowof, &p->cap_rowof, (size_t)nnz)) || (rc = grow(&p->d_cv, &p->cap_cv, (size_t)nnz + 1)) ||
         (rc = grow(&p->d_rowidx, &p->cap_rowidx, (size_t)nnz)) || (rc = grow(&p->d_perm, &p->cap_perm, (size_t)nnz)) ||
-        (rc = grow(&p->d_cvT, &p->cap_cvT, (size_t)nnz)))
+        (rc = grow(&p->d_cvT, &p->cap_cvT, (size_t)nnz + 1)))
         return rc;
+    // one zero pad entry after the (col, value) streams: the shared-memory SpMM stages whole pairs
+    CUDA_TRY(cudaMemset(p->d_cv + nnz, 0, sizeof(int2)));
+    CUDA_TRY(cudaMemset(p->d_cvT + nnz, 0, sizeof(int2)));
     if (nnz > 0) {
         {
             Launch L(p, st, K_MISC);
@@ -947,6 +1045,7 @@ int compress_from_wsrc(wino_plan* p, double tol, int keep_all) {
     p->nnz = nnz;
     p->has_weights = true;
     p->dense = false;
+    if ((rc = build_tm_streams(p))) return rc;
     if (p->contraction_mode != 0) return apply_contraction(p);
     return WINO_OK;
 }
@@ -1101,6 +1200,9 @@ int wino_plan_destroy(wino_plan* p) {
     if (p->ev_dz) chk(cudaEventDestroy(p->ev_dz), "ev_dz");
     if (p->ev_join2) chk(cudaEventDestroy(p->ev_join2), "ev_join2");
     if (p->d_slice_off) chk(cudaFree(p->d_slice_off), "d_slice_off");
+    for (auto& ts : p->tms)
+        for (void* q : {(void*)ts.cv, (void*)ts.pidx, (void*)ts.bnd, (void*)ts.cnt})
+            if (q) chk(cudaFree(q), "tmem spmm stream");
     for (auto& r : p->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -1219,6 +1321,14 @@ int wino_values_updated(wino_plan* p, void* stream) {
     wino::refresh_values_kernel<<<grid_for(p->nnz, 256, p->sm_count), 256, 0, st>>>(p->d_cv, p->d_cvT, p->d_vals,
                                                                                    p->d_perm, p->nnz);
     rc = L.done();
+    for (int dir = 0; dir < 2 && rc == WINO_OK; ++dir) {
+        auto& ts = p->tms[dir];
+        if (!ts.ready) continue;
+        Launch L2(p, st, K_MISC);
+        wino::tm::tm_refresh_kernel<<<grid_for(ts.n, 256, p->sm_count), 256, 0, st>>>(ts.cv, ts.pidx,
+                                                                                      dir ? p->d_cvT : p->d_cv, ts.n);
+        rc = L2.done();
+    }
     if (rc == WINO_OK && p->tc_ready) rc = refresh_tc_operands(p, st);
     return rc;
 }
@@ -1708,6 +1818,12 @@ int wino_set_option(wino_plan* p, int option, int value) {
         if (value < 0 || value > 1000) return set_err(WINO_INVALID_ARGUMENT, "auto density is per mille, 0..1000");
         p->auto_permille = value;
         return p->contraction_mode == 2 ? apply_contraction(p) : WINO_OK;
+    }
+    if (option == WINO_OPT_SPMM_OPERANDS) {
+        if (value < 0 || value > 2)
+            return set_err(WINO_INVALID_ARGUMENT, "spmm operands: 0 auto, 1 shared memory, 2 tensor memory");
+        p->spmm_operands = value;
+        return p->has_weights && !p->dense ? build_tm_streams(p) : WINO_OK;
     }
     if (option == WINO_OPT_DW_MODE) {  // one dW_F path: the exact int8 digit GEMM (wino_xdw.cuh)
         if (value != 0) return set_err(WINO_INVALID_ARGUMENT, "dW mode: only 0 (exact) exists");

@@ -1,0 +1,364 @@
+// K2 / K6 with the operand chunk resident in tensor memory (128 < ncols <= 512).
+//
+//   Y(r, t) = Σ_{e ∈ row r} v_e · X(col_e, t)      (sparse.cpp:51-69; layer.cpp:145-155 on the mask)
+//
+// The shared-memory SpMM (wino_kernels.cuh) delivers 4 bytes of X per multiply-add through the
+// LSU pipe (~100 B/clk/SM for LDS.128), which caps it at ~25 multiply-adds/clk/SM.  TMEM reads
+// (tcgen05.ld.32x32b.x4: 4 columns of a warp's 32 lanes) sustain ~156 B/clk/SM, but only with
+// four columns per lane and nonzero, i.e. 4 consecutive t per lane -> 128 c of a 512-column TMEM.
+// So the X chunk of all ncols rows is spread over the lane quarters by STAGE:
+//
+//   S = ncols <= 256 ? 2 : 4 stages, stage j holds c ∈ [128j, 128j + 128);  TB = 4/S t-blocks,
+//   chunk width TW = 128·TB.  Lane quarter q = warp & 3 holds stage j = q / TB, t-block b = q % TB:
+//   TMEM lane 32q + l, columns 4c' .. 4c'+3  =  X(128j + c', t0 + 128b + 4l .. +3).
+//
+// A row's walk over its (column-sorted) CSR entries therefore passes through the S stages in
+// order: the warp of stage j applies the row's entries with c in stage j's range and hands its
+// accumulators (4 per lane) to the warp of stage j+1 through a shared-memory slot ring (mbarrier
+// full/empty).  Every output element is still one thread's left-to-right sum from +0 in CSR order
+// with each product rounded before the add (FFMA2 with a -0 addend = the rounded product, then
+// FADD2) — bitwise the reference's order and the shared-memory kernel.
+//
+// Persistent CTAs, one per SM (the whole TMEM), 16 warps: warp w = (quarter w & 3, row set w >> 2);
+// chain (t-block b, row set g) = the S warps that process rows r ≡ g (mod 4) for t-block b.  A
+// unit = (slice, chunk); its X chunk is written into TMEM by every warp for its own quarter
+// (coalesced 16-byte loads, tcgen05.st.32x32b.x16); the unit's slice of the CSR and its per-row
+// stage boundaries (precomputed once per CSR structure) are staged in shared memory when they fit,
+// else read warp-uniformly through L1.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wino {
+namespace tm {
+
+constexpr int THREADS = 1024;
+constexpr int ROWSETS = 8;   // warps per lane quarter
+constexpr int FILL_C = 128 / ROWSETS;  // stage rows c' each warp writes into TMEM
+constexpr int SLOTS = 4;        // handoff ring depth per (chain, stage boundary)
+constexpr int SLOT_BYTES = 512; // 32 lanes x 4 floats
+constexpr int TMEM_COLS = 512;
+
+__host__ __device__ constexpr int stages_for(int ncols) { return ncols <= 256 ? 2 : 4; }
+// handoff slots: chains x (S-1) boundaries x SLOTS (S=2: 8 chains, S=4: 4 chains -> <= 24 KB)
+__host__ __device__ constexpr int handoff_slots(int S) { return (4 / S) * ROWSETS * (S - 1) * SLOTS; }
+// handoff ring + barriers, then (STAGED) the slice's stage boundaries and its CSR entries
+__host__ __device__ constexpr int smem_fixed(int S) { return handoff_slots(S) * (SLOT_BYTES + 16) + 16; }
+__host__ __device__ constexpr int smem_bytes(int S, int nrows, int64_t entries) {
+    return smem_fixed(S) + ((nrows * (S + 1) + 3) & ~3) * 4 + (int)(entries * 8);
+}
+// > half the SM's shared memory: one CTA per SM (it owns all 512 TMEM columns)
+constexpr int kMinSmem = 120 * 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tld4(uint32_t taddr, float (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tst16(uint32_t taddr, const float4 (&v)[4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "f"(v[0].x), "f"(v[0].y), "f"(v[0].z), "f"(v[0].w), "f"(v[1].x), "f"(v[1].y), "f"(v[1].z), "f"(v[1].w),
+        "f"(v[2].x), "f"(v[2].y), "f"(v[2].z), "f"(v[2].w), "f"(v[3].x), "f"(v[3].y), "f"(v[3].z), "f"(v[3].w)
+        : "memory");
+}
+
+__device__ __forceinline__ int4 ldg_pair(const int2* p) {
+    int4 v;
+    asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int2 ldg_one(const int2* p) {
+    int2 v;
+    asm volatile("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+// acc += round(w·x) for two lanes' t at once: FFMA2 with the runtime -0 addend z is the rounded
+// product (ptxas cannot fuse it with the add), FADD2 the reference's rounded sum.
+__device__ __forceinline__ void madd2(unsigned long long& acc, float w, float x0, float x1, unsigned long long z) {
+    unsigned long long xv, wv, pr;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(xv) : "f"(x0), "f"(x1));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(wv) : "f"(w));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr) : "l"(xv), "l"(wv), "l"(z));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pr));
+}
+
+// ---- the kernel's operand stream: per (slice, row, stage) segments ----
+// For every (slice, row) and stage j the row's entries with col ∈ [128j, 128j+128), in CSR order,
+// as (TMEM column 4·(col − 128j), value), each segment padded to an even length with (the
+// segment's last column, +0) — an exact no-op for finite operands (the accumulator starts at +0
+// and is never -0, so adding ±0 leaves it unchanged) — so every segment starts on a 16-byte
+// entry pair.  tbnd[(s·nrows + r)·(S+1) + j] = start of segment j (j = S: the row's end), global
+// positions in the stream; tpidx = source entry of each stream entry (-1: pad), for value refreshes.
+__global__ void tm_count_kernel(const int* __restrict__ rowptr, const int2* __restrict__ cv, int nrows, int P2,
+                                int S, int* __restrict__ cnt) {
+    const int64_t total = (int64_t)P2 * nrows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i / nrows), r = (int)(i - (int64_t)s * nrows);
+        const int e0 = rowptr[(int64_t)s * (nrows + 1) + r], e1 = rowptr[(int64_t)s * (nrows + 1) + r + 1];
+        int n = 0, j = 0, len = 0;
+        for (int e = e0; e < e1; ++e) {
+            const int sj = cv[e].x >> 7;
+            if (sj != j) {
+                n += (len + 1) & ~1;
+                len = 0;
+                j = sj;
+            }
+            ++len;
+        }
+        cnt[i] = n + ((len + 1) & ~1);
+    }
+}
+
+// in-place exclusive scan of cnt[0..n) (one block of 1024 threads); cnt[n] = the total
+__global__ void __launch_bounds__(1024) tm_scan_kernel(int* __restrict__ cnt, int n) {
+    __shared__ int part[1024];
+    const int per = (n + 1023) / 1024;
+    const int a = threadIdx.x * per, b = min(n, a + per);
+    int s = 0;
+    for (int i = a; i < b; ++i) s += cnt[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const int v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - s;
+    for (int i = a; i < b; ++i) {
+        const int c = cnt[i];
+        cnt[i] = run;
+        run += c;
+    }
+    if (threadIdx.x == 1023) cnt[n] = part[1023];
+}
+
+__global__ void tm_fill_kernel(const int* __restrict__ rowptr, const int2* __restrict__ cv,
+                               const int* __restrict__ off, int nrows, int P2, int S, int2* __restrict__ tcv,
+                               int* __restrict__ tpidx, int* __restrict__ tbnd) {
+    const int64_t total = (int64_t)P2 * nrows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i / nrows), r = (int)(i - (int64_t)s * nrows);
+        const int e0 = rowptr[(int64_t)s * (nrows + 1) + r], e1 = rowptr[(int64_t)s * (nrows + 1) + r + 1];
+        int* b = tbnd + i * (S + 1);
+        int pos = off[i];
+        int e = e0;
+        for (int j = 0; j < S; ++j) {
+            b[j] = pos;
+            int last = 0, len = 0;
+            for (; e < e1 && (cv[e].x >> 7) == j; ++e, ++len) {
+                last = 4 * (cv[e].x & 127);
+                tcv[pos] = make_int2(last, cv[e].y);
+                tpidx[pos++] = e;
+            }
+            if (len & 1) {
+                tcv[pos] = make_int2(last, 0);
+                tpidx[pos++] = -1;
+            }
+        }
+        b[S] = pos;
+    }
+}
+
+// new values (same structure): stream entries take the value of their source entry
+__global__ void tm_refresh_kernel(int2* __restrict__ tcv, const int* __restrict__ tpidx, const int2* __restrict__ cv,
+                                  int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = tpidx[i];
+        if (e >= 0) tcv[i].y = cv[e].y;
+    }
+}
+
+// (col, value) entries from the staged slice in shared memory or warp-uniformly from global
+template <bool STAGED>
+__device__ __forceinline__ int4 fetch_pair(const int2* p) {
+    if constexpr (STAGED) return *reinterpret_cast<const int4*>(p);
+    else return ldg_pair(p);
+}
+template <bool STAGED>
+__device__ __forceinline__ int2 fetch_one(const int2* p) {
+    if constexpr (STAGED) return *p;
+    else return ldg_one(p);
+}
+
+// NB entries of the stream from e (NB, e even): their TMEM reads in flight together, one wait
+template <int NB, bool STAGED>
+__device__ __forceinline__ void batch(const int2* __restrict__ cv, int e, uint32_t tq,
+                                      unsigned long long (&acc)[2], unsigned long long z) {
+    int2 a[NB];
+#pragma unroll
+    for (int u = 0; u < NB; u += 2) {
+        const int4 two = fetch_pair<STAGED>(cv + e + u);
+        a[u] = make_int2(two.x, two.y);
+        a[u + 1] = make_int2(two.z, two.w);
+    }
+    float x[NB][4];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) tld4(tq + (uint32_t)a[u].x, x[u]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+        madd2(acc[0], __int_as_float(a[u].y), x[u][0], x[u][1], z);
+        madd2(acc[1], __int_as_float(a[u].y), x[u][2], x[u][3], z);
+    }
+}
+
+// One row segment [e, ee) of a stage (e, ee even): acc (4 t per lane as 2 packed pairs) += the
+// entries' rounded products in order, in batches of 8 and one final batch of 6, 4 or 2.
+template <bool STAGED>
+__device__ __forceinline__ void walk(const int2* __restrict__ cv, int e, int ee, uint32_t tq,
+                                     unsigned long long (&acc)[2], unsigned long long z) {
+    for (; e + 8 <= ee; e += 8) batch<8, STAGED>(cv, e, tq, acc, z);
+    const int rem = ee - e;
+    if (rem == 6) batch<6, STAGED>(cv, e, tq, acc, z);
+    else if (rem == 4) batch<4, STAGED>(cv, e, tq, acc, z);
+    else if (rem == 2) batch<2, STAGED>(cv, e, tq, acc, z);
+}
+
+// X, Y: [P2][ncols or nrows][NTs] (offset to a column range's first column; NTr = owned columns),
+// cv / bnd: the padded stage-segment stream and its segment starts (tm_fill_kernel), units =
+// P2 · chunks, z = -0.0f pair.  STAGED: each unit copies its slice of the stream (and the slice's
+// segment starts) into shared memory; otherwise both are read through L1.
+template <int S, bool STAGED>
+__global__ void __launch_bounds__(THREADS, 1)
+spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
+                 const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs, int NTr,
+                 int chunks, int units, unsigned long long z) {
+    constexpr int TB = 4 / S;
+    constexpr int TW = 128 * TB;
+    constexpr int NSLOT = handoff_slots(S);
+    extern __shared__ __align__(16) uint8_t tm_smem[];
+    float4* slots = reinterpret_cast<float4*>(tm_smem);                       // [NSLOT][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(tm_smem + NSLOT * SLOT_BYTES);
+    uint64_t* empty = full + NSLOT;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + NSLOT);
+    int* sbnd = reinterpret_cast<int*>(tm_smem + NSLOT * (SLOT_BYTES + 16) + 16);  // [nrows][S+1]
+    int2* scv = reinterpret_cast<int2*>(sbnd + ((nrows * (S + 1) + 3) & ~3));     // slice entries
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, g = warp >> 2;
+    const int st = q / TB, b = q % TB;
+    if (threadIdx.x < NSLOT) {
+        mb_init(&full[threadIdx.x], 1);
+        mb_init(&empty[threadIdx.x], 1);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tq = *tslot + ((uint32_t)(32 * q) << 16);
+    // the handoff rings of this warp's chain: into stage st (st > 0) and out of it (st < S-1)
+    const int chain = b * ROWSETS + g;
+    const int ring_in = (chain * (S - 1) + (st - 1)) * SLOTS;
+    const int ring_out = (chain * (S - 1) + st) * SLOTS;
+    int nrow_chain = 0;  // rows this chain has passed through its rings so far (all units)
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int s = u / chunks, ch = u - s * chunks;
+        const int t = ch * TW + 128 * b + 4 * lane;  // this lane's 4 columns
+        const bool tok = t < NTr;
+        // ---- stage the slice's boundaries and entries (cp.async, overlaps the fill) ----
+        const int* bs = bnd + (int64_t)s * nrows * (S + 1);
+        const int e_lo = STAGED ? __ldg(bs) : 0;  // even
+        if constexpr (STAGED) {
+            const int nb = nrows * (S + 1);
+            for (int i = threadIdx.x; i < nb; i += THREADS) sbnd[i] = __ldg(bs + i);
+            const int e_hi = __ldg(bs + nb - 1);  // even
+            const int n2 = (e_hi - e_lo) >> 1;      // whole 16-byte pairs
+            const int4* src = reinterpret_cast<const int4*>(cv + e_lo);
+            int4* dst = reinterpret_cast<int4*>(scv);
+            for (int i = threadIdx.x; i < n2; i += THREADS) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst + i)), "l"(src + i));
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // ---- fill: X(128·st + c', t .. t+3) for this warp's FILL_C c' -> TMEM columns 4c' ----
+        {
+            const float* xs = X + ((int64_t)s * ncols + 128 * st) * NTs + t;
+#pragma unroll
+            for (int h = 0; h < FILL_C / 4; ++h) {
+                float4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int cl = FILL_C * g + 4 * h + i;
+                    v[i] = (tok && 128 * st + cl < ncols)
+                               ? __ldg(reinterpret_cast<const float4*>(xs + (int64_t)cl * NTs))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                tst16(tq + (uint32_t)(4 * (FILL_C * g + 4 * h)), v);
+            }
+        }
+        if constexpr (STAGED) asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // ---- rows of this chain ----
+        const int* rb = STAGED ? sbnd : bs;
+        const int2* cvb = STAGED ? scv - e_lo : cv;  // indexed by global entry numbers
+        float* ys = Y + (int64_t)s * nrows * NTs + t;
+        for (int r = g; r < nrows; r += ROWSETS, ++nrow_chain) {
+            const int slot = nrow_chain % SLOTS;
+            const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
+            const int e = rb[r * (S + 1) + st], ee = rb[r * (S + 1) + st + 1];
+            unsigned long long acc[2] = {0ull, 0ull};
+            if (st > 0) {  // the previous stage's accumulators for this row
+                mb_wait(&full[ring_in + slot], par);
+                const float4 a = slots[(ring_in + slot) * 32 + lane];
+                asm("mov.b64 %0, {%1,%2};" : "=l"(acc[0]) : "f"(a.x), "f"(a.y));
+                asm("mov.b64 %0, {%1,%2};" : "=l"(acc[1]) : "f"(a.z), "f"(a.w));
+                __syncwarp();
+                if (lane == 0) mb_arrive(&empty[ring_in + slot]);
+            }
+            walk<STAGED>(cvb, e, ee, tq, acc, z);
+            float4 o;
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[0]));
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[1]));
+            if (st == S - 1) {
+                if (tok) *reinterpret_cast<float4*>(ys + (int64_t)r * NTs) = o;
+            } else {
+                if (nrow_chain >= SLOTS) mb_wait(&empty[ring_out + slot], par ^ 1u);
+                slots[(ring_out + slot) * 32 + lane] = o;
+                __syncwarp();
+                if (lane == 0) mb_arrive(&full[ring_out + slot]);
+            }
+        }
+        // every warp is done reading this chunk (and the staged slice) before the next unit
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "r"(TMEM_COLS));
+}
+
+}  // namespace tm
+}  // namespace wino

@@ -212,6 +212,12 @@ class WinogradLayer:
         'auto' (tensor cores at density >= set_auto_density's value, else 'csr')."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_CONTRACTION, {"csr": 0, "tc": 1, "auto": 2}[mode]))
 
+    def set_spmm_operands(self, where: str):
+        """CSR kernels' dense operand chunk: 'auto' (default; tensor memory where it is measured
+        faster: 128 < rows <= 512, density >= 7%, enough work units), 'smem' (shared memory always)
+        or 'tmem' (tensor memory whenever 128 < rows <= 512).  Bitwise the same results."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_SPMM_OPERANDS, {"auto": 0, "smem": 1, "tmem": 2}[where]))
+
     def set_auto_density(self, density: float):
         """Density from which contraction 'auto' uses the tensor cores (default 0.08)."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_AUTO_DENSITY, int(round(density * 1000))))

@@ -763,3 +763,47 @@ def test_dw_mode_option():
     for bad in ("sddmm", "tc", "precise", "int8"):
         with pytest.raises(wb.InvalidArgument):
             layer.set_dw_mode(bad)
+
+
+def _step_with_operands(img, w_f, go, where, lr=None):
+    n, c, h, w = img.shape
+    layer = wb.WinogradLayer(c, w_f.shape[0], h, w, pad=1, m=4)
+    layer.set_weights(w_f, dense=False)
+    layer.set_spmm_operands(where)
+    cache = layer.new_cache(n)
+    x, g = dev(img), dev(go)
+    outs = []
+    for _ in range(2 if lr else 1):
+        o = layer.forward(x, cache)
+        dw = layer.backward_weights(g, cache)
+        di = layer.backward_input(cache)
+        torch.cuda.synchronize()
+        outs.append((o.cpu().numpy(), dw.cpu().numpy(), di.cpu().numpy()))
+        if lr:
+            layer.sgd_step(dw, lr=lr, scale=1.0, l2=0.0)  # new values, same structure
+    layer.close()
+    return outs
+
+
+@pytest.mark.parametrize("c,k,h,n,sparsity", [(256, 256, 28, 4, 0.9), (256, 384, 13, 8, 0.9),
+                                              (512, 512, 14, 2, 0.5), (160, 200, 12, 3, 0.7),
+                                              (256, 256, 20, 3, 0.97)])
+def test_tmem_spmm_bitwise_equals_shared_memory(c, k, h, n, sparsity):
+    """The TMEM-resident CSR kernels (wino_spmm_tm.cuh: S = 2 and 4 stages, staged and global
+    stream, ragged row counts) give the shared-memory kernels' results bit for bit — O, dĨ_F -> dI,
+    and dW_F — before and after a value update (the padded stream's value refresh)."""
+    rng = np.random.default_rng(c * 1000 + k + h)
+    img = rng.standard_normal((n, c, h, h)).astype(np.float32)
+    go = rng.standard_normal((n, k, h, h)).astype(np.float32)
+    w_f = rng.standard_normal((k, c, 6, 6)) * np.sqrt(2.0 / (9 * c))
+    w_f *= rng.random(w_f.shape) >= sparsity
+    a = _step_with_operands(img, w_f, go, "tmem", lr=1e-3)
+    b = _step_with_operands(img, w_f, go, "smem", lr=1e-3)
+    for (oa, dwa, dia), (ob, dwb, dib) in zip(a, b):
+        assert np.array_equal(oa, ob), "O differs between TMEM and shared-memory operands"
+        assert np.array_equal(dia, dib), "dI differs between TMEM and shared-memory operands"
+        assert np.array_equal(dwa, dwb), "dW_F differs"
+    if c == 160:  # anchor the TMEM path itself to the reference's f32 operation order
+        mir = wo.layer_f32(img, wo.compress(w_f), go, m=4, pad=1)
+        assert np.array_equal(a[0][0], mir["o"])
+        assert np.array_equal(a[0][2], mir["di"])
