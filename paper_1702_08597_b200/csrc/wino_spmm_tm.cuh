@@ -263,8 +263,8 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     const int q = warp & 3, g = warp >> 2;
     const int st = q / TB, b = q % TB;
     if (threadIdx.x < NSLOT) {
-        mb_init(&full[threadIdx.x], 1);
-        mb_init(&empty[threadIdx.x], 1);
+        mb_init(&full[threadIdx.x], 32);  // every lane arrives after its own slot access
+        mb_init(&empty[threadIdx.x], 32);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
@@ -321,6 +321,16 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // ---- the next unit's chunk rows of this warp: L2 prefetch behind this unit's compute ----
+        if (u + (int)gridDim.x < units && lane < FILL_C) {
+            const int un = u + gridDim.x, sn = un / chunks, chn = un - sn * chunks;
+            const int cl = FILL_C * g + lane, tn = chn * TW + 128 * b;
+            if (128 * st + cl < ncols && tn < NTr) {
+                const float* src = X + ((int64_t)sn * ncols + 128 * st + cl) * NTs + tn;
+                const int bytes = 4 * min(128, NTr - tn);  // multiple of 16
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+            }
+        }
         // ---- rows of this chain ----
         const int* rb = STAGED ? sbnd : bs;
         const int2* cvb = STAGED ? scv - e_lo : cv;  // indexed by global entry numbers
@@ -335,8 +345,7 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
                 const float4 a = slots[(ring_in + slot) * 32 + lane];
                 asm("mov.b64 %0, {%1,%2};" : "=l"(acc[0]) : "f"(a.x), "f"(a.y));
                 asm("mov.b64 %0, {%1,%2};" : "=l"(acc[1]) : "f"(a.z), "f"(a.w));
-                __syncwarp();
-                if (lane == 0) mb_arrive(&empty[ring_in + slot]);
+                mb_arrive(&empty[ring_in + slot]);
             }
             walk<STAGED>(cvb, e, ee, tq, acc, z);
             float4 o;
@@ -347,8 +356,7 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
             } else {
                 if (nrow_chain >= SLOTS) mb_wait(&empty[ring_out + slot], par ^ 1u);
                 slots[(ring_out + slot) * 32 + lane] = o;
-                __syncwarp();
-                if (lane == 0) mb_arrive(&full[ring_out + slot]);
+                mb_arrive(&full[ring_out + slot]);
             }
         }
         // every warp is done reading this chunk (and the staged slice) before the next unit
