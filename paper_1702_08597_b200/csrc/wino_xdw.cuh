@@ -224,14 +224,36 @@ input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ 
         const int ty = t / tiles_x, tx = t - ty * tiles_x;
         const int y0 = ty * M - pad, x0 = tx * M - pad;
         const float* src = in + ((int64_t)n * C + c) * H * W;
+        if (M == 4 && P == 6 && pad == 1 && (W & 3) == 0) {
+            // row i of the patch = x0 - 0 .. x0 + 5 = 4tx-1 | 4tx .. 4tx+3 (one aligned 16-byte
+            // load, always inside the row) | 4tx+4
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-            const int y = y0 + i;
-            const bool yok = (unsigned)y < (unsigned)H;
+            for (int i = 0; i < P; ++i) {
+                const int y = y0 + i;
+                if ((unsigned)y < (unsigned)H) {
+                    const float* row = src + y * W + (x0 + 1);
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(row));
+                    d[i][0] = x0 >= 0 ? __ldg(row - 1) : 0.f;
+                    d[i][1] = v.x;
+                    d[i][2] = v.y;
+                    d[i][3] = v.z;
+                    d[i][4] = v.w;
+                    d[i][5] = x0 + 5 < W ? __ldg(row + 4) : 0.f;
+                } else {
 #pragma unroll
-            for (int k = 0; k < P; ++k) {
-                const int x = x0 + k;
-                d[i][k] = (yok && (unsigned)x < (unsigned)W) ? __ldg(src + y * W + x) : 0.f;
+                    for (int k = 0; k < P; ++k) d[i][k] = 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int y = y0 + i;
+                const bool yok = (unsigned)y < (unsigned)H;
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    const int x = x0 + k;
+                    d[i][k] = (yok && (unsigned)x < (unsigned)W) ? __ldg(src + y * W + x) : 0.f;
+                }
             }
         }
     } else {
