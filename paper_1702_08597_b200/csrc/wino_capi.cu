@@ -641,7 +641,7 @@ int launch_tc_gemm(wino_plan* p, cudaStream_t st, int kind, const CUtensorMap& a
     set_smem_attr(kern, tc::flush::WS_SMEM_BYTES);
     Launch L(p, st, kind);
     kern<<<std::min(ntiles, p->sm_count), 64 + 32 * (2 + 8), tc::flush::WS_SMEM_BYTES, st>>>(
-        ah, al, mb, md, mb, D, M, N, Kd, NTs, p->P2, 1, kb, tiles_n, tiles_m, ntiles);
+        ah, al, mb, md, D, M, N, Kd, NTs, p->P2, 1, kb, tiles_n, tiles_m, ntiles);
     return L.done();
 }
 
@@ -1333,12 +1333,6 @@ int wino_values_updated(wino_plan* p, void* stream) {
     return rc;
 }
 
-// Every reader of Ĩ_F and dZ on this plan is a tcgen05 GEMM through the warp-specialised kernel
-// (dense plan, or tensor-core contraction with the tensor-core dW): the producers then write the
-// tf32 hi/lo split once (input_transform_kernel / grad_z_kernel) and the GEMMs skip their own.
-// Opt-in (WINO_TC_PRESPLIT=1): measured at c3 dense 2041 vs 1945 µs — the dW GEMM gains (581 ->
-// 401 µs) but K1/K4 write twice the bytes (+50/+90 µs) and the forward/dĨ_F GEMMs, which were not
-// split-bound, load twice the B bytes (+25/+40 µs); c1 with the tensor-core contraction: 141 vs 148.
 int wino_cache_create(wino_plan* p, int n_max, wino_cache** out) {
     if (!p || !out || n_max <= 0) return set_err(WINO_INVALID_ARGUMENT, "bad argument");
     CUDA_TRY(cudaSetDevice(p->device));

@@ -205,165 +205,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
 }
 
-// grid = (ceil(N/BN), ceil(M/BM), slices·splits); blockIdx.z = s·splits + q.  The CTA reduces
-// k-blocks [q·kb_per, (q+1)·kb_per) and writes D + (q·slices + s)·M·ldd (rows < M, cols < N).
-// A_SPLIT: A arrives raw through mapAh and is split in shared memory (mapAl unused); otherwise
-// mapAh/mapAl hold the pre-split weights.  B_MN: B is MN-major [Kd][N] (else K-major [N][Kd]).
-template <bool A_SPLIT, bool B_MN>
-__global__ void __launch_bounds__(THREADS, 1)
-gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
-                   const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N, int Kd,
-                   int64_t ldd, int slices, int splits, int kb_per) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;                 // [STAGES] TMA landed
-    uint64_t* split = bars + STAGES;       // [STAGES] hi/lo ready (128 arrivals)
-    uint64_t* empty = bars + 2 * STAGES;   // [STAGES] MMAs done reading the stage
-    uint64_t* tmem_full = bars + 3 * STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-    const int s = blockIdx.z / splits, q = blockIdx.z - s * splits;
-    const int kb_total = (Kd + BK - 1) / BK;
-    const int kb0 = q * kb_per;
-    const int kblocks = max(0, min(kb_total, kb0 + kb_per) - kb0);
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&split[i], 128);
-            mbar_init(&empty[i], 1);
-        }
-        mbar_init(tmem_full, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(BN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int st = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
-                uint8_t* base = stage_ptr(st);
-                const int kk = (kb0 + kb) * BK;
-                mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
-                tma_load_3d(base, &mapAh, &full[st], kk, m0, s);
-                if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, m0, s);
-                if (B_MN) {
-#pragma unroll
-                    for (int j = 0; j < BN / 32; ++j)  // 8 MN atoms of 32 columns × BK rows
-                        tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], n0 + 32 * j, kk, s);
-                } else {
-                    tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, n0, s);  // BN rows × 128 B
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(B_MN);
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int st = kb % STAGES;
-                mbar_wait(&split[st], (kb / STAGES) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a_hi = smem_u32(stage_ptr(st));
-                const uint32_t a_lo = a_hi + A_TILE;
-                const uint32_t b_hi = a_hi + 2 * A_TILE;
-                const uint32_t b_lo = b_hi + B_TILE;
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-                    // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); +32 B per
-                    // K step inside the 128-byte swizzle row.
-                    const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
-                    const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
-                    uint64_t dbh, dbl;
-                    if (B_MN) {
-                        // MN-major SW128 with 32-byte atoms: 32-column (128 B) atoms BK*128 B apart
-                        // (LBO), 4-row K groups 512 B apart (SBO); +8 rows = 1024 B per K step.
-                        dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                        dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                    } else {
-                        dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
-                        dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
-                    }
-                    const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-                    mma_tf32(tmem, dah, dbh, idesc, acc0);
-                    mma_tf32(tmem, dah, dbl, idesc, 1u);
-                    mma_tf32(tmem, dal, dbh, idesc, 1u);
-                }
-                mma_commit(&empty[st]);
-            }
-            mma_commit(tmem_full);
-        }
-    } else if (warp >= 4) {
-        const int t = threadIdx.x - 128;  // 0..127
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const int st = kb % STAGES;
-            mbar_wait(&full[st], (kb / STAGES) & 1);
-            uint8_t* base = stage_ptr(st);
-            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t, 128);
-            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t, 128);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-            mbar_arrive(&split[st]);
-        }
-        // epilogue: TMEM lane = output row (warp quarter), columns = output columns
-        const int qd = warp & 3;
-        const int row = m0 + qd * 32 + lane;
-        float* drow = D + (((int64_t)q * slices + s) * M + row) * ldd;
-        if (kblocks == 0) {
-            if (row < M)
-                for (int c = 0; c < BN; ++c)
-                    if (n0 + c < N) drow[n0 + c] = 0.f;
-        } else {
-            mbar_wait(tmem_full, 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)c, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int col = n0 + c;
-                if (row < M) {
-                    if (col + 32 <= N && (ldd & 3) == 0) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4*>(drow + col + j) =
-                                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col + j < N) drow[col + j] = __uint_as_float(v[j]);
-                    }
-                }
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
-}
-
 // ---------------------------------------------------------------------------------------
-// Accurate variant: every k-block (32 reduction elements × 3 tf32 products) accumulates into a
-// FRESH TMEM accumulator (double-buffered), which the epilogue warps fold into fp64 registers.
-// Long fp32 accumulation chains inside TMEM are what cost 3xTF32 its accuracy (measured: error
-// /Σ|p| 2.4e-6 with 63 k-blocks per accumulator vs 4.6e-8 with one), so this variant lands at
-// the fp32-rounding level of the result.  Tile 128×128; 320 threads:
-//   warp 0 TMA · warp 1 TMEM alloc + MMA · warps 2-9 hi/lo split of the stage two k-blocks
-//   ahead, then the drain of this k-block's accumulator (warp w reads TMEM lane quarter w%4,
-//   column half (w-2)/4: 64 fp64 sums per thread).
+// The accurate tcgen05 GEMM: every k-block (32 reduction elements × 3 tf32 products) accumulates
+// into a FRESH TMEM accumulator, folded outside TMEM (long fp32 accumulation chains inside TMEM
+// are what cost 3xTF32 its accuracy — measured error/Σ|p| 2.4e-6 with 63 k-blocks per
+// accumulator vs 4.6e-8 with one).  Tile 128×128.  (Earlier generations — single-accumulator,
+// non-persistent and persistent-with-shared-epilogue-warps forms — are described with their
+// measurements in DESIGN.md §7.)
 // ---------------------------------------------------------------------------------------
 namespace flush {
 constexpr int BN = 128;
@@ -382,380 +230,25 @@ __host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
 }
 }  // namespace flush
 
-template <bool A_SPLIT, bool B_MN, int F>
-__global__ void __launch_bounds__(flush::THREADS, 1)
-gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
-                         const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N, int Kd,
-                         int64_t ldd, int slices, int splits, int kb_per) {
-    constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
-    constexpr int STAGE_BYTES = flush::STAGE_BYTES, TMEM_COLS = flush::TMEM_COLS;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;                       // [STAGES]
-    uint64_t* split = bars + STAGES;             // [STAGES] (64 arrivals)
-    uint64_t* empty = bars + 2 * STAGES;         // [STAGES]
-    uint64_t* tfull = bars + 3 * STAGES;         // [2]
-    uint64_t* tempty = bars + 3 * STAGES + 2;    // [2] (256 arrivals)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-    const int s = blockIdx.z / splits, q = blockIdx.z - s * splits;
-    const int kb_total = (Kd + BK - 1) / BK;
-    const int kb0 = q * kb_per;
-    const int kblocks = max(0, min(kb_total, kb0 + kb_per) - kb0);
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&split[i], 256);
-            mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 256);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int st = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
-                uint8_t* base = stage_ptr(st);
-                const int kk = (kb0 + kb) * BK;
-                mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
-                tma_load_3d(base, &mapAh, &full[st], kk, m0, s);
-                if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, m0, s);
-                if (B_MN) {
-#pragma unroll
-                    for (int j = 0; j < BN / 32; ++j)
-                        tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], n0 + 32 * j, kk, s);
-                } else {
-                    tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, n0, s);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id = flush::idesc(B_MN);
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int st = kb % STAGES, g = kb / F, b = g & 1;
-                const bool first = (kb % F) == 0, last = (kb % F) == F - 1 || kb == kblocks - 1;
-                if (first && g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-                mbar_wait(&split[st], (kb / STAGES) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a_hi = smem_u32(stage_ptr(st));
-                const uint32_t a_lo = a_hi + A_TILE;
-                const uint32_t b_hi = a_hi + 2 * A_TILE;
-                const uint32_t b_lo = b_hi + B_TILE;
-                const uint32_t acc = tmem + (uint32_t)(b * BN);
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-                    const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
-                    const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
-                    uint64_t dbh, dbl;
-                    if (B_MN) {
-                        dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                        dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                    } else {
-                        dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
-                        dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
-                    }
-                    mma_tf32(acc, dah, dbh, id, (first && k == 0) ? 0u : 1u);  // fresh per group
-                    mma_tf32(acc, dah, dbl, id, 1u);
-                    mma_tf32(acc, dal, dbh, id, 1u);
-#ifdef WINO_TC_FOUR_PRODUCTS  // lo·lo measured no accuracy gain (the MMA's internal sum dominates)
-                    mma_tf32(acc, dal, dbl, id, 1u);
-#endif
-                }
-                mma_commit(&empty[st]);
-                if (last) mma_commit(&tfull[b]);
-            }
-        }
-    } else {
-        const int t = threadIdx.x - 64;  // 0..255
-        const int qd = warp & 3, half = (warp - 2) >> 2;
-        auto split_stage = [&](int kb) {
-            const int st = kb % STAGES;
-            mbar_wait(&full[st], (kb / STAGES) & 1);
-            uint8_t* base = stage_ptr(st);
-            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, t, 256);
-            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, t, 256);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&split[st]);
-        };
-        for (int kb = 0; kb < min(kblocks, STAGES - 1); ++kb) split_stage(kb);
-        double accd[64];
-#pragma unroll
-        for (int j = 0; j < 64; ++j) accd[j] = 0.0;
-        for (int kb = 0; kb < kblocks; ++kb) {
-            if (kb + STAGES - 1 < kblocks) split_stage(kb + STAGES - 1);
-            if ((kb % F) != F - 1 && kb != kblocks - 1) continue;  // drain once per group
-            const int g = kb / F, b = g & 1;
-            mbar_wait(&tfull[b], (g >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + half * 64);
-            uint32_t v[32];
-            tmem_ld32(ta, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int j = 0; j < 32; ++j) accd[j] += (double)__uint_as_float(v[j]);
-            tmem_ld32(ta + 32, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&tempty[b]);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) accd[32 + j] += (double)__uint_as_float(v[j]);
-        }
-        const int row = m0 + qd * 32 + lane;
-        if (row < M) {
-            float* drow = D + (((int64_t)q * slices + s) * M + row) * ldd + n0 + half * 64;
-            const int col0 = n0 + half * 64;
-            if (col0 + 64 <= N && (ldd & 3) == 0) {
-#pragma unroll
-                for (int j = 0; j < 64; j += 4)
-                    *reinterpret_cast<float4*>(drow + j) =
-                        make_float4((float)accd[j], (float)accd[j + 1], (float)accd[j + 2], (float)accd[j + 3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 64; ++j)
-                    if (col0 + j < N) drow[j] = (float)accd[j];
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-}
-
-// Persistent form of the accurate kernel: one CTA per SM walks tiles blockIdx.x, +gridDim.x, …
-// with the TMA ring, the TMEM double buffer and every barrier phase carried across tiles by
-// global counters, so the prologue (barrier init, TMEM alloc), the pipeline fill and the epilogue
-// store of one tile overlap the next tile's loads and MMAs.  Same arithmetic per tile.
-template <bool A_SPLIT, bool B_MN, int F, int EPI>
-__global__ void __launch_bounds__(64 + 32 * EPI, 1)
-gemm_3xtf32_flush_persistent_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
-                                    const __grid_constant__ CUtensorMap mapB, float* __restrict__ D, int M, int N,
-                                    int Kd, int64_t ldd, int slices, int splits, int kb_per, int tiles_n,
-                                    int tiles_m, int ntiles) {
-    constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
-    constexpr int STAGE_BYTES = flush::STAGE_BYTES, TMEM_COLS = flush::TMEM_COLS;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;
-    uint64_t* split = bars + STAGES;
-    uint64_t* empty = bars + 2 * STAGES;
-    uint64_t* tfull = bars + 3 * STAGES;
-    uint64_t* tempty = bars + 3 * STAGES + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kb_total = (Kd + BK - 1) / BK;
-    struct Tile { int n0, m0, s, q, kb0, kblocks; };
-    auto decode = [&](int tile) {
-        Tile t;
-        const int nt = tile % tiles_n, rest = tile / tiles_n;
-        const int mt = rest % tiles_m, z = rest / tiles_m;
-        t.n0 = nt * BN;
-        t.m0 = mt * BM;
-        t.s = z / splits;
-        t.q = z - t.s * splits;
-        t.kb0 = t.q * kb_per;
-        t.kblocks = max(0, min(kb_total, t.kb0 + kb_per) - t.kb0);
-        return t;
-    };
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&split[i], 32 * EPI);
-            mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 32 * EPI);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-    auto stage_ptr = [&](int st) { return smem + st * STAGE_BYTES; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int kbg = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const Tile t = decode(tile);
-                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
-                    const int st = kbg % STAGES;
-                    if (kbg >= STAGES) mbar_wait(&empty[st], ((kbg / STAGES) - 1) & 1);
-                    uint8_t* base = stage_ptr(st);
-                    const int kk = (t.kb0 + kb) * BK;
-                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
-                    tma_load_3d(base, &mapAh, &full[st], kk, t.m0, t.s);
-                    if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, t.m0, t.s);
-                    if (B_MN) {
-#pragma unroll
-                        for (int j = 0; j < BN / 32; ++j)
-                            tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], t.n0 + 32 * j, kk, t.s);
-                    } else {
-                        tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, t.n0, t.s);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id = flush::idesc(B_MN);
-            int kbg = 0, gg = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const Tile t = decode(tile);
-                for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
-                    const int st = kbg % STAGES, b = gg & 1;
-                    const bool first = (kb % F) == 0, last = (kb % F) == F - 1 || kb == t.kblocks - 1;
-                    if (first && gg >= 2) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
-                    mbar_wait(&split[st], (kbg / STAGES) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t a_hi = smem_u32(stage_ptr(st));
-                    const uint32_t a_lo = a_hi + A_TILE;
-                    const uint32_t b_hi = a_hi + 2 * A_TILE;
-                    const uint32_t b_lo = b_hi + B_TILE;
-                    const uint32_t acc = tmem + (uint32_t)(b * BN);
-#pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-                        const uint64_t dah = make_desc(a_hi + k * 32, 0, 1024, kLayoutSW128);
-                        const uint64_t dal = make_desc(a_lo + k * 32, 0, 1024, kLayoutSW128);
-                        uint64_t dbh, dbl;
-                        if (B_MN) {
-                            dbh = make_desc(b_hi + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                            dbl = make_desc(b_lo + k * 1024, BK * 128, 512, kLayoutSW128Base32);
-                        } else {
-                            dbh = make_desc(b_hi + k * 32, 0, 1024, kLayoutSW128);
-                            dbl = make_desc(b_lo + k * 32, 0, 1024, kLayoutSW128);
-                        }
-                        mma_tf32(acc, dah, dbh, id, (first && k == 0) ? 0u : 1u);
-                        mma_tf32(acc, dah, dbl, id, 1u);
-                        mma_tf32(acc, dal, dbh, id, 1u);
-                    }
-                    mma_commit(&empty[st]);
-                    if (last) {
-                        mma_commit(&tfull[b]);
-                        ++gg;
-                    }
-                }
-            }
-        }
-    } else {
-        // EPI epilogue warps: warp w reads TMEM lane quarter w % 4 (its sub-partition) and the
-        // column block (w - 2) / 4 of COLS columns
-        constexpr int NT_EPI = 32 * EPI, COLS = BN / (EPI / 4);
-        const int te = threadIdx.x - 64;
-        const int qd = warp & 3, cb = (warp - 2) >> 2;
-        int total_kb = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) total_kb += decode(tile).kblocks;
-        auto split_stage = [&](int kbx) {
-            const int st = kbx % STAGES;
-            mbar_wait(&full[st], (kbx / STAGES) & 1);
-            uint8_t* base = stage_ptr(st);
-            if (A_SPLIT) split_tile(base, base + A_TILE, A_TILE, te, NT_EPI);
-            split_tile(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, te, NT_EPI);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&split[st]);
-        };
-        for (int kbx = 0; kbx < min(total_kb, STAGES - 1); ++kbx) split_stage(kbx);
-        int kbg = 0, gg = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const Tile t = decode(tile);
-            double accd[COLS];
-#pragma unroll
-            for (int j = 0; j < COLS; ++j) accd[j] = 0.0;
-            for (int kb = 0; kb < t.kblocks; ++kb, ++kbg) {
-                if (kbg + STAGES - 1 < total_kb) split_stage(kbg + STAGES - 1);
-                if ((kb % F) != F - 1 && kb != t.kblocks - 1) continue;  // drain once per group
-                const int b = gg & 1;
-                mbar_wait(&tfull[b], (gg >> 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * BN + cb * COLS);
-#pragma unroll
-                for (int c = 0; c < COLS; c += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(ta + c, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (c + 16 == COLS) {  // the buffer is free once the last columns are in registers
-                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                        mbar_arrive(&tempty[b]);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) accd[c + j] += (double)__uint_as_float(v[j]);
-                }
-                ++gg;
-            }
-            const int row = t.m0 + qd * 32 + lane;
-            if (row < M) {
-                float* drow = D + (((int64_t)t.q * slices + t.s) * M + row) * ldd + t.n0 + cb * COLS;
-                const int col0 = t.n0 + cb * COLS;
-                if (col0 + COLS <= N && (ldd & 3) == 0) {
-#pragma unroll
-                    for (int j = 0; j < COLS; j += 4)
-                        *reinterpret_cast<float4*>(drow + j) = make_float4((float)accd[j], (float)accd[j + 1],
-                                                                           (float)accd[j + 2], (float)accd[j + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < COLS; ++j)
-                        if (col0 + j < N) drow[j] = (float)accd[j];
-                }
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-}
-
-// Warp-specialised form of the persistent accurate kernel.  In the kernels above the same
-// epilogue warps split the operands of stage kb+2 and then drain the accumulator of k-block kb,
-// so the split feeding the MMA waits behind every drain (ncu: tensor pipe ~20% active, warps
-// mostly waiting on mbarriers).  Here the roles are separate warps:
+// Persistent and warp-specialised (when one set of epilogue warps both split the operands of
+// stage kb+2 and drained the accumulator of k-block kb, the split feeding the MMA waited behind
+// every drain — ncu: tensor pipe ~20% active).  The roles are separate warps:
 //   warp 0 TMA · warp 1 TMEM alloc + MMA · SW split warps (hi/lo of the stage, runs up to STAGES
 //   ahead, gated only by TMA) · DW drain warps (fold each k-block's fresh accumulator; warp w
 //   reads TMEM lane quarter w % 4 and column block of COLS = BN/(DW/4) columns).
 // NBUF TMEM accumulators let the MMA run NBUF-1 k-blocks ahead of the drain.  Same arithmetic
-// per tile as gemm_3xtf32_flush_persistent_kernel (bitwise, with KAHAN = false).
-// B_PRE: B arrives already split (hi through mapB, lo through mapBl; the producers wrote both,
-// wino_kernels.cuh tf32_split); with A pre-split too there is nothing to split (SW = 0).
-template <bool A_SPLIT, bool B_MN, int SW, int DW, bool KAHAN, int NBUF, bool B_PRE = false>
+// per tile as the shared-epilogue form (bitwise, with KAHAN = false).
+template <bool A_SPLIT, bool B_MN, int SW, int DW, bool KAHAN, int NBUF>
 __global__ void __launch_bounds__(64 + 32 * (SW + DW), 1)
 gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
                       const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapD,
-                      const __grid_constant__ CUtensorMap mapBl,
                       float* __restrict__ D, int M, int N, int Kd,
                       int64_t ldd, int slices, int splits, int kb_per, int tiles_n, int tiles_m, int ntiles) {
     constexpr int BN = flush::BN, STAGES = flush::STAGES, A_TILE = flush::A_TILE, B_TILE = flush::B_TILE;
     constexpr int STAGE_BYTES = flush::STAGE_BYTES;
     constexpr int TMEM_COLS = NBUF * BN;
     static_assert(TMEM_COLS <= 512 && (NBUF & (NBUF - 1)) == 0, "TMEM holds 512 columns");
-    static_assert(SW > 0 || (!A_SPLIT && B_PRE), "nothing to split needs no split warps");
+    static_assert(SW > 0, "split warps");
     static_assert(DW == 8 || DW == 16, "drain warps: 4 lane quarters x 2 or 4 column blocks");
     constexpr int COLS = BN / (DW / 4);
     // output staging box per drain warp: 32 rows x BOXC columns (4 KB with a 128-byte swizzle for
@@ -819,20 +312,16 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                     if (kbg >= STAGES) mbar_wait(&empty[st], ((kbg / STAGES) - 1) & 1);
                     uint8_t* base = stage_ptr(st);
                     const int kk = (t.kb0 + kb) * BK;
-                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + (B_PRE ? 2 : 1) * B_TILE);
+                    mbar_expect_tx(&full[st], (A_SPLIT ? A_TILE : 2 * A_TILE) + B_TILE);
                     tma_load_3d(base, &mapAh, &full[st], kk, t.m0, t.s);
                     if (!A_SPLIT) tma_load_3d(base + A_TILE, &mapAl, &full[st], kk, t.m0, t.s);
                     if (B_MN) {
 #pragma unroll
                         for (int j = 0; j < BN / 32; ++j) {
                             tma_load_3d(base + 2 * A_TILE + j * (BK * 128), &mapB, &full[st], t.n0 + 32 * j, kk, t.s);
-                            if (B_PRE)
-                                tma_load_3d(base + 2 * A_TILE + B_TILE + j * (BK * 128), &mapBl, &full[st],
-                                            t.n0 + 32 * j, kk, t.s);
                         }
                     } else {
                         tma_load_3d(base + 2 * A_TILE, &mapB, &full[st], kk, t.n0, t.s);
-                        if (B_PRE) tma_load_3d(base + 2 * A_TILE + B_TILE, &mapBl, &full[st], kk, t.n0, t.s);
                     }
                 }
             }
@@ -887,7 +376,7 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
                 mbar_wait(&full[st], (kbg / STAGES) & 1);
                 uint8_t* base = stage_ptr(st);
                 if (A_SPLIT) split_tile_fast(base, base + A_TILE, A_TILE, ts, 32 * SW);
-                if (!B_PRE) split_tile_fast(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, ts, 32 * SW);
+                split_tile_fast(base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, B_TILE, ts, 32 * SW);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&split[st]);
             }
@@ -968,38 +457,6 @@ gemm_3xtf32_ws_kernel(const __grid_constant__ CUtensorMap mapAh, const __grid_co
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-}
-
-// dW_F from the split-K partials [splits][P2][K][C]: fp64 sum in split order, written in the
-// W_F layout K×C×p×q (layer.hpp:36).
-__global__ void reduce_dw_kernel(const float* __restrict__ part, float* __restrict__ dw, int K, int C, int P2,
-                                 int splits) {
-    const int64_t total = (int64_t)P2 * K * C;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double a = 0.0;
-        for (int q = 0; q < splits; ++q) a += (double)part[(int64_t)q * total + i];
-        const int64_t s = i / ((int64_t)K * C), kc = i - s * K * C;
-        dw[kc * P2 + s] = (float)a;
-    }
-}
-
-// Sparse plan, dW on the tensor cores: sum the split-K partials [splits][P2][K][C] in fp64 at the
-// surviving coordinates only, written in CSR order (e -> (slice, row, col)).
-__global__ void reduce_dw_masked_kernel(const float* __restrict__ part, float* __restrict__ dwc,
-                                        const int* __restrict__ rowof, const int* __restrict__ colidx,
-                                        const int64_t* __restrict__ slice_off, int K, int C, int P2,
-                                        int splits, int64_t nnz) {
-    const int64_t plane = (int64_t)P2 * K * C;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        int s = 0;  // slice of e: P2 ≤ 64 offsets, linear scan
-        while (s + 1 < P2 && slice_off[s + 1] <= e) ++s;
-        const int64_t idx = ((int64_t)s * K + rowof[e]) * C + colidx[e];
-        double a = 0.0;
-        for (int q = 0; q < splits; ++q) a += (double)part[(int64_t)q * plane + idx];
-        dwc[e] = (float)a;
-    }
 }
 
 }  // namespace tc
