@@ -419,10 +419,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
     else:
         compute = lb.compute
 
+    exchange = "none (1 GPU)"
+    if world > 1 and not fwd_only:
+        # the step's one exchange runs inside the backward call (wino_set_dw_allreduce): NCCL on
+        # the dW_F stream right after the dW_F kernels, overlapping the dI chain and the forward
+        from paper_1702_08597_b200.dist import nccl_comm_ptr
+
+        layer.set_dw_allreduce(nccl_comm_ptr(device=local_rank))
+        exchange = "NCCL all-reduce of nnz-compact dW_F inside the backward call (dW_F stream, overlaps dI)"
+
     def step():
         compute()
-        if world > 1 and not fwd_only:
-            dist.all_reduce(dw)
 
     for _ in range(args.warmup):
         step()
@@ -431,16 +438,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     step()
     torch.cuda.synchronize()
     per_step_launches = layer.launch_count()
-    # the layer's kernels as one CUDA graph; the step's one collective (N > 1) is issued eagerly
-    # after the replay, on the same stream, so no NCCL call is ever graph-captured
-    run_c, graph_note = capture(compute, args)
-    if world > 1 and not fwd_only:
-        def run():
-            run_c()
-            dist.all_reduce(dw)
-        graph_note += " + eager NCCL all-reduce of dW_F"
-    else:
-        run = run_c
+    # the step as one CUDA graph (N > 1: the in-backward NCCL exchange is captured with it; if the
+    # capture fails the step runs eagerly and the line says so)
+    run, graph_note = capture(compute, args)
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local_rank)
@@ -460,7 +460,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     allreduce = None
-    if world > 1 and not fwd_only:  # the one exchange of the step, timed alone
+    if world > 1 and not fwd_only:  # the exchange's own cost, timed alone
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
         dist.barrier()
         for a, b in evs:
@@ -471,7 +471,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         ar = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / len(evs)], device=dev, dtype=torch.float64)
         dist.all_reduce(ar, op=dist.ReduceOp.MAX)
         allreduce = {"ms": float(ar.item()), "bytes": dw.numel() * 4, "share_of_step": float(ar.item()) / ms_max,
-                     "backend": dist.get_backend()}
+                     "backend": dist.get_backend(), "placement": exchange}
     passes = 1 if fwd_only else 3
     flops_step = passes * flops_per_image(cfg) * n
     value = world * flops_step / (ms_max * 1e-3) / 1e9
@@ -544,9 +544,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 normals)",
         "config": {"workload": workload_name(cfg, "fwd" if fwd_only else "fwd+bwd"), "global_batch": n * world,
                    "n_per_gpu": n, "sparsity": cfg.sparsity, "nnz": layer.nnz, "path": lb.path(),
-                   "dw": "exact: f64 digit kernels + int8 tcgen05 digit-pair GEMM (strict vs the f64 reference)",
+                   "dw": "exact: f64 digits fused into K1/K4 + int8 tcgen05 digit-pair GEMM (strict vs the f64 reference)",
                    "l2_flush": "256 MB write between timed steps (inputs also exceed L2 at c2/c3)",
-                   "parallelism": f"dp{world} (batch shards, NCCL all-reduce of nnz-compact dW_F)"},
+                   "parallelism": f"dp{world} (batch shards; {exchange})"},
         "ms_per_layer": ms_max,
         "roofline": roofline,
         "kernels": kernels,
@@ -617,10 +617,15 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
     g_o = torch.from_numpy(go).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
 
+    if world > 1:  # each layer's dW_F exchange inside its backward, overlapping its dI chain
+        from paper_1702_08597_b200.dist import nccl_comm_ptr
+
+        st.set_dw_allreduce(nccl_comm_ptr(device=local_rank))
+
     def step():
         st.step(x, g_o, lr=1e-4, n_global=n_global)
 
-    # the same step in three parts (WinogradStack.step with mode=None): forward + backward and the
+    # the same step in parts (WinogradStack.step with mode=None): forward + backward and the
     # masked SGD update each as a CUDA graph, the bucket's one all-reduce issued eagerly between
     # them (no NCCL call is graph-captured)
     def fwd_bwd():
@@ -644,10 +649,11 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
 
     def run():
         run_fb()
-        st.bucket.allreduce()
+        if not st.in_backward_exchange:
+            st.bucket.allreduce()
         run_up()
     if world > 1:
-        graph_note += " (forward+backward and update graphs, eager NCCL all-reduce between)"
+        graph_note += " (forward+backward graph with each layer's NCCL dW_F exchange inside its backward, update graph)"
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local_rank)
@@ -683,7 +689,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     allreduce = None
-    if world > 1:  # the step's one exchange (the bucket of all layers' dW_F), timed alone
+    if world > 1:  # the exchange's own cost (the bucket of all layers' dW_F as one collective), timed alone
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
         dist.barrier()
         for a, b in evs:
@@ -732,7 +738,7 @@ def run_gpu_stack(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded splitmix64 normals)",
         "config": {"workload": f"c4: 4-layer Winograd stack C=K=256 H=W=28 F(4x4,3x3) pad 1, ReLU, "
                                f"90% fixed masks, global batch {n_global} sharded over {world} GPU(s), "
-                               "masked SGD, one NCCL all-reduce of nnz-compact dW_F per step",
+                               "masked SGD, NCCL all-reduce of each layer's nnz-compact dW_F inside its backward",
                    "global_batch": n_global, "n_per_gpu": n, "parallelism": f"dp{world}",
                    "l2_flush": "256 MB write between timed steps"},
         "kernels": kernels,

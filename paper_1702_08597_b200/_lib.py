@@ -116,6 +116,7 @@ SIGNATURES = {
     "wino_backward_range": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "wino_backward_weights_cached": (C.c_int, [_vp, _vp, _vp, _vp]),
     "wino_allreduce_dw": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "wino_set_dw_allreduce": (C.c_int, [_vp, _vp]),
     "wino_update_weights": (C.c_int, [_vp, _vp, C.POINTER(Update), _vp]),
     "wino_sgd_step": (C.c_int, [_vp, _vp, C.c_float, C.c_float, C.c_float, _vp]),
     "wino_update_status": (C.c_int, [_vp, _pi64]),

@@ -212,6 +212,7 @@ struct wino_plan {
     // TMEM SpMM (wino_spmm_tm.cuh): the padded stage-segment streams of the CSR [0] and CSC [1],
     // rebuilt whenever the structure changes, values refreshed by wino_values_updated
     int spmm_operands = 0;  // WINO_OPT_SPMM_OPERANDS: 0 auto, 1 shared memory, 2 tensor memory
+    void* dw_comm = nullptr;  // wino_set_dw_allreduce: ncclComm_t of the in-backward dW_F exchange
     struct TmStream {        // the TMEM SpMM's padded stage-segment stream of one direction
         int2* cv = nullptr;  // (TMEM column, value)
         int* pidx = nullptr; // source entry (-1: pad)
@@ -800,6 +801,8 @@ int launch_grad_fused(wino_plan* p, cudaStream_t st, const float* dO, const floa
     return WINO_OK;
 }
 
+int dw_exchange(wino_plan* p, float* grad_w, cudaStream_t st);
+
 // dW_F from the digits of every segment: the int8 GEMM per accumulation chunk, then the ordered
 // chunk sum gathered on the mask (CSR order) or into K×C×p×q (dense plan).
 int launch_xdw(wino_plan* p, cudaStream_t st, const wino_cache* c, float* grad_w) {
@@ -850,7 +853,8 @@ int launch_xdw(wino_plan* p, cudaStream_t st, const wino_cache* c, float* grad_w
         x::reduce_sparse_kernel<<<dim3(per_slice, (unsigned)P2), 256, 0, st>>>(
             p->d_xpart, grad_w, p->d_rowof, p->d_colidx, p->d_slice_off, K, C, P2, ct.n, p->nnz);
     }
-    return L.done();
+    const int rc = L.done();
+    return rc ? rc : dw_exchange(p, grad_w, st);
 }
 int check_plan(const wino_plan* p) {
     if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
@@ -1706,6 +1710,32 @@ void resolve_nccl() {
     g_nccl_errstr = reinterpret_cast<nccl_errstr_t>(dlsym(h, "ncclGetErrorString"));
 }
 }  // namespace
+
+}  // extern "C"
+
+namespace {
+// the in-backward exchange (wino_set_dw_allreduce): sum grad_w over the plan's communicator
+int dw_exchange(wino_plan* p, float* grad_w, cudaStream_t st) {
+    if (!p->dw_comm || !grad_w) return WINO_OK;
+    const int64_t count = p->dense ? (int64_t)p->P2 * p->K * p->C : p->nnz;
+    if (count == 0) return WINO_OK;
+    std::call_once(g_nccl_once, resolve_nccl);
+    if (!g_nccl_allreduce) return set_err(WINO_CAPABILITY_ERROR, "dW_F exchange: libnccl.so.2 not found");
+    ++p->launches;
+    const int r = g_nccl_allreduce(grad_w, grad_w, (size_t)count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, p->dw_comm, st);
+    if (r != 0)
+        return set_err(WINO_CUDA_ERROR, std::string("ncclAllReduce: ") + (g_nccl_errstr ? g_nccl_errstr(r) : "error"));
+    return WINO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int wino_set_dw_allreduce(wino_plan* p, void* nccl_comm) {
+    if (!p) return set_err(WINO_INVALID_ARGUMENT, "null plan");
+    p->dw_comm = nccl_comm;
+    return WINO_OK;
+}
 
 int wino_allreduce_dw(wino_plan* p, void* nccl_comm, float* grad_w, int64_t count, void* stream) {
     int rc = check_plan(p);

@@ -11,6 +11,18 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 
+def nccl_comm_ptr(group=None, device=None) -> int:
+    """The ncclComm_t (as an int) behind a torch.distributed NCCL process group (default group
+    if None) — what wino_set_dw_allreduce / WinogradLayer.set_dw_allreduce take to run the dW_F
+    exchange inside the backward on the same communicator torch uses."""
+    import torch
+    import torch.distributed as dist
+
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return int(pg._get_backend(dev)._comm_ptr())
+
+
 def shard(n_global: int, rank: int, world: int) -> tuple[int, int]:
     """(start, count) of rank's contiguous slice of a batch of n_global images; the first
     n_global % world ranks take one extra image, so every image belongs to exactly one rank."""

@@ -276,6 +276,16 @@ class WinogradLayer:
                                           _stream_ptr(stream)))
         return out
 
+    def set_dw_allreduce(self, comm=None):
+        """Run the data-parallel dW_F exchange inside every backward (wino_set_dw_allreduce): right
+        after the dW_F kernels, on their stream, overlapping the dI chain.  `comm`: an ncclComm_t
+        address, a torch.distributed NCCL process group (its communicator), or None (off)."""
+        if comm is not None and not isinstance(comm, int):
+            from .dist import nccl_comm_ptr
+
+            comm = nccl_comm_ptr(comm, self.device)
+        check(lib().wino_set_dw_allreduce(self._h, C.c_void_p(comm or 0)))
+
     def allreduce_dw(self, grad_w, nccl_comm: int, count: int = -1, stream=None):
         """Sum grad_w in place over an NCCL communicator (an ncclComm_t address)."""
         check(lib().wino_allreduce_dw(self._h, C.c_void_p(nccl_comm), _dptr(grad_w), count, _stream_ptr(stream)))

@@ -5,7 +5,8 @@ The reference trainer runs one sample at a time (train.cpp:167) through run_forw
 backward_weights, Σ_n·(1/B), backward_input for l > 0; train.cpp:189-211), then the masked
 SGD update of train_step (train.cpp:281-290).  Here one call per layer and minibatch does the
 same on the device: ReLU is fused into the output-transform epilogue, the mask into the dZ
-kernel, dW_F of all layers lands in one GradBucket that is all-reduced once (data parallel),
+kernel, dW_F of all layers lands in one GradBucket that is all-reduced once (data parallel; or,
+with set_dw_allreduce, each layer's slice is summed inside its own backward, overlapping its dI chain),
 and the update runs on the live CSR values (masked coordinates do not exist in the CSR, so
 they stay exactly zero — the fine-tune invariant check_masks enforces, train.cpp:340-347).
 """
@@ -41,10 +42,20 @@ class WinogradStack:
         self.outs = [None] * len(self.layers)
         self.dis = [None] * len(self.layers)
         self._torch = torch
+        self.in_backward_exchange = False
 
     def _alloc_bucket(self):
         self.bucket = GradBucket.allocate([lay.nnz for lay in self.layers], device=f"cuda:{self.device}")
         self.grads = [v.view(lay.grad_w_shape()) for v, lay in zip(self.bucket.views, self.layers)]
+
+    def set_dw_allreduce(self, comm=None):
+        """Move the data-parallel exchange into the backward: every layer sums its own dW_F over
+        `comm` (an NCCL process group or ncclComm_t address; None: back to the one bucketed
+        all-reduce after the backward) right after its dW_F kernels, overlapping that layer's dI
+        chain (WinogradLayer.set_dw_allreduce).  step() then skips the bucket all-reduce."""
+        for lay in self.layers:
+            lay.set_dw_allreduce(comm)
+        self.in_backward_exchange = comm is not None
 
     def forward(self, x):
         """run_forward (train.cpp:66-87): conv -> ReLU for every layer; returns the last output."""
@@ -83,7 +94,8 @@ class WinogradStack:
         'train': λ‖w‖_norm without threshold."""
         self.forward(x)
         self.backward(grad_out)
-        self.bucket.allreduce(group)
+        if not self.in_backward_exchange:
+            self.bucket.allreduce(group)
         scale = 1.0 / float(n_global)
         for lay, g in zip(self.layers, self.grads):
             if mode is None:

@@ -284,3 +284,64 @@ def test_backward_without_input_gradient():
     dw_ref = layer.backward_weights(dev(go), cache)
     dw, di = layer.backward(dev(go), cache, want_input_grad=False)
     assert di is None and torch.equal(dw, dw_ref)
+
+
+def test_in_backward_exchange_over_a_torch_nccl_group():
+    """wino_set_dw_allreduce with the communicator of a real torch.distributed NCCL group (one
+    rank): the exchange runs inside forward_backward / backward on the dW_F stream — eagerly and
+    captured in a CUDA graph, as bench.py runs it at N > 1 — and the sum over one rank leaves
+    dW_F bit for bit; the stack's per-layer exchange replaces its bucket all-reduce."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1702_08597_b200.graph import GraphedStep
+    from paper_1702_08597_b200.stack import WinogradStack
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = CONFIGS["c0"]
+        img, w_f, go = make_inputs(cfg, n=3)
+        x, g = dev(img), dev(go)
+        ref = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+        ref.set_weights(w_f)
+        rc = ref.new_cache(3)
+        o0 = torch.empty((3, cfg.k, ref.ho, ref.wo), device="cuda")
+        dw0 = torch.empty(ref.grad_w_shape(), device="cuda")
+        di0 = torch.empty((3, cfg.c, cfg.h, cfg.w), device="cuda")
+        ref.forward_backward(x, g, rc, out=o0, out_w=dw0, out_i=di0)
+
+        lay = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
+        lay.set_weights(w_f)
+        lay.set_dw_allreduce(dist.group.WORLD)
+        cache = lay.new_cache(3)
+        o, dw, di = torch.empty_like(o0), torch.empty_like(dw0), torch.empty_like(di0)
+
+        def step():
+            lay.forward_backward(x, g, cache, out=o, out_w=dw, out_i=di)
+
+        step()
+        torch.cuda.synchronize()
+        assert torch.equal(dw, dw0) and torch.equal(di, di0) and torch.equal(o, o0)
+        dw.zero_()
+        GraphedStep(step).replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dw, dw0), "graph-captured in-backward exchange changed dW_F"
+        dw2, _ = lay.backward(g, cache)
+        torch.cuda.synchronize()
+        assert torch.equal(dw2, dw0)
+
+        st = WinogradStack([w_f, w_f], cfg.c, cfg.h, cfg.w, pad=1, m=4, n_max=3)
+        st.set_dw_allreduce(dist.group.WORLD)
+        assert st.in_backward_exchange
+        st.forward(x)
+        st.backward(g)
+        torch.cuda.synchronize()
+        assert torch.isfinite(st.bucket.flat).all()
+    finally:
+        dist.destroy_process_group()
