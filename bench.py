@@ -240,10 +240,20 @@ def kernel_work(cfg, layer, n):
     }
 
 
-def kernel_table(prof, steps, cfg, layer, n, pk):
+# On-chip operand bounds of the CSR kernels (tools/microbench/tmem_bw.cu, spmm_hybrid_bw.cu, one
+# B200): a multiply-add needs 4 bytes of the dense operand per lane; tcgen05.ld.32x32b.x4 delivers
+# 156 B/clk/SM (the TMEM SpMM), LDS.128 101 B/clk/SM (the shared-memory SpMM).
+TMEM_MAC_PER_CLK = 156.3 / 4
+LDS_MAC_PER_CLK = 101.3 / 4
+
+
+def kernel_table(prof, steps, cfg, layer, n, pk, sm_mhz=None):
     """Per-kind time per step (profiled steps, CUDA events on the launching stream) with its
-    roofline: tensor-pipe kinds against the measured TF32 / int8 rate, the rest against HBM."""
+    roofline: tensor-pipe kinds against the measured TF32 / int8 rate, the rest against HBM; the
+    CSR kinds also against their on-chip operand bound (multiply-adds per clock per SM)."""
     work = kernel_work(cfg, layer, n)
+    nt = n * layer.geometry["t"]
+    clk = (sm_mhz or 1965.0) * 1e6
     tot = sum(v[0] for v in prof.values()) or 1.0
     out = {}
     for name, (ms_tot, cnt) in prof.items():
@@ -264,6 +274,12 @@ def kernel_table(prof, steps, cfg, layer, n, pk):
             else:
                 k["roofline"] = {"bound": "hbm", "achieved": k["GBps"], "peak": pk["hbm_gbs"],
                                  "frac": k["GBps"] / pk["hbm_gbs"], "unit": "GB/s", "peak_source": pk["source"]}
+        if name.startswith("spmm"):
+            mac = layer.nnz * nt / (ms * 1e-3) / (148 * clk)
+            k["on_chip"] = {"mac_per_clk_sm": mac, "tmem_bound": TMEM_MAC_PER_CLK, "lds_bound": LDS_MAC_PER_CLK,
+                            "frac_of_tmem_bound": mac / TMEM_MAC_PER_CLK,
+                            "note": "nnz·n·T multiply-adds per pass / time / (148 SMs · SM clock); the "
+                                    "operand bytes per multiply-add come from TMEM (or shared memory), not HBM"}
         out[name] = k
     return out
 
@@ -377,7 +393,9 @@ def sweep_point(cfg, dev, local_rank, flush, pk, args, contraction="csr"):
           "eff_tflops": passes * flops_per_image(cfg) * cfg.n / (ms * 1e-3) / 1e12,
           "dominant": dominant_roofline(kernels, f"{cfg.name}:{cfg.sparsity}"),
           "kernels": {k: {"ms": v["ms_per_step"], "frac": (v.get("roofline") or {}).get("frac"),
-                          "bound": (v.get("roofline") or {}).get("bound")} for k, v in kernels.items()}}
+                          "bound": (v.get("roofline") or {}).get("bound"),
+                          **({"mac_per_clk_sm": v["on_chip"]["mac_per_clk_sm"]} if "on_chip" in v else {})}
+                      for k, v in kernels.items()}}
     lb.close()
     del lb, run
     torch.cuda.empty_cache()
@@ -535,7 +553,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if rank != 0:
         return
     pk = peaks()
-    kernels = kernel_table(prof, 3, cfg, layer, n, pk)
+    kernels = kernel_table(prof, 3, cfg, layer, n, pk, clocks.get("sm_mhz"))
     roofline = dominant_roofline(kernels, f"{cfg.name}:{cfg.sparsity}")
     line = {
         "metric": METRIC_FWD if fwd_only else METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,

@@ -21,9 +21,11 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 PROF = ROOT / "profiles"
 
-KIND = [("input_transform", "input_transform"), ("output_transform", "output_transform"),
-        ("grad_z", "grad_z"), ("input_grad", "input_grad"), ("sddmm", "sddmm_dw"),
-        ("split_sum", "sddmm_dw"), ("gemm_3xtf32", "dense_tc"), ("spmm", "spmm")]
+KIND = [("input_transform_digits", "input_transform"), ("input_transform", "input_transform"),
+        ("grad_z_digits", "grad_z"), ("output_transform", "output_transform"), ("input_grad", "input_grad"),
+        ("plane_amax", "amax"), ("xdw::gemm_kernel", "dw_gemm_i8"), ("reduce_sparse", "dw_reduce"),
+        ("reduce_dense", "dw_reduce"), ("spmm_tmem", "spmm"), ("spmm_kernel", "spmm"),
+        ("gemm_3xtf32", "dense_tc"), ("tm_", "stream_build"), ("stage_bounds", "stream_build")]
 
 METRICS = OrderedDict([
     ("gpu__time_duration.sum", "duration"),
@@ -56,7 +58,7 @@ def to_bytes(v: str, unit: str) -> float:
     return x * scale.get(unit, 1)
 
 
-def launches(path: Path, rnd: str):
+def launches(path: Path, rnd: str, what: str):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
@@ -66,16 +68,16 @@ def launches(path: Path, rnd: str):
         k = kind_of(r[ki])
         agg[k][0] += float(r[vi].replace(",", ""))
         agg[k][1] += 1
-    shutil.copy(path, PROF / f"{rnd}_launches_c1.csv")
+    shutil.copy(path, PROF / f"{rnd}_{path.name}")
     ours = {k: v for k, v in agg.items() if "at::" not in k and "vectorized" not in k}
     tot = sum(v[0] for v in ours.values())
-    lines = [f"# {rnd}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (c1)",
+    lines = [f"# {rnd}: ncu launch list of `{what}`",
              "", "Cold-cache, serialised per-launch times (`gpu__time_duration.sum`, `--clock-control none`);",
              "compare shares, not absolutes. Torch's L2-flush fills are excluded from the shares.", "",
              "| kernel | launches | mean µs | share |", "|---|---|---|---|"]
     for k, (t, n) in sorted(ours.items(), key=lambda kv: -kv[1][0]):
         lines.append(f"| {k} | {n} | {t / n / 1e3:.1f} | {t / tot:.1%} |")
-    (PROF / f"{rnd}_launch_shares.md").write_text("\n".join(lines) + "\n")
+    (PROF / f"{rnd}_launch_shares_{path.stem}.md").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
@@ -130,11 +132,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r1")
     ap.add_argument("--launches")
+    ap.add_argument("--launches-cmd", default="python bench.py --config c3 --steps 2 --warmup 3 --no-cpu-baseline --no-sweep")
     ap.add_argument("--full", action="append", default=[], help="tag=path[:cfgkey]")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     if a.launches:
-        launches(Path(a.launches), a.round)
+        launches(Path(a.launches), a.round, a.launches_cmd)
     tfile = PROF / "ncu_traffic.json"
     traffic = json.loads(tfile.read_text()) if tfile.exists() else {}
     md = [f"# {a.round}: per-kernel counters from single `ncu --set full --clock-control none` captures", "",
