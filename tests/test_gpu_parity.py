@@ -679,8 +679,8 @@ def test_ragged_tile_shapes(mode):
 @pytest.mark.slow
 @pytest.mark.parametrize("sparsity", [0.8, 0.9, 0.95])
 def test_c2_forward_bitwise(sparsity):
-    """configs[2] at its full size (N=64, C=K=512, H=W=28) at 80/90/95%: the SpMM takes its
-    2-wide-t variant (a 512-row X chunk does not fit shared memory at 4-wide); the forward of 8
+    """configs[2] at its full size (N=64, C=K=512, H=W=28) at 80/90/95%: the SpMM runs with its
+    operand chunk in TMEM in 4 stages (80/90%) or in shared memory, 2-wide t (95%); the forward of 8
     sampled images is bitwise the f32 mirror of the reference's sparse_forward<float>
     (sparse.cpp:189-253) and within the strict bound of the f64 layer."""
     cfg = with_sparsity(CONFIGS["c2"], sparsity)
