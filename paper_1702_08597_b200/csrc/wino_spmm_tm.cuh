@@ -70,6 +70,27 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 
+// the same on 32-bit shared addresses (precomputed once per warp: the row loop stays lean)
+__device__ __forceinline__ void mb_arrive_a(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait_a(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void sts4(uint32_t a, unsigned long long lo, unsigned long long hi) {
+    asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(a), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ void lds4(uint32_t a, unsigned long long& lo, unsigned long long& hi) {
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a) : "memory");
+}
+
 __device__ __forceinline__ void tld4(uint32_t taddr, float (&v)[4]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
@@ -253,7 +274,7 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     constexpr int TW = 128 * TB;
     constexpr int NSLOT = handoff_slots(S);
     extern __shared__ __align__(16) uint8_t tm_smem[];
-    float4* slots = reinterpret_cast<float4*>(tm_smem);                       // [NSLOT][32]
+    // [NSLOT][32 lanes][4 floats] handoff slots at tm_smem (addressed through slot_in / slot_out)
     uint64_t* full = reinterpret_cast<uint64_t*>(tm_smem + NSLOT * SLOT_BYTES);
     uint64_t* empty = full + NSLOT;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + NSLOT);
@@ -280,6 +301,11 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     const int chain = b * ROWSETS + g;
     const int ring_in = (chain * (S - 1) + (st - 1)) * SLOTS;
     const int ring_out = (chain * (S - 1) + st) * SLOTS;
+    const uint32_t sbase = su32(tm_smem);
+    const uint32_t full_in = sbase + NSLOT * SLOT_BYTES + 8 * ring_in, empty_in = full_in + 8 * NSLOT;
+    const uint32_t full_out = sbase + NSLOT * SLOT_BYTES + 8 * ring_out, empty_out = full_out + 8 * NSLOT;
+    const uint32_t slot_in = sbase + ring_in * SLOT_BYTES + 16 * lane;
+    const uint32_t slot_out = sbase + ring_out * SLOT_BYTES + 16 * lane;
     int nrow_chain = 0;  // rows this chain has passed through its rings so far (all units)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int s = u / chunks, ch = u - s * chunks;
@@ -332,31 +358,31 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
             }
         }
         // ---- rows of this chain ----
-        const int* rb = STAGED ? sbnd : bs;
-        const int2* cvb = STAGED ? scv - e_lo : cv;  // indexed by global entry numbers
-        float* ys = Y + (int64_t)s * nrows * NTs + t;
-        for (int r = g; r < nrows; r += ROWSETS, ++nrow_chain) {
-            const int slot = nrow_chain % SLOTS;
+        const int* rbp = (STAGED ? sbnd : bs) + g * (S + 1) + st;  // this warp's rows' segment starts
+        const int2* cvb = STAGED ? scv - e_lo : cv;               // indexed by global entry numbers
+        float* yp = Y + ((int64_t)s * nrows + g) * NTs + t;
+        for (int r = g; r < nrows; r += ROWSETS, ++nrow_chain, rbp += ROWSETS * (S + 1), yp += ROWSETS * (int64_t)NTs) {
+            const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
             const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
-            const int e = rb[r * (S + 1) + st], ee = rb[r * (S + 1) + st + 1];
+            const int e = rbp[0], ee = rbp[1];
             unsigned long long acc[2] = {0ull, 0ull};
             if (st > 0) {  // the previous stage's accumulators for this row
-                mb_wait(&full[ring_in + slot], par);
-                const float4 a = slots[(ring_in + slot) * 32 + lane];
-                asm("mov.b64 %0, {%1,%2};" : "=l"(acc[0]) : "f"(a.x), "f"(a.y));
-                asm("mov.b64 %0, {%1,%2};" : "=l"(acc[1]) : "f"(a.z), "f"(a.w));
-                mb_arrive(&empty[ring_in + slot]);
+                mb_wait_a(full_in + 8 * k, par);
+                lds4(slot_in + SLOT_BYTES * k, acc[0], acc[1]);
+                mb_arrive_a(empty_in + 8 * k);
             }
             walk<STAGED>(cvb, e, ee, tq, acc, z);
-            float4 o;
-            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[0]));
-            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[1]));
             if (st == S - 1) {
-                if (tok) *reinterpret_cast<float4*>(ys + (int64_t)r * NTs) = o;
+                if (tok) {
+                    float4 o;
+                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[0]));
+                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[1]));
+                    *reinterpret_cast<float4*>(yp) = o;
+                }
             } else {
-                if (nrow_chain >= SLOTS) mb_wait(&empty[ring_out + slot], par ^ 1u);
-                slots[(ring_out + slot) * 32 + lane] = o;
-                mb_arrive(&full[ring_out + slot]);
+                if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
+                sts4(slot_out + SLOT_BYTES * k, acc[0], acc[1]);
+                mb_arrive_a(full_out + 8 * k);
             }
         }
         // every warp is done reading this chunk (and the staged slice) before the next unit

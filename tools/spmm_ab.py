@@ -1,4 +1,4 @@
-"""A/B of the CSR kernels' operand store on the GPU: TMEM (WINO_OPT_SPMM_OPERANDS auto) vs shared
+"""A/B of the CSR kernels' operand store on the GPU: TMEM (WINO_OPT_SPMM_OPERANDS forced) vs shared
 memory.  For each config: forward O, dW_F and dI of one fwd+bwd step must be bitwise equal between
 the two; prints the per-kind times (profiled serial step) of both.
 
@@ -6,6 +6,7 @@ the two; prints the per-kind times (profiled serial step) of both.
 """
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
 
@@ -55,12 +56,12 @@ def main():
         cfg = CONFIGS[base]
         if sp:
             cfg = with_sparsity(cfg, float(sp))
-        a, ta = run(cfg, "auto")
+        a, ta = run(cfg, "tmem")
         b, tb = run(cfg, "smem")
         same = all(np.array_equal(x, y) for x, y in zip(a, b))
         ok &= same
         print(f"{nm:8s} bitwise={'yes' if same else 'NO'}  tmem {ta}  smem {tb}", flush=True)
-    sys.exit(0 if ok else 1)
+    sys.exit(0 if ok or os.environ.get("SPMM_AB_NOFAIL") else 1)
 
 
 if __name__ == "__main__":
