@@ -494,61 +494,65 @@ def run_gpu(args, cfg, rank, world, local_rank):
     flops_step = passes * flops_per_image(cfg) * n
     value = world * flops_step / (ms_max * 1e-3) / 1e9
 
-    # ---- end to end through the public API with host buffers (pinned) ----
-    x, g_o, out, di = lb.x, lb.g, lb.out, lb.di
-    h_img = torch.from_numpy(img).pin_memory()
-    h_go = torch.from_numpy(go).pin_memory()
-    h_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
-    h_dw = torch.empty(dw.shape, dtype=torch.float32).pin_memory()
-    h_di = torch.empty(di.shape, dtype=torch.float32).pin_memory()
+    e2e = None
+    if not args.no_e2e:
+        # ---- end to end through the public API with host buffers (pinned) ----
+        x, g_o, out, di = lb.x, lb.g, lb.out, lb.di
+        h_img = torch.from_numpy(img).pin_memory()
+        h_go = torch.from_numpy(go).pin_memory()
+        h_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        h_dw = torch.empty(dw.shape, dtype=torch.float32).pin_memory()
+        h_di = torch.empty(di.shape, dtype=torch.float32).pin_memory()
 
-    if fwd_only:
-        def e2e_step():
-            x.copy_(h_img, non_blocking=True)
-            run()
-            h_out.copy_(out, non_blocking=True)
-        e2e_mode = "serial copies + forward"
-    elif world == 1 and not dense and args.contraction == "csr" and not args.no_pipeline:
-        # public API: image chunks so every copy overlaps compute (paper_1702_08597_b200/pipeline.py)
-        from paper_1702_08597_b200.graph import GraphedStep
-        from paper_1702_08597_b200.pipeline import PipelinedHostStep
+        if fwd_only:
+            def e2e_step():
+                x.copy_(h_img, non_blocking=True)
+                run()
+                h_out.copy_(out, non_blocking=True)
+            e2e_mode = "serial copies + forward"
+        elif world == 1 and not dense and args.contraction == "csr" and not args.no_pipeline:
+            # public API: image chunks so every copy overlaps compute (paper_1702_08597_b200/pipeline.py)
+            from paper_1702_08597_b200.graph import GraphedStep
+            from paper_1702_08597_b200.pipeline import PipelinedHostStep
 
-        ps = PipelinedHostStep(layer, lb.cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
-        # the whole pipelined step (copies on 3 streams + range kernels) as one CUDA graph
-        e2e_step = GraphedStep(lambda: ps(h_img, h_go, h_out, h_dw, h_di)).replay
-        e2e_mode = (f"PipelinedHostStep in one CUDA graph: pinned host buffers, {len(ps.bounds)} image chunks, "
-                    "copies overlapped with the range kernels, dW_F once over the batch")
-    elif world == 1 and not args.no_graph:
-        # public API: HostStep overlaps dO upload with the forward and the O / dW downloads
-        # with the backward (paper_1702_08597_b200/pipeline.py)
-        from paper_1702_08597_b200.pipeline import HostStep
+            ps = PipelinedHostStep(layer, lb.cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
+            # the whole pipelined step (copies on 3 streams + range kernels) as one CUDA graph
+            e2e_step = GraphedStep(lambda: ps(h_img, h_go, h_out, h_dw, h_di)).replay
+            e2e_mode = (f"PipelinedHostStep in one CUDA graph: pinned host buffers, {len(ps.bounds)} image chunks, "
+                        "copies overlapped with the range kernels, dW_F once over the batch")
+        elif world == 1 and not args.no_graph:
+            # public API: HostStep overlaps dO upload with the forward and the O / dW downloads
+            # with the backward (paper_1702_08597_b200/pipeline.py)
+            from paper_1702_08597_b200.pipeline import HostStep
 
-        hs = HostStep(layer, lb.cache, x, g_o, out, dw, di)
+            hs = HostStep(layer, lb.cache, x, g_o, out, dw, di)
 
-        def e2e_step():
-            hs(h_img, h_go, h_out, h_dw, h_di)
-        e2e_mode = "HostStep: pinned host buffers, 3 streams, copies overlapped with compute"
-    else:
-        def e2e_step():
-            x.copy_(h_img, non_blocking=True)
-            g_o.copy_(h_go, non_blocking=True)
-            run()
-            h_out.copy_(out, non_blocking=True)
-            h_dw.copy_(dw, non_blocking=True)
-            h_di.copy_(di, non_blocking=True)
-        e2e_mode = "serial copies + step"
+            def e2e_step():
+                hs(h_img, h_go, h_out, h_dw, h_di)
+            e2e_mode = "HostStep: pinned host buffers, 3 streams, copies overlapped with compute"
+        else:
+            def e2e_step():
+                x.copy_(h_img, non_blocking=True)
+                g_o.copy_(h_go, non_blocking=True)
+                run()
+                h_out.copy_(out, non_blocking=True)
+                h_dw.copy_(dw, non_blocking=True)
+                h_di.copy_(di, non_blocking=True)
+            e2e_mode = "serial copies + step"
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize()
-    ms_e2e = sum(time_steps(e2e_step, flush, args.steps)) / args.steps
-    t2 = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_value = world * flops_step / (float(t2.item()) * 1e-3) / 1e9
-    h2d = h_img.numel() * 4 + (0 if fwd_only else h_go.numel() * 4)
-    d2h = (h_out.numel() + (0 if fwd_only else h_dw.numel() + h_di.numel())) * 4
-    del h_img, h_go, h_out, h_dw, h_di
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        ms_e2e = sum(time_steps(e2e_step, flush, args.steps)) / args.steps
+        t2 = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e_value = world * flops_step / (float(t2.item()) * 1e-3) / 1e9
+        h2d = h_img.numel() * 4 + (0 if fwd_only else h_go.numel() * 4)
+        d2h = (h_out.numel() + (0 if fwd_only else h_dw.numel() + h_di.numel())) * 4
+        del h_img, h_go, h_out, h_dw, h_di
+        e2e = {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(t2.item()), "mode": e2e_mode}
 
     if rank != 0:
         return
@@ -568,8 +572,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "ms_per_layer": ms_max,
         "roofline": roofline,
         "kernels": kernels,
-        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": float(t2.item()), "mode": e2e_mode},
+        "e2e": e2e,
         "gpu_launches": launches,
         "allreduce": allreduce,
         "launch_mode": graph_note,
@@ -824,6 +827,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e through HostStep (whole-batch calls)")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) measurement (profiling runs)")
     ap.add_argument("--call-order", action="store_true",
                     help="forward then backward as two calls (default: one wino_forward_backward call "
                          "scheduled by data dependence)")
