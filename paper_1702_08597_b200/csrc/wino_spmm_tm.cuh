@@ -36,8 +36,8 @@ namespace tm {
 constexpr int THREADS = 1024;
 constexpr int ROWSETS = 8;   // warps per lane quarter
 constexpr int FILL_C = 128 / ROWSETS;  // stage rows c' each warp writes into TMEM
-constexpr int SLOTS = 4;        // handoff ring depth per (chain, stage boundary)
-constexpr int SLOT_BYTES = 512; // 32 lanes x 4 floats
+constexpr int SLOTS = 2;         // handoff ring depth per (chain, stage boundary), in row pairs
+constexpr int SLOT_BYTES = 1024; // a row pair: 2 x 32 lanes x 4 floats
 constexpr int TMEM_COLS = 512;
 
 __host__ __device__ constexpr int stages_for(int ncols) { return ncols <= 256 ? 2 : 4; }
@@ -306,7 +306,7 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     const uint32_t full_out = sbase + NSLOT * SLOT_BYTES + 8 * ring_out, empty_out = full_out + 8 * NSLOT;
     const uint32_t slot_in = sbase + ring_in * SLOT_BYTES + 16 * lane;
     const uint32_t slot_out = sbase + ring_out * SLOT_BYTES + 16 * lane;
-    int nrow_chain = 0;  // rows this chain has passed through its rings so far (all units)
+    int nrow_chain = 0;  // row pairs this chain has passed through its rings so far (all units)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int s = u / chunks, ch = u - s * chunks;
         const int t = ch * TW + 128 * b + 4 * lane;  // this lane's 4 columns
@@ -361,27 +361,40 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
         const int* rbp = (STAGED ? sbnd : bs) + g * (S + 1) + st;  // this warp's rows' segment starts
         const int2* cvb = STAGED ? scv - e_lo : cv;               // indexed by global entry numbers
         float* yp = Y + ((int64_t)s * nrows + g) * NTs + t;
-        for (int r = g; r < nrows; r += ROWSETS, ++nrow_chain, rbp += ROWSETS * (S + 1), yp += ROWSETS * (int64_t)NTs) {
+        // rows in pairs (r, r + ROWSETS): one handoff (wait, two slot halves, arrive) per pair
+        constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between the pair's rows
+        for (int r = g; r < nrows;
+             r += 2 * ROWSETS, ++nrow_chain, rbp += 2 * PB, yp += 2 * ROWSETS * (int64_t)NTs) {
             const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
             const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
-            const int e = rbp[0], ee = rbp[1];
-            unsigned long long acc[2] = {0ull, 0ull};
-            if (st > 0) {  // the previous stage's accumulators for this row
+            const bool hasb = r + ROWSETS < nrows;
+            const int ea = rbp[0], eea = rbp[1];
+            const int eb = hasb ? rbp[PB] : 0, eeb = hasb ? rbp[PB + 1] : 0;
+            unsigned long long acca[2] = {0ull, 0ull}, accb[2] = {0ull, 0ull};
+            if (st > 0) {  // the previous stage's accumulators for these rows
                 mb_wait_a(full_in + 8 * k, par);
-                lds4(slot_in + SLOT_BYTES * k, acc[0], acc[1]);
+                lds4(slot_in + SLOT_BYTES * k, acca[0], acca[1]);
+                lds4(slot_in + SLOT_BYTES * k + 512, accb[0], accb[1]);
                 mb_arrive_a(empty_in + 8 * k);
             }
-            walk<STAGED>(cvb, e, ee, tq, acc, z);
+            walk<STAGED>(cvb, ea, eea, tq, acca, z);
+            walk<STAGED>(cvb, eb, eeb, tq, accb, z);
             if (st == S - 1) {
                 if (tok) {
                     float4 o;
-                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[0]));
-                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[1]));
+                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acca[0]));
+                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acca[1]));
                     *reinterpret_cast<float4*>(yp) = o;
+                    if (hasb) {
+                        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(accb[0]));
+                        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(accb[1]));
+                        *reinterpret_cast<float4*>(yp + ROWSETS * (int64_t)NTs) = o;
+                    }
                 }
             } else {
                 if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
-                sts4(slot_out + SLOT_BYTES * k, acc[0], acc[1]);
+                sts4(slot_out + SLOT_BYTES * k, acca[0], acca[1]);
+                sts4(slot_out + SLOT_BYTES * k + 512, accb[0], accb[1]);
                 mb_arrive_a(full_out + 8 * k);
             }
         }
