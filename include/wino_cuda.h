@@ -231,7 +231,7 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
 #define WINO_OPT_AUTO_DENSITY 3
 /*   WINO_OPT_SPMM_OPERANDS: where the CSR kernels keep their dense operand chunk (Ĩ_F / dZ):
  *     0 (default) auto — tensor memory (tcgen05.ld, operand rows spread over the lane quarters
- *       by stage, wino_spmm_tm.cuh) when 128 < rows <= 512, the density is >= 7% and the work
+ *       by stage, wino_spmm_tm.cuh) when 128 < rows <= 512, the density is >= 4% and the work
  *       units fill the GPU twice; shared memory otherwise;
  *     1 shared memory always; 2 tensor memory whenever 128 < rows <= 512.  All are bitwise the
  *     reference's order. */

@@ -515,12 +515,13 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
                 int64_t NTs, int64_t NTr = -1) {
     if (NTr < 0) NTr = NTs;
     // TMEM operands where they pay (measured): their per-(row, stage) and per-unit
-    // costs are fixed, so they win once a row has enough entries (density >= 7%) and the units
-    // fill the GPU at least twice; below that the shared-memory kernel is faster
+    // costs are fixed, so they win once a row has enough entries (density >= 4%: c3 95% 317 vs
+    // 344 µs, 97% 272 vs 265) and the units fill the GPU at least twice; below that the
+    // shared-memory kernel is faster
     const double density = (double)p->nnz / ((double)p->P2 * p->K * p->C);
     const int64_t tm_units = (NTr + 512 / wino::tm::stages_for(ncols) - 1) / (512 / wino::tm::stages_for(ncols)) * p->P2;
     if (tm_applies(p, ncols) && p->tms[kind == K_SPMM_T ? 1 : 0].ready &&
-        (p->spmm_operands == 2 || (density >= 0.07 && tm_units >= 2 * p->sm_count)))
+        (p->spmm_operands == 2 || (density >= 0.04 && tm_units >= 2 * p->sm_count)))
         return launch_spmm_tm(p, st, kind, X, Y, nrows, ncols, NTs, NTr);
     switch (spmm_r(ncols)) {
         case 4: return launch_spmm_r<4>(p, st, kind, rowptr, cv, hptr, X, Y, nrows, ncols, NT, NTs, NTr);

@@ -36,15 +36,18 @@ namespace tm {
 constexpr int THREADS = 1024;
 constexpr int ROWSETS = 8;   // warps per lane quarter
 constexpr int FILL_C = 128 / ROWSETS;  // stage rows c' each warp writes into TMEM
-constexpr int SLOTS = 2;         // handoff ring depth per (chain, stage boundary), in row pairs
-constexpr int SLOT_BYTES = 1024; // a row pair: 2 x 32 lanes x 4 floats
+// rows per visit (one handoff per group of rows; measured: 3 for S = 2, 2 for S = 4)
+__host__ __device__ constexpr int group_rows(int S) { return S == 2 ? 3 : 2; }
+constexpr int SLOTS = 2;  // handoff ring depth per (chain, stage boundary), in row groups
+// a row group's slot: group_rows x 32 lanes x 4 floats
+__host__ __device__ constexpr int slot_bytes(int S) { return 512 * group_rows(S); }
 constexpr int TMEM_COLS = 512;
 
 __host__ __device__ constexpr int stages_for(int ncols) { return ncols <= 256 ? 2 : 4; }
 // handoff slots: chains x (S-1) boundaries x SLOTS (S=2: 8 chains, S=4: 4 chains -> <= 24 KB)
 __host__ __device__ constexpr int handoff_slots(int S) { return (4 / S) * ROWSETS * (S - 1) * SLOTS; }
 // handoff ring + barriers, then (STAGED) the slice's stage boundaries and its CSR entries
-__host__ __device__ constexpr int smem_fixed(int S) { return handoff_slots(S) * (SLOT_BYTES + 16) + 16; }
+__host__ __device__ constexpr int smem_fixed(int S) { return handoff_slots(S) * (slot_bytes(S) + 16) + 16; }
 __host__ __device__ constexpr int smem_bytes(int S, int nrows, int64_t entries) {
     return smem_fixed(S) + ((nrows * (S + 1) + 3) & ~3) * 4 + (int)(entries * 8);
 }
@@ -273,6 +276,8 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     constexpr int TB = 4 / S;
     constexpr int TW = 128 * TB;
     constexpr int NSLOT = handoff_slots(S);
+    constexpr int GR = group_rows(S);
+    constexpr int SLOT_BYTES = slot_bytes(S);
     extern __shared__ __align__(16) uint8_t tm_smem[];
     // [NSLOT][32 lanes][4 floats] handoff slots at tm_smem (addressed through slot_in / slot_out)
     uint64_t* full = reinterpret_cast<uint64_t*>(tm_smem + NSLOT * SLOT_BYTES);
@@ -361,6 +366,7 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
         const int* rbp = (STAGED ? sbnd : bs) + g * (S + 1) + st;  // this warp's rows' segment starts
         const int2* cvb = STAGED ? scv - e_lo : cv;               // indexed by global entry numbers
         float* yp = Y + ((int64_t)s * nrows + g) * NTs + t;
+        if constexpr (GR == 2) {
         // rows in pairs (r, r + ROWSETS): one handoff (wait, two slot halves, arrive) per pair
         constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between the pair's rows
         for (int r = g; r < nrows;
@@ -397,6 +403,47 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
                 sts4(slot_out + SLOT_BYTES * k + 512, accb[0], accb[1]);
                 mb_arrive_a(full_out + 8 * k);
             }
+        }
+        } else {
+        // rows in groups (r, r + ROWSETS, ...): one handoff (wait, GR slot parts, arrive) per group
+        constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between the group's rows
+        for (int r = g; r < nrows;
+             r += GR * ROWSETS, ++nrow_chain, rbp += GR * PB, yp += GR * ROWSETS * (int64_t)NTs) {
+            const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
+            const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
+            unsigned long long acc[GR][2];
+#pragma unroll
+            for (int i = 0; i < GR; ++i) acc[i][0] = acc[i][1] = 0ull;
+            if (st > 0) {  // the previous stage's accumulators for these rows
+                mb_wait_a(full_in + 8 * k, par);
+#pragma unroll
+                for (int i = 0; i < GR; ++i) lds4(slot_in + SLOT_BYTES * k + 512 * i, acc[i][0], acc[i][1]);
+                mb_arrive_a(empty_in + 8 * k);
+            }
+#pragma unroll
+            for (int i = 0; i < GR; ++i) {
+                const bool has = r + i * ROWSETS < nrows;
+                walk<STAGED>(cvb, has ? rbp[i * PB] : 0, has ? rbp[i * PB + 1] : 0, tq, acc[i], z);
+            }
+            if (st == S - 1) {
+                if (tok) {
+#pragma unroll
+                    for (int i = 0; i < GR; ++i) {
+                        if (r + i * ROWSETS < nrows) {
+                            float4 o;
+                            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[i][0]));
+                            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[i][1]));
+                            *reinterpret_cast<float4*>(yp + i * ROWSETS * (int64_t)NTs) = o;
+                        }
+                    }
+                }
+            } else {
+                if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
+#pragma unroll
+                for (int i = 0; i < GR; ++i) sts4(slot_out + SLOT_BYTES * k + 512 * i, acc[i][0], acc[i][1]);
+                mb_arrive_a(full_out + 8 * k);
+            }
+        }
         }
         // every warp is done reading this chunk (and the staged slice) before the next unit
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -214,7 +214,7 @@ class WinogradLayer:
 
     def set_spmm_operands(self, where: str):
         """CSR kernels' dense operand chunk: 'auto' (default; tensor memory where it is measured
-        faster: 128 < rows <= 512, density >= 7%, enough work units), 'smem' (shared memory always)
+        faster: 128 < rows <= 512, density >= 4%, enough work units), 'smem' (shared memory always)
         or 'tmem' (tensor memory whenever 128 < rows <= 512).  Bitwise the same results."""
         check(lib().wino_set_option(self._h, _lib.WINO_OPT_SPMM_OPERANDS, {"auto": 0, "smem": 1, "tmem": 2}[where]))
 
