@@ -221,6 +221,7 @@ struct wino_plan {
         size_t cap_cv = 0, cap_pidx = 0, cap_bnd = 0, cap_cnt = 0;
         int64_t n = 0;       // stream length
         int64_t max_slice = 0;
+        int R = 4, S = 2;    // t per lane and stages of the layout the stream encodes
         bool ready = false;
     } tms[2];
     double* d_xpart = nullptr;  // exact dW_F: scaled fp64 products per accumulation chunk [chunk][P2][K][C]
@@ -452,14 +453,18 @@ int build_tm_stream(wino_plan* p, int dir) {
     ts.ready = false;
     const int nrows = dir ? p->C : p->K, ncols = dir ? p->K : p->C;
     if (!(ncols > 128 && ncols <= 512) || p->nnz == 0) return WINO_OK;
-    const int S = t::stages_for(ncols);
+    // the layout: R t per lane and S stages (wino_spmm_tm.cuh)
+    const int R = t::lanes_t(ncols);
+    const int S = (ncols + t::stage_rows(R) - 1) / t::stage_rows(R) <= 2 ? 2 : 4;
+    ts.R = R;
+    ts.S = S;
     const int* rowptr = dir ? p->d_colptr : p->d_rowptr;
     const int2* cv = dir ? p->d_cvT : p->d_cv;
     const int64_t rows = (int64_t)p->P2 * nrows;
     int rc;
     if ((rc = grow(&ts.cnt, &ts.cap_cnt, (size_t)rows + 1)) || (rc = grow(&ts.bnd, &ts.cap_bnd, (size_t)rows * (S + 1))))
         return rc;
-    t::tm_count_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, nrows, p->P2, S, ts.cnt);
+    t::tm_count_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, nrows, p->P2, S, R, ts.cnt);
     t::tm_scan_kernel<<<1, 1024>>>(ts.cnt, (int)rows);
     CUDA_TRY(cudaGetLastError());
     std::vector<int> off((size_t)rows + 1);
@@ -470,7 +475,7 @@ int build_tm_stream(wino_plan* p, int dir) {
         ts.max_slice = std::max<int64_t>(ts.max_slice, off[(size_t)(s + 1) * nrows] - off[(size_t)s * nrows]);
     if ((rc = grow(&ts.cv, &ts.cap_cv, (size_t)ts.n + 2)) || (rc = grow(&ts.pidx, &ts.cap_pidx, (size_t)ts.n + 2)))
         return rc;
-    t::tm_fill_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, ts.cnt, nrows, p->P2, S, ts.cv, ts.pidx,
+    t::tm_fill_kernel<<<grid_for(rows, 128, p->sm_count), 128>>>(rowptr, cv, ts.cnt, nrows, p->P2, S, R, ts.cv, ts.pidx,
                                                                  ts.bnd);
     p->launches += 3;
     CUDA_TRY(cudaGetLastError());
@@ -490,14 +495,14 @@ int launch_spmm_tm(wino_plan* p, cudaStream_t st, int kind, const float* X, floa
     namespace t = wino::tm;
     const int dir = kind == K_SPMM_T ? 1 : 0;
     const auto& ts = p->tms[dir];
-    const int S = t::stages_for(ncols);
-    const int TW = 512 / S;
+    const int R = ts.R, S = ts.S;
+    const int TW = 32 * R * (4 / S);
     const int chunks = (int)((NTr + TW - 1) / TW);
     const int units = chunks * p->P2;
     // stage each slice's stream in shared memory when the largest slice fits
-    const int staged_smem = t::smem_bytes(S, nrows, ts.max_slice);
+    const int staged_smem = t::smem_bytes(R, S, nrows, ts.max_slice);
     const bool staged = staged_smem <= p->max_smem;
-    const int smem = std::max(staged ? staged_smem : t::smem_fixed(S), t::kMinSmem);
+    const int smem = std::max(staged ? staged_smem : t::smem_fixed(R, S), t::kMinSmem);
     const unsigned long long z = 0x8000000080000000ull;  // (-0.f, -0.f)
     const int grid = std::min(units, p->sm_count);
     Launch L(p, st, kind);
@@ -505,8 +510,8 @@ int launch_spmm_tm(wino_plan* p, cudaStream_t st, int kind, const float* X, floa
         set_smem_attr(kern, smem);
         kern<<<grid, t::THREADS, smem, st>>>(ts.cv, ts.bnd, X, Y, nrows, ncols, (int)NTs, (int)NTr, chunks, units, z);
     };
-    if (S == 2) staged ? go(t::spmm_tmem_kernel<2, true>) : go(t::spmm_tmem_kernel<2, false>);
-    else staged ? go(t::spmm_tmem_kernel<4, true>) : go(t::spmm_tmem_kernel<4, false>);
+    if (S == 2) staged ? go(t::spmm_tmem_kernel<4, 2, true>) : go(t::spmm_tmem_kernel<4, 2, false>);
+    else staged ? go(t::spmm_tmem_kernel<4, 4, true>) : go(t::spmm_tmem_kernel<4, 4, false>);
     return L.done();
 }
 
@@ -519,7 +524,9 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
     // 344 µs, 97% 272 vs 265) and the units fill the GPU at least twice; below that the
     // shared-memory kernel is faster
     const double density = (double)p->nnz / ((double)p->P2 * p->K * p->C);
-    const int64_t tm_units = (NTr + 512 / wino::tm::stages_for(ncols) - 1) / (512 / wino::tm::stages_for(ncols)) * p->P2;
+    const auto& tms = p->tms[kind == K_SPMM_T ? 1 : 0];
+    const int64_t tm_w = 32 * tms.R * (4 / tms.S);
+    const int64_t tm_units = (NTr + tm_w - 1) / tm_w * p->P2;  // CTA-units
     if (tm_applies(p, ncols) && p->tms[kind == K_SPMM_T ? 1 : 0].ready &&
         (p->spmm_operands == 2 || (density >= 0.04 && tm_units >= 2 * p->sm_count)))
         return launch_spmm_tm(p, st, kind, X, Y, nrows, ncols, NTs, NTr);

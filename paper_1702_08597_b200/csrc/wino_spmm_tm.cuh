@@ -35,21 +35,27 @@ namespace tm {
 
 constexpr int THREADS = 1024;
 constexpr int ROWSETS = 8;   // warps per lane quarter
-constexpr int FILL_C = 128 / ROWSETS;  // stage rows c' each warp writes into TMEM
+constexpr int TMEM_COLS = 512;
+// R = t per lane (tcgen05.ld.32x32b.xR per entry): a stage holds 512 / R input rows
+__host__ __device__ constexpr int stage_rows(int R) { return 512 / R; }
+// R for an operand of ncols rows (128 < ncols <= 512): 4.  (R = 8 — twice the multiply-adds per
+// entry instruction, but 64-row stages, i.e. 4 stages and 3 handoffs per row for 256 rows — was
+// measured slower at 80-95% sparsity: c3 90% 536 vs 439 µs; the kernel stays generic in R.)
+__host__ __device__ constexpr int lanes_t(int) { return 4; }
+__host__ __device__ constexpr int stages_for(int ncols) {
+    return (ncols + stage_rows(lanes_t(ncols)) - 1) / stage_rows(lanes_t(ncols)) <= 2 ? 2 : 4;
+}
 // rows per visit (one handoff per group of rows; measured: 3 for S = 2, 2 for S = 4)
 __host__ __device__ constexpr int group_rows(int S) { return S == 2 ? 3 : 2; }
 constexpr int SLOTS = 2;  // handoff ring depth per (chain, stage boundary), in row groups
-// a row group's slot: group_rows x 32 lanes x 4 floats
-__host__ __device__ constexpr int slot_bytes(int S) { return 512 * group_rows(S); }
-constexpr int TMEM_COLS = 512;
-
-__host__ __device__ constexpr int stages_for(int ncols) { return ncols <= 256 ? 2 : 4; }
-// handoff slots: chains x (S-1) boundaries x SLOTS (S=2: 8 chains, S=4: 4 chains -> <= 24 KB)
+// a row group's slot: group_rows x 32 lanes x R floats
+__host__ __device__ constexpr int slot_bytes(int R, int S) { return 128 * R * group_rows(S); }
+// handoff slots: chains x (S-1) boundaries x SLOTS
 __host__ __device__ constexpr int handoff_slots(int S) { return (4 / S) * ROWSETS * (S - 1) * SLOTS; }
 // handoff ring + barriers, then (STAGED) the slice's stage boundaries and its CSR entries
-__host__ __device__ constexpr int smem_fixed(int S) { return handoff_slots(S) * (slot_bytes(S) + 16) + 16; }
-__host__ __device__ constexpr int smem_bytes(int S, int nrows, int64_t entries) {
-    return smem_fixed(S) + ((nrows * (S + 1) + 3) & ~3) * 4 + (int)(entries * 8);
+__host__ __device__ constexpr int smem_fixed(int R, int S) { return handoff_slots(S) * (slot_bytes(R, S) + 16) + 16; }
+__host__ __device__ constexpr int smem_bytes(int R, int S, int nrows, int64_t entries) {
+    return smem_fixed(R, S) + ((nrows * (S + 1) + 3) & ~3) * 4 + (int)(entries * 8);
 }
 // > half the SM's shared memory: one CTA per SM (it owns all 512 TMEM columns)
 constexpr int kMinSmem = 120 * 1024;
@@ -99,6 +105,16 @@ __device__ __forceinline__ void tld4(uint32_t taddr, float (&v)[4]) {
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
                  : "r"(taddr));
 }
+__device__ __forceinline__ void tld8(uint32_t taddr, float (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(taddr));
+}
+template <int R>
+__device__ __forceinline__ void tld(uint32_t taddr, float (&v)[R]) {
+    if constexpr (R == 8) tld8(taddr, v);
+    else tld4(taddr, v);
+}
 __device__ __forceinline__ void tst16(uint32_t taddr, const float4 (&v)[4]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -130,14 +146,15 @@ __device__ __forceinline__ void madd2(unsigned long long& acc, float w, float x0
 }
 
 // ---- the kernel's operand stream: per (slice, row, stage) segments ----
-// For every (slice, row) and stage j the row's entries with col ∈ [128j, 128j+128), in CSR order,
-// as (TMEM column 4·(col − 128j), value), each segment padded to an even length with (the
+// For every (slice, row) and stage j the row's entries with col in stage j's rows [jW, jW + W)
+// (W = 512 / R), in CSR order, as (TMEM column R·(col − jW), value), each segment padded to an even length with (the
 // segment's last column, +0) — an exact no-op for finite operands (the accumulator starts at +0
 // and is never -0, so adding ±0 leaves it unchanged) — so every segment starts on a 16-byte
 // entry pair.  tbnd[(s·nrows + r)·(S+1) + j] = start of segment j (j = S: the row's end), global
 // positions in the stream; tpidx = source entry of each stream entry (-1: pad), for value refreshes.
 __global__ void tm_count_kernel(const int* __restrict__ rowptr, const int2* __restrict__ cv, int nrows, int P2,
-                                int S, int* __restrict__ cnt) {
+                                int S, int R, int* __restrict__ cnt) {
+    const int swc = 512 / R;
     const int64_t total = (int64_t)P2 * nrows;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -145,7 +162,7 @@ __global__ void tm_count_kernel(const int* __restrict__ rowptr, const int2* __re
         const int e0 = rowptr[(int64_t)s * (nrows + 1) + r], e1 = rowptr[(int64_t)s * (nrows + 1) + r + 1];
         int n = 0, j = 0, len = 0;
         for (int e = e0; e < e1; ++e) {
-            const int sj = cv[e].x >> 7;
+            const int sj = cv[e].x / swc;
             if (sj != j) {
                 n += (len + 1) & ~1;
                 len = 0;
@@ -182,8 +199,9 @@ __global__ void __launch_bounds__(1024) tm_scan_kernel(int* __restrict__ cnt, in
 }
 
 __global__ void tm_fill_kernel(const int* __restrict__ rowptr, const int2* __restrict__ cv,
-                               const int* __restrict__ off, int nrows, int P2, int S, int2* __restrict__ tcv,
+                               const int* __restrict__ off, int nrows, int P2, int S, int R, int2* __restrict__ tcv,
                                int* __restrict__ tpidx, int* __restrict__ tbnd) {
+    const int swc = 512 / R;
     const int64_t total = (int64_t)P2 * nrows;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -195,8 +213,8 @@ __global__ void tm_fill_kernel(const int* __restrict__ rowptr, const int2* __res
         for (int j = 0; j < S; ++j) {
             b[j] = pos;
             int last = 0, len = 0;
-            for (; e < e1 && (cv[e].x >> 7) == j; ++e, ++len) {
-                last = 4 * (cv[e].x & 127);
+            for (; e < e1 && cv[e].x / swc == j; ++e, ++len) {
+                last = R * (cv[e].x % swc);
                 tcv[pos] = make_int2(last, cv[e].y);
                 tpidx[pos++] = e;
             }
@@ -231,9 +249,9 @@ __device__ __forceinline__ int2 fetch_one(const int2* p) {
 }
 
 // NB entries of the stream from e (NB, e even): their TMEM reads in flight together, one wait
-template <int NB, bool STAGED>
+template <int NB, int R, bool STAGED>
 __device__ __forceinline__ void batch(const int2* __restrict__ cv, int e, uint32_t tq,
-                                      unsigned long long (&acc)[2], unsigned long long z) {
+                                      unsigned long long (&acc)[R / 2], unsigned long long z) {
     int2 a[NB];
 #pragma unroll
     for (int u = 0; u < NB; u += 2) {
@@ -241,45 +259,77 @@ __device__ __forceinline__ void batch(const int2* __restrict__ cv, int e, uint32
         a[u] = make_int2(two.x, two.y);
         a[u + 1] = make_int2(two.z, two.w);
     }
-    float x[NB][4];
+    float x[NB][R];
 #pragma unroll
-    for (int u = 0; u < NB; ++u) tld4(tq + (uint32_t)a[u].x, x[u]);
+    for (int u = 0; u < NB; ++u) tld<R>(tq + (uint32_t)a[u].x, x[u]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int u = 0; u < NB; ++u) {
-        madd2(acc[0], __int_as_float(a[u].y), x[u][0], x[u][1], z);
-        madd2(acc[1], __int_as_float(a[u].y), x[u][2], x[u][3], z);
+    for (int u = 0; u < NB; ++u)
+#pragma unroll
+        for (int h = 0; h < R / 2; ++h) madd2(acc[h], __int_as_float(a[u].y), x[u][2 * h], x[u][2 * h + 1], z);
+}
+
+// One row segment [e, ee) of a stage (e, ee even): acc (R t per lane as R/2 packed pairs) += the
+// entries' rounded products in order: batches of 8 and a final 6, 4 or 2 (R = 4); batches of 4
+// and a final 2 (R = 8: the same registers per batch)
+template <int R, bool STAGED>
+__device__ __forceinline__ void walk(const int2* __restrict__ cv, int e, int ee, uint32_t tq,
+                                     unsigned long long (&acc)[R / 2], unsigned long long z) {
+    if constexpr (R == 4) {
+        for (; e + 8 <= ee; e += 8) batch<8, 4, STAGED>(cv, e, tq, acc, z);
+        const int rem = ee - e;
+        if (rem == 6) batch<6, 4, STAGED>(cv, e, tq, acc, z);
+        else if (rem == 4) batch<4, 4, STAGED>(cv, e, tq, acc, z);
+        else if (rem == 2) batch<2, 4, STAGED>(cv, e, tq, acc, z);
+    } else {
+        for (; e + 4 <= ee; e += 4) batch<4, 8, STAGED>(cv, e, tq, acc, z);
+        if (e < ee) batch<2, 8, STAGED>(cv, e, tq, acc, z);
     }
 }
 
-// One row segment [e, ee) of a stage (e, ee even): acc (4 t per lane as 2 packed pairs) += the
-// entries' rounded products in order, in batches of 8 and one final batch of 6, 4 or 2.
-template <bool STAGED>
-__device__ __forceinline__ void walk(const int2* __restrict__ cv, int e, int ee, uint32_t tq,
-                                     unsigned long long (&acc)[2], unsigned long long z) {
-    for (; e + 8 <= ee; e += 8) batch<8, STAGED>(cv, e, tq, acc, z);
-    const int rem = ee - e;
-    if (rem == 6) batch<6, STAGED>(cv, e, tq, acc, z);
-    else if (rem == 4) batch<4, STAGED>(cv, e, tq, acc, z);
-    else if (rem == 2) batch<2, STAGED>(cv, e, tq, acc, z);
+// R floats of the handoff slot / the output row per lane, as R/2 packed pairs
+template <int R>
+__device__ __forceinline__ void sts_acc(uint32_t a, const unsigned long long (&acc)[R / 2]) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h) sts4(a + 16 * h, acc[2 * h], acc[2 * h + 1]);
+}
+template <int R>
+__device__ __forceinline__ void lds_acc(uint32_t a, unsigned long long (&acc)[R / 2]) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h) lds4(a + 16 * h, acc[2 * h], acc[2 * h + 1]);
+}
+template <int R>
+__device__ __forceinline__ void stg_acc(float* y, const unsigned long long (&acc)[R / 2]) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h) {
+        float4 o;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[2 * h]));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[2 * h + 1]));
+        *reinterpret_cast<float4*>(y + 4 * h) = o;
+    }
 }
 
 // X, Y: [P2][ncols or nrows][NTs] (offset to a column range's first column; NTr = owned columns),
 // cv / bnd: the padded stage-segment stream and its segment starts (tm_fill_kernel), units =
 // P2 · chunks, z = -0.0f pair.  STAGED: each unit copies its slice of the stream (and the slice's
 // segment starts) into shared memory; otherwise both are read through L1.
-template <int S, bool STAGED>
+template <int R, int S, bool STAGED>
 __global__ void __launch_bounds__(THREADS, 1)
 spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
                  const float* __restrict__ X, float* __restrict__ Y, int nrows, int ncols, int NTs, int NTr,
                  int chunks, int units, unsigned long long z) {
     constexpr int TB = 4 / S;
-    constexpr int TW = 128 * TB;
+    constexpr int SWC = stage_rows(R);          // input rows per stage
+    constexpr int QT = 32 * R;                  // t per lane quarter
+    constexpr int TW = QT * TB;                 // chunk width
+    constexpr int FILL_C = SWC / ROWSETS;       // stage rows each warp writes into TMEM
     constexpr int NSLOT = handoff_slots(S);
     constexpr int GR = group_rows(S);
-    constexpr int SLOT_BYTES = slot_bytes(S);
+    constexpr int SLOT_BYTES = slot_bytes(R, S);
+    constexpr int RB = 128 * R;                 // one row's part of a slot
+    static_assert(FILL_C * R == 64, "fill: 16 float4 per lane");
     extern __shared__ __align__(16) uint8_t tm_smem[];
-    // [NSLOT][32 lanes][4 floats] handoff slots at tm_smem (addressed through slot_in / slot_out)
+    // [NSLOT][GR rows][32 lanes][R floats] handoff slots at tm_smem (addressed through slot_in / slot_out)
     uint64_t* full = reinterpret_cast<uint64_t*>(tm_smem + NSLOT * SLOT_BYTES);
     uint64_t* empty = full + NSLOT;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + NSLOT);
@@ -309,12 +359,12 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
     const uint32_t sbase = su32(tm_smem);
     const uint32_t full_in = sbase + NSLOT * SLOT_BYTES + 8 * ring_in, empty_in = full_in + 8 * NSLOT;
     const uint32_t full_out = sbase + NSLOT * SLOT_BYTES + 8 * ring_out, empty_out = full_out + 8 * NSLOT;
-    const uint32_t slot_in = sbase + ring_in * SLOT_BYTES + 16 * lane;
-    const uint32_t slot_out = sbase + ring_out * SLOT_BYTES + 16 * lane;
-    int nrow_chain = 0;  // row pairs this chain has passed through its rings so far (all units)
+    const uint32_t slot_in = sbase + ring_in * SLOT_BYTES + 4 * R * lane;
+    const uint32_t slot_out = sbase + ring_out * SLOT_BYTES + 4 * R * lane;
+    int nrow_chain = 0;  // row groups this chain has passed through its rings so far (all units)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int s = u / chunks, ch = u - s * chunks;
-        const int t = ch * TW + 128 * b + 4 * lane;  // this lane's 4 columns
+        const int t = ch * TW + QT * b + R * lane;  // this lane's R columns
         const bool tok = t < NTr;
         // ---- stage the slice's boundaries and entries (cp.async, overlaps the fill) ----
         const int* bs = bnd + (int64_t)s * nrows * (S + 1);
@@ -331,20 +381,22 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        // ---- fill: X(128·st + c', t .. t+3) for this warp's FILL_C c' -> TMEM columns 4c' ----
+        // ---- fill: X(SWC·st + c', t .. t+R) for this warp's FILL_C rows c' -> TMEM columns R·c' ----
+        // (16 float4 per lane; float4 f = row FILL_C·g + f / (R/4), part f % (R/4), column 4f + R·FILL_C·g)
         {
-            const float* xs = X + ((int64_t)s * ncols + 128 * st) * NTs + t;
+            const int c0 = SWC * st + FILL_C * g;
+            const float* xs = X + ((int64_t)s * ncols + c0) * NTs + t;
 #pragma unroll
-            for (int h = 0; h < FILL_C / 4; ++h) {
+            for (int h = 0; h < 4; ++h) {
                 float4 v[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int cl = FILL_C * g + 4 * h + i;
-                    v[i] = (tok && 128 * st + cl < ncols)
-                               ? __ldg(reinterpret_cast<const float4*>(xs + (int64_t)cl * NTs))
+                    const int f = 4 * h + i, cl = f / (R / 4), pt = f % (R / 4);
+                    v[i] = (tok && c0 + cl < ncols)
+                               ? __ldg(reinterpret_cast<const float4*>(xs + (int64_t)cl * NTs + 4 * pt))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-                tst16(tq + (uint32_t)(4 * (FILL_C * g + 4 * h)), v);
+                tst16(tq + (uint32_t)(R * FILL_C * g + 16 * h), v);
             }
         }
         if constexpr (STAGED) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -355,95 +407,83 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
         // ---- the next unit's chunk rows of this warp: L2 prefetch behind this unit's compute ----
         if (u + (int)gridDim.x < units && lane < FILL_C) {
             const int un = u + gridDim.x, sn = un / chunks, chn = un - sn * chunks;
-            const int cl = FILL_C * g + lane, tn = chn * TW + 128 * b;
-            if (128 * st + cl < ncols && tn < NTr) {
-                const float* src = X + ((int64_t)sn * ncols + 128 * st + cl) * NTs + tn;
-                const int bytes = 4 * min(128, NTr - tn);  // multiple of 16
+            const int cl = SWC * st + FILL_C * g + lane, tn = chn * TW + QT * b;
+            if (cl < ncols && tn < NTr) {
+                const float* src = X + ((int64_t)sn * ncols + cl) * NTs + tn;
+                const int bytes = 4 * min(QT, NTr - tn);  // multiple of 16
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
             }
         }
-        // ---- rows of this chain ----
+        // ---- rows of this chain, in groups (r, r + ROWSETS, ...): one handoff per group ----
         const int* rbp = (STAGED ? sbnd : bs) + g * (S + 1) + st;  // this warp's rows' segment starts
         const int2* cvb = STAGED ? scv - e_lo : cv;               // indexed by global entry numbers
         float* yp = Y + ((int64_t)s * nrows + g) * NTs + t;
+        constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between a group's rows
         if constexpr (GR == 2) {
-        // rows in pairs (r, r + ROWSETS): one handoff (wait, two slot halves, arrive) per pair
-        constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between the pair's rows
-        for (int r = g; r < nrows;
-             r += 2 * ROWSETS, ++nrow_chain, rbp += 2 * PB, yp += 2 * ROWSETS * (int64_t)NTs) {
-            const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
-            const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
-            const bool hasb = r + ROWSETS < nrows;
-            const int ea = rbp[0], eea = rbp[1];
-            const int eb = hasb ? rbp[PB] : 0, eeb = hasb ? rbp[PB + 1] : 0;
-            unsigned long long acca[2] = {0ull, 0ull}, accb[2] = {0ull, 0ull};
-            if (st > 0) {  // the previous stage's accumulators for these rows
-                mb_wait_a(full_in + 8 * k, par);
-                lds4(slot_in + SLOT_BYTES * k, acca[0], acca[1]);
-                lds4(slot_in + SLOT_BYTES * k + 512, accb[0], accb[1]);
-                mb_arrive_a(empty_in + 8 * k);
-            }
-            walk<STAGED>(cvb, ea, eea, tq, acca, z);
-            walk<STAGED>(cvb, eb, eeb, tq, accb, z);
-            if (st == S - 1) {
-                if (tok) {
-                    float4 o;
-                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acca[0]));
-                    asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acca[1]));
-                    *reinterpret_cast<float4*>(yp) = o;
-                    if (hasb) {
-                        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(accb[0]));
-                        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(accb[1]));
-                        *reinterpret_cast<float4*>(yp + ROWSETS * (int64_t)NTs) = o;
-                    }
+            for (int r = g; r < nrows;
+                 r += 2 * ROWSETS, ++nrow_chain, rbp += 2 * PB, yp += 2 * ROWSETS * (int64_t)NTs) {
+                const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
+                const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
+                const bool hasb = r + ROWSETS < nrows;
+                const int ea = rbp[0], eea = rbp[1];
+                const int eb = hasb ? rbp[PB] : 0, eeb = hasb ? rbp[PB + 1] : 0;
+                unsigned long long acca[R / 2], accb[R / 2];
+#pragma unroll
+                for (int h = 0; h < R / 2; ++h) acca[h] = accb[h] = 0ull;
+                if (st > 0) {  // the previous stage's accumulators for these rows
+                    mb_wait_a(full_in + 8 * k, par);
+                    lds_acc<R>(slot_in + SLOT_BYTES * k, acca);
+                    lds_acc<R>(slot_in + SLOT_BYTES * k + RB, accb);
+                    mb_arrive_a(empty_in + 8 * k);
                 }
-            } else {
-                if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
-                sts4(slot_out + SLOT_BYTES * k, acca[0], acca[1]);
-                sts4(slot_out + SLOT_BYTES * k + 512, accb[0], accb[1]);
-                mb_arrive_a(full_out + 8 * k);
+                walk<R, STAGED>(cvb, ea, eea, tq, acca, z);
+                walk<R, STAGED>(cvb, eb, eeb, tq, accb, z);
+                if (st == S - 1) {
+                    if (tok) {
+                        stg_acc<R>(yp, acca);
+                        if (hasb) stg_acc<R>(yp + ROWSETS * (int64_t)NTs, accb);
+                    }
+                } else {
+                    if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
+                    sts_acc<R>(slot_out + SLOT_BYTES * k, acca);
+                    sts_acc<R>(slot_out + SLOT_BYTES * k + RB, accb);
+                    mb_arrive_a(full_out + 8 * k);
+                }
             }
-        }
         } else {
-        // rows in groups (r, r + ROWSETS, ...): one handoff (wait, GR slot parts, arrive) per group
-        constexpr int PB = ROWSETS * (S + 1);  // segment-start stride between the group's rows
-        for (int r = g; r < nrows;
-             r += GR * ROWSETS, ++nrow_chain, rbp += GR * PB, yp += GR * ROWSETS * (int64_t)NTs) {
-            const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
-            const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
-            unsigned long long acc[GR][2];
+            for (int r = g; r < nrows;
+                 r += GR * ROWSETS, ++nrow_chain, rbp += GR * PB, yp += GR * ROWSETS * (int64_t)NTs) {
+                const uint32_t k = (uint32_t)nrow_chain & (SLOTS - 1);
+                const uint32_t par = (uint32_t)(nrow_chain / SLOTS) & 1u;
+                unsigned long long acc[GR][R / 2];
 #pragma unroll
-            for (int i = 0; i < GR; ++i) acc[i][0] = acc[i][1] = 0ull;
-            if (st > 0) {  // the previous stage's accumulators for these rows
-                mb_wait_a(full_in + 8 * k, par);
+                for (int i = 0; i < GR; ++i)
 #pragma unroll
-                for (int i = 0; i < GR; ++i) lds4(slot_in + SLOT_BYTES * k + 512 * i, acc[i][0], acc[i][1]);
-                mb_arrive_a(empty_in + 8 * k);
-            }
+                    for (int h = 0; h < R / 2; ++h) acc[i][h] = 0ull;
+                if (st > 0) {  // the previous stage's accumulators for these rows
+                    mb_wait_a(full_in + 8 * k, par);
 #pragma unroll
-            for (int i = 0; i < GR; ++i) {
-                const bool has = r + i * ROWSETS < nrows;
-                walk<STAGED>(cvb, has ? rbp[i * PB] : 0, has ? rbp[i * PB + 1] : 0, tq, acc[i], z);
-            }
-            if (st == S - 1) {
-                if (tok) {
-#pragma unroll
-                    for (int i = 0; i < GR; ++i) {
-                        if (r + i * ROWSETS < nrows) {
-                            float4 o;
-                            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[i][0]));
-                            asm("mov.b64 {%0,%1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[i][1]));
-                            *reinterpret_cast<float4*>(yp + i * ROWSETS * (int64_t)NTs) = o;
-                        }
-                    }
+                    for (int i = 0; i < GR; ++i) lds_acc<R>(slot_in + SLOT_BYTES * k + RB * i, acc[i]);
+                    mb_arrive_a(empty_in + 8 * k);
                 }
-            } else {
-                if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
 #pragma unroll
-                for (int i = 0; i < GR; ++i) sts4(slot_out + SLOT_BYTES * k + 512 * i, acc[i][0], acc[i][1]);
-                mb_arrive_a(full_out + 8 * k);
+                for (int i = 0; i < GR; ++i) {
+                    const bool has = r + i * ROWSETS < nrows;
+                    walk<R, STAGED>(cvb, has ? rbp[i * PB] : 0, has ? rbp[i * PB + 1] : 0, tq, acc[i], z);
+                }
+                if (st == S - 1) {
+                    if (tok) {
+#pragma unroll
+                        for (int i = 0; i < GR; ++i)
+                            if (r + i * ROWSETS < nrows) stg_acc<R>(yp + i * ROWSETS * (int64_t)NTs, acc[i]);
+                    }
+                } else {
+                    if (nrow_chain >= SLOTS) mb_wait_a(empty_out + 8 * k, par ^ 1u);
+#pragma unroll
+                    for (int i = 0; i < GR; ++i) sts_acc<R>(slot_out + SLOT_BYTES * k + RB * i, acc[i]);
+                    mb_arrive_a(full_out + 8 * k);
+                }
             }
-        }
         }
         // every warp is done reading this chunk (and the staged slice) before the next unit
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
