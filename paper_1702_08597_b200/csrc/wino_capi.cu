@@ -573,7 +573,8 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
         const size_t smem = (size_t)cg * per_c;
         set_smem_attr(wino::input_grad_kernel<M, P, CF>, (int)std::max<size_t>(smem, 48 * 1024));
         wino::input_grad_kernel<M, P, CF><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
-            DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg);
+            DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg,
+            0x8000000080000000ull);
     } else {
         const int64_t total = (int64_t)n * p->C * p->H * p->W;
         wino::input_grad_direct_kernel<M, P, CF><<<grid_for(total, 256, p->sm_count), 256, 0, st>>>(

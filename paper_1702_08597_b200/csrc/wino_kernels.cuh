@@ -71,6 +71,42 @@ __device__ __forceinline__ float cmadd(float acc, float c, float x) {
     return madd(acc, c, x);
 }
 
+// Packed fp32 pairs (FFMA2 / FADD2 on Blackwell): two lanes of the same rounded operations.
+// mul2 forms the rounded product with a runtime -0 addend z (so ptxas cannot contract it with the
+// following add2 into one rounding); every result is bitwise the scalar __fmul_rn / __fadd_rn.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long v;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(a), "f"(b));
+    return v;
+}
+__device__ __forceinline__ void upk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long x, unsigned long long w, unsigned long long z) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(w), "l"(z));
+    return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// acc2 += c·x2 with a compile-time coefficient: zero skipped, ±1 without the multiply (as cmadd)
+template <class CF>
+__device__ __forceinline__ unsigned long long cmadd2(unsigned long long acc, float c, unsigned long long x,
+                                                     unsigned long long z) {
+    if (c == 0.f) return acc;
+    if (c == 1.f) return add2(acc, x);
+    if (c == -1.f) return sub2(acc, x);
+    return add2(acc, mul2(x, pk2(c, c), z));
+}
+
 // The same transform in the reference's doubles (the exact dW_F digit kernels, wino_xdw.cuh).
 struct CoefsD {
     double a[kMaxP * kMaxP];  // a1: p×m row-major
@@ -125,14 +161,15 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                 for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + i), d[k][j]);
                 tmp[i][j] = acc;
             }
+        float* vp = V + (int64_t)c * NTs + nt;
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
+            for (int j = 0; j < P; ++j, vp += plane) {
                 float acc = 0.f;
 #pragma unroll
                 for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
-                V[(int64_t)(i * P + j) * plane + (int64_t)c * NTs + nt] = acc;
+                *vp = acc;
             }
     }
 }
@@ -214,7 +251,8 @@ __device__ __forceinline__ float tile_grad_entry(const float* __restrict__ dv, i
 template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Coefs cf, int C,
-                  int H, int W, int pad, int tiles_y, int tiles_x, int T, int NTs, int CG) {
+                  int H, int W, int pad, int tiles_y, int tiles_x, int T, int NTs, int CG,
+                  unsigned long long z) {
     constexpr int TS = P * P + 1;  // odd per-tile stride: conflict-free tile stores
     extern __shared__ float gsm[];  // [CG][T][TS]
     const int n = blockIdx.y;
@@ -229,7 +267,7 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
-            for (int l = 0; l < P; ++l) x[k][l] = __ldg(src + (int64_t)(k * P + l) * plane);
+            for (int l = 0; l < P; ++l, src += plane) x[k][l] = __ldg(src);
         float m1[P][P];
 #pragma unroll
         for (int i = 0; i < P; ++i)

@@ -281,7 +281,8 @@ input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ 
             float acc = 0.f;
 #pragma unroll
             for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + l), t32[k]);
-            if (vok) vp[(int64_t)(i * P + l) * vplane] = acc;
+            if (vok) *vp = acc;
+            vp += vplane;
         }
         double t64[P];
 #pragma unroll
@@ -369,7 +370,8 @@ grad_z_digits_kernel(const float* __restrict__ dO, const float* __restrict__ rel
             float acc = 0.f;
 #pragma unroll
             for (int x = 0; x < M; ++x) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, l * M + x), m32[x]);
-            if (vok) zp[(int64_t)(i * P + l) * zplane] = acc;
+            if (vok) *zp = acc;
+            zp += zplane;
         }
         double m64[M];
 #pragma unroll
