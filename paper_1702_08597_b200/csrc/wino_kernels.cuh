@@ -307,23 +307,24 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
         const float* gul = gu - TS;                // (ty-1, tx-1)
         const bool up = ty > 0, left = tx > 0;
         const int ni = ty == tiles_y - 1 ? P : M, nj = tx == tiles_x - 1 ? P : M;
-        float* dst = dI + ((int64_t)n * C + c) * H * W;
+        const int xb = tx * M - pad;
+        float* dst = dI + ((int64_t)n * C + c) * H * W + xb;  // + y·W per row, + j per pixel
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             if (i >= ni) break;
             const int y = ty * M + i - pad;
             if ((unsigned)y >= (unsigned)H) continue;
+            float* drow = dst + y * W;
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 if (j >= nj) break;
-                const int x = tx * M + j - pad;
-                if ((unsigned)x >= (unsigned)W) continue;
+                if ((unsigned)(xb + j) >= (unsigned)W) continue;
                 float acc = 0.f;
                 if (i < O && j < O && up && left) acc = __fadd_rn(acc, gul[(i + M) * P + j + M]);
                 if (i < O && up) acc = __fadd_rn(acc, gu[(i + M) * P + j]);
                 if (j < O && left) acc = __fadd_rn(acc, gl[i * P + j + M]);
                 acc = __fadd_rn(acc, g0[i * P + j]);
-                dst[y * W + x] = acc;
+                drow[j] = acc;
             }
         }
     }
