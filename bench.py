@@ -515,7 +515,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
             from paper_1702_08597_b200.graph import GraphedStep
             from paper_1702_08597_b200.pipeline import PipelinedHostStep
 
-            ps = PipelinedHostStep(layer, lb.cache, x, g_o, out, dw, di, chunks=args.e2e_chunks)
+            ps = PipelinedHostStep(layer, lb.cache, x, g_o, out, dw, di, chunks=("auto" if args.e2e_chunks == "auto"
+                                           else [int(v) for v in args.e2e_chunks.split(",")] if "," in args.e2e_chunks
+                                           else int(args.e2e_chunks)))
             # the whole pipelined step (copies on 3 streams + range kernels) as one CUDA graph
             e2e_step = GraphedStep(lambda: ps(h_img, h_go, h_out, h_dw, h_di)).replay
             e2e_mode = (f"PipelinedHostStep in one CUDA graph: pinned host buffers, {len(ps.bounds)} image chunks, "
@@ -826,7 +828,9 @@ def main():
     ap.add_argument("--sweep-steps", type=int, default=10, help="timed steps per sweep point")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e through HostStep (whole-batch calls)")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks of the pipelined e2e step")
+    ap.add_argument("--e2e-chunks", default="auto",
+                    help="image chunks of the pipelined e2e step: auto, a count (equal chunks) or a comma list of "
+                         "image counts, e.g. 16,16,16,8,4,4")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) measurement (profiling runs)")
     ap.add_argument("--call-order", action="store_true",
                     help="forward then backward as two calls (default: one wino_forward_backward call "

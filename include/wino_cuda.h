@@ -233,8 +233,10 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *     0 (default) auto — tensor memory (tcgen05.ld, operand rows spread over the lane quarters
  *       by stage, wino_spmm_tm.cuh) when 128 < rows <= 512, the density is >= 4% and the work
  *       units fill the GPU twice; shared memory otherwise;
- *     1 shared memory always; 2 tensor memory whenever 128 < rows <= 512.  All are bitwise the
- *     reference's order. */
+ *     1 shared memory always; 2 tensor memory whenever 128 < rows <= 512; 3 hybrid whenever
+ *     128 < rows <= 256: operand rows [0,128) in tensor memory and the rest in shared memory, one
+ *     warp per output row and no stage handoffs (auto picks it when the slice's entry stream fits
+ *     in shared memory next to the chunk).  All are bitwise the reference's order. */
 #define WINO_OPT_SPMM_OPERANDS 4
 WINO_API int wino_set_option(wino_plan* plan, int option, int value);
 

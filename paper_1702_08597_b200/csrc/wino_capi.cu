@@ -211,7 +211,7 @@ struct wino_plan {
     int64_t* d_slice_off = nullptr;
     // TMEM SpMM (wino_spmm_tm.cuh): the padded stage-segment streams of the CSR [0] and CSC [1],
     // rebuilt whenever the structure changes, values refreshed by wino_values_updated
-    int spmm_operands = 0;  // WINO_OPT_SPMM_OPERANDS: 0 auto, 1 shared memory, 2 tensor memory
+    int spmm_operands = 0;  // WINO_OPT_SPMM_OPERANDS: 0 auto, 1 shared memory, 2 tensor memory, 3 hybrid
     void* dw_comm = nullptr;  // wino_set_dw_allreduce: ncclComm_t of the in-backward dW_F exchange
     struct TmStream {        // the TMEM SpMM's padded stage-segment stream of one direction
         int2* cv = nullptr;  // (TMEM column, value)
@@ -515,6 +515,31 @@ int launch_spmm_tm(wino_plan* p, cudaStream_t st, int kind, const float* X, floa
     return L.done();
 }
 
+// K2/K6 with operand rows [0,128) in TMEM and [128, ncols) in shared memory (128 < ncols <= 256)
+bool hyb_applies(const wino_plan* p, int ncols, int dir) {
+    return ncols > 128 && ncols <= 256 && p->tms[dir].ready && p->tms[dir].S == 2 && p->tms[dir].R == 4;
+}
+
+int launch_spmm_hyb(wino_plan* p, cudaStream_t st, int kind, const float* X, float* Y, int nrows, int ncols,
+                    int64_t NTs, int64_t NTr) {
+    namespace t = wino::tm;
+    const auto& ts = p->tms[kind == K_SPMM_T ? 1 : 0];
+    const int chunks = (int)((NTr + t::HYB_TW - 1) / t::HYB_TW);
+    const int units = chunks * p->P2;
+    const int staged_smem = t::hyb_smem_bytes(ncols, nrows, ts.max_slice);
+    const bool staged = staged_smem <= p->max_smem;
+    const int smem = std::max(staged ? staged_smem : t::hyb_smem_fixed(ncols), t::kMinSmem);
+    const unsigned long long z = 0x8000000080000000ull;  // (-0.f, -0.f)
+    const int grid = std::min(units, p->sm_count);
+    Launch L(p, st, kind);
+    auto go = [&](auto kern) {
+        set_smem_attr(kern, smem);
+        kern<<<grid, t::THREADS, smem, st>>>(ts.cv, ts.bnd, X, Y, nrows, ncols, (int)NTs, (int)NTr, chunks, units, z);
+    };
+    staged ? go(t::spmm_hyb_kernel<true>) : go(t::spmm_hyb_kernel<false>);
+    return L.done();
+}
+
 int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, const int2* cv,
                 const std::vector<int>& hptr, const float* X, float* Y, int nrows, int ncols, int64_t NT,
                 int64_t NTs, int64_t NTr = -1) {
@@ -527,6 +552,14 @@ int launch_spmm(wino_plan* p, cudaStream_t st, int kind, const int* rowptr, cons
     const auto& tms = p->tms[kind == K_SPMM_T ? 1 : 0];
     const int64_t tm_w = 32 * tms.R * (4 / tms.S);
     const int64_t tm_units = (NTr + tm_w - 1) / tm_w * p->P2;  // CTA-units
+    // hybrid operands (TMEM + shared memory, no stage handoffs) when its staged stream fits next to
+    // the shared-memory half of the chunk (c3: 90% 428 vs 441 µs, 95% 284 vs 315; unstaged it loses)
+    const int dir = kind == K_SPMM_T ? 1 : 0;
+    if (hyb_applies(p, ncols, dir) &&
+        (p->spmm_operands == 3 ||
+         (p->spmm_operands == 0 && density >= 0.04 && tm_units >= 2 * p->sm_count &&
+          wino::tm::hyb_smem_bytes(ncols, nrows, tms.max_slice) <= p->max_smem)))
+        return launch_spmm_hyb(p, st, kind, X, Y, nrows, ncols, NTs, NTr);
     if (tm_applies(p, ncols) && p->tms[kind == K_SPMM_T ? 1 : 0].ready &&
         (p->spmm_operands == 2 || (density >= 0.04 && tm_units >= 2 * p->sm_count)))
         return launch_spmm_tm(p, st, kind, X, Y, nrows, ncols, NTs, NTr);
@@ -1853,8 +1886,8 @@ int wino_set_option(wino_plan* p, int option, int value) {
         return p->contraction_mode == 2 ? apply_contraction(p) : WINO_OK;
     }
     if (option == WINO_OPT_SPMM_OPERANDS) {
-        if (value < 0 || value > 2)
-            return set_err(WINO_INVALID_ARGUMENT, "spmm operands: 0 auto, 1 shared memory, 2 tensor memory");
+        if (value < 0 || value > 3)
+            return set_err(WINO_INVALID_ARGUMENT, "spmm operands: 0 auto, 1 shared memory, 2 tensor memory, 3 hybrid");
         p->spmm_operands = value;
         return p->has_weights && !p->dense ? build_tm_streams(p) : WINO_OK;
     }

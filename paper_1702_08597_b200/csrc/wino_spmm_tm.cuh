@@ -494,5 +494,166 @@ spmm_tmem_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd,
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "r"(TMEM_COLS));
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// K2 / K6, hybrid operand delivery (128 < ncols <= 256): input rows [0, 128) of the chunk in
+// tensor memory, rows [128, ncols) in shared memory.  The staged kernel above is bound by what the
+// TMEM read path delivers (every multiply-add needs its own 4-byte operand) and pays a handoff per
+// (row, stage); here the two operand halves come through two different pipes (tcgen05.ld and LDS)
+// and ONE warp walks a whole row: its stage-0 segment against TMEM, its stage-1 segment against
+// shared memory, the same accumulators throughout — no handoff ring, no barriers inside a unit.
+// Same operand stream (tm_fill_kernel, S = 2) and the same per-element operation order: bitwise
+// the staged kernel, the shared-memory kernel and the reference.
+//
+// Chunk = 256 t (two 128-t blocks).  Warp w: lane quarter q = w & 3, t-block b = q & 1, row set
+// g = (w >> 2) + 8·(q >> 1) of 16.  A warp only reads its own lane quarter of TMEM, so quarters
+// q and q + 2 hold the same block b of rows [0, 128): TMEM lane 32q + l, columns 4c .. 4c+3 =
+// X(c, t0 + 128b + 4l .. +3).  Shared memory: xs[c − 128][256] floats (a warp's LDS.128 reads 512
+// contiguous bytes: conflict-free).
+// ---------------------------------------------------------------------------------------------
+constexpr int HYB_TW = 256;
+__host__ __device__ constexpr int hyb_x_bytes(int ncols) { return (ncols - 128) * HYB_TW * 4; }
+__host__ __device__ constexpr int hyb_smem_fixed(int ncols) { return hyb_x_bytes(ncols) + 16; }
+__host__ __device__ constexpr int hyb_smem_bytes(int ncols, int nrows, int64_t entries) {
+    return hyb_smem_fixed(ncols) + ((nrows * 3 + 3) & ~3) * 4 + (int)(entries * 8);
+}
+
+// NB stream entries from e against the shared-memory rows: xl = this lane's 16 bytes of row 128
+template <int NB, bool STAGED>
+__device__ __forceinline__ void batch_sm(const int2* __restrict__ cv, int e, uint32_t xl,
+                                         unsigned long long (&acc)[2], unsigned long long z) {
+    int2 a[NB];
+#pragma unroll
+    for (int u = 0; u < NB; u += 2) {
+        const int4 two = fetch_pair<STAGED>(cv + e + u);
+        a[u] = make_int2(two.x, two.y);
+        a[u + 1] = make_int2(two.z, two.w);
+    }
+    float x[NB][4];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {  // stream column = 4·(c − 128): row stride 1024 bytes
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x[u][0]), "=f"(x[u][1]), "=f"(x[u][2]), "=f"(x[u][3])
+                     : "r"(xl + ((uint32_t)a[u].x << 8)));
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) madd2(acc[h], __int_as_float(a[u].y), x[u][2 * h], x[u][2 * h + 1], z);
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void walk_sm(const int2* __restrict__ cv, int e, int ee, uint32_t xl,
+                                        unsigned long long (&acc)[2], unsigned long long z) {
+    for (; e + 8 <= ee; e += 8) batch_sm<8, STAGED>(cv, e, xl, acc, z);
+    const int rem = ee - e;
+    if (rem == 6) batch_sm<6, STAGED>(cv, e, xl, acc, z);
+    else if (rem == 4) batch_sm<4, STAGED>(cv, e, xl, acc, z);
+    else if (rem == 2) batch_sm<2, STAGED>(cv, e, xl, acc, z);
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(THREADS, 1)
+spmm_hyb_kernel(const int2* __restrict__ cv, const int* __restrict__ bnd, const float* __restrict__ X,
+                float* __restrict__ Y, int nrows, int ncols, int NTs, int NTr, int chunks, int units,
+                unsigned long long z) {
+    constexpr int R = 4, QT = 128, TW = HYB_TW, FILL_C = 16, NSETS = 16;
+    extern __shared__ __align__(16) uint8_t tm_smem[];
+    const int xbytes = hyb_x_bytes(ncols);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tm_smem + xbytes);
+    int* sbnd = reinterpret_cast<int*>(tm_smem + xbytes + 16);    // [nrows][3]
+    int2* scv = reinterpret_cast<int2*>(sbnd + ((nrows * 3 + 3) & ~3));  // slice entries
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, b = q & 1, wq = warp >> 2;
+    const int g = wq + 8 * (q >> 1);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tq = *tslot + ((uint32_t)(32 * q) << 16);
+    const uint32_t xl = su32(tm_smem) + 4 * (QT * b + R * lane);
+    const int nsm = ncols - 128;  // rows held in shared memory
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int s = u / chunks, ch = u - s * chunks;
+        const int t = ch * TW + QT * b + R * lane;  // this lane's 4 columns
+        const bool tok = t < NTr;
+        const int* bs = bnd + (int64_t)s * nrows * 3;
+        const int e_lo = STAGED ? __ldg(bs) : 0;                    // even
+        const int e_hi = STAGED ? __ldg(bs + nrows * 3 - 1) : 0;     // even
+        const float* xs = X + (int64_t)s * ncols * NTs;
+        // ---- rows [128, ncols) of the chunk -> shared memory (cp.async, zero-filled past NTr) ----
+        for (int i = threadIdx.x; i < nsm * (TW / 4); i += THREADS) {
+            const int row = i >> 6, c4 = i & 63;
+            const int tt = ch * TW + 4 * c4;
+            const bool ok = tt < NTr;
+            const float* src = xs + (int64_t)(128 + row) * NTs + (ok ? tt : 0);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(tm_smem) + 16 * i), "l"(src),
+                         "r"(ok ? 16 : 0));
+        }
+        if constexpr (STAGED) {
+            const int nb = nrows * 3;
+            for (int i = threadIdx.x; i < nb; i += THREADS)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(sbnd + i)), "l"(bs + i));
+            const int n2 = (e_hi - e_lo) >> 1;  // whole 16-byte pairs
+            const int4* src = reinterpret_cast<const int4*>(cv + e_lo);
+            int4* dst = reinterpret_cast<int4*>(scv);
+            for (int i = threadIdx.x; i < n2; i += THREADS)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst + i)), "l"(src + i));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // ---- rows [0, 128) -> this warp's lane quarter: its 16 rows c0 .. c0+15, 16 float4 per lane ----
+        {
+            const int c0 = FILL_C * wq;
+            const float* xr = xs + (int64_t)c0 * NTs + t;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                float4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    v[i] = tok ? __ldg(reinterpret_cast<const float4*>(xr + (int64_t)(4 * h + i) * NTs))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                tst16(tq + (uint32_t)(R * c0 + 16 * h), v);
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // ---- the next unit's chunk: L2 prefetch behind this unit's compute (quarters 0,1: the TMEM
+        //      rows, quarters 2,3: the shared-memory rows) ----
+        if (u + (int)gridDim.x < units) {  // 16 rows x 512 bytes per warp: two 128-byte lines per lane
+            const int un = u + gridDim.x, sn = un / chunks, chn = un - sn * chunks;
+            const int cl = 128 * (q >> 1) + FILL_C * wq + (lane >> 1), tn = chn * TW + QT * b + 64 * (lane & 1);
+            if (cl < ncols) {
+                const float* src = X + ((int64_t)sn * ncols + cl) * NTs + tn;
+                if (tn < NTr) asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+                if (tn + 32 < NTr) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 32));
+            }
+        }
+        // ---- rows g, g + 16, ...: stage-0 segment from TMEM, stage-1 segment from shared memory ----
+        const int* rbp = (STAGED ? sbnd : bs) + g * 3;
+        const int2* cvb = STAGED ? scv - e_lo : cv;  // indexed by global entry numbers
+        float* yp = Y + ((int64_t)s * nrows + g) * NTs + t;
+        for (int r = g; r < nrows; r += NSETS, rbp += 3 * NSETS, yp += NSETS * (int64_t)NTs) {
+            const int e0 = rbp[0], e1 = rbp[1], e2 = rbp[2];
+            unsigned long long acc[2] = {0ull, 0ull};
+            walk<4, STAGED>(cvb, e0, e1, tq, acc, z);
+            walk_sm<STAGED>(cvb, e1, e2, xl, acc, z);
+            if (tok) stg_acc<4>(yp, acc);
+        }
+        // every warp is done reading this chunk (and the staged slice) before the next unit
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "r"(TMEM_COLS));
+}
+
 }  // namespace tm
 }  // namespace wino

@@ -214,9 +214,11 @@ class WinogradLayer:
 
     def set_spmm_operands(self, where: str):
         """CSR kernels' dense operand chunk: 'auto' (default; tensor memory where it is measured
-        faster: 128 < rows <= 512, density >= 4%, enough work units), 'smem' (shared memory always)
-        or 'tmem' (tensor memory whenever 128 < rows <= 512).  Bitwise the same results."""
-        check(lib().wino_set_option(self._h, _lib.WINO_OPT_SPMM_OPERANDS, {"auto": 0, "smem": 1, "tmem": 2}[where]))
+        faster: 128 < rows <= 512, density >= 4%, enough work units — the hybrid split when its
+        stream fits in shared memory), 'smem' (shared memory always), 'tmem' (tensor memory whenever
+        128 < rows <= 512) or 'hybrid' (rows [0,128) in tensor memory, the rest in shared memory,
+        whenever 128 < rows <= 256).  Bitwise the same results."""
+        check(lib().wino_set_option(self._h, _lib.WINO_OPT_SPMM_OPERANDS, {"auto": 0, "smem": 1, "tmem": 2, "hybrid": 3}[where]))
 
     def set_auto_density(self, density: float):
         """Density from which contraction 'auto' uses the tensor cores (default 0.08)."""

@@ -803,6 +803,14 @@ def test_tmem_spmm_bitwise_equals_shared_memory(c, k, h, n, sparsity):
         assert np.array_equal(oa, ob), "O differs between TMEM and shared-memory operands"
         assert np.array_equal(dia, dib), "dI differs between TMEM and shared-memory operands"
         assert np.array_equal(dwa, dwb), "dW_F differs"
+    if 128 < c <= 256 and 128 < k <= 256:
+        # hybrid operands (rows [0,128) in TMEM, the rest in shared memory; wino_spmm_tm.cuh):
+        # forced here on both directions, staged (0.9 / 0.97) and unstaged (0.7) streams, ragged rows
+        h_ = _step_with_operands(img, w_f, go, "hybrid", lr=1e-3)
+        for (oa, dwa, dia), (ob, dwb, dib) in zip(h_, b):
+            assert np.array_equal(oa, ob), "O differs between hybrid and shared-memory operands"
+            assert np.array_equal(dia, dib), "dI differs between hybrid and shared-memory operands"
+            assert np.array_equal(dwa, dwb), "dW_F differs"
     if c == 160:  # anchor the TMEM path itself to the reference's f32 operation order
         mir = wo.layer_f32(img, wo.compress(w_f), go, m=4, pad=1)
         assert np.array_equal(a[0][0], mir["o"])

@@ -1,4 +1,4 @@
-"""Diagnostics of the pipelined host step at c1: times (CUDA events) of copy-only, compute-only and
+"""Diagnostics of the pipelined host step (default c1; `python tools/e2e_diag.py c3:0.9`): times (CUDA events) of copy-only, compute-only and
 full variants, each captured as a CUDA graph."""
 import sys
 from pathlib import Path
@@ -10,9 +10,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1702_08597_b200 as wb  # noqa: E402
 from paper_1702_08597_b200.graph import GraphedStep  # noqa: E402
 from paper_1702_08597_b200.pipeline import PipelinedHostStep  # noqa: E402
-from paper_1702_08597_b200.synth import CONFIGS, make_inputs  # noqa: E402
+from paper_1702_08597_b200.synth import CONFIGS, make_inputs, with_sparsity  # noqa: E402
 
-cfg = CONFIGS["c1"]
+_nm, _, _sp = (sys.argv[1] if len(sys.argv) > 1 else "c1").partition(":")
+cfg = CONFIGS[_nm]
+if _sp:
+    cfg = with_sparsity(cfg, float(_sp))
 img, w_f, go = make_inputs(cfg)
 n = cfg.n
 layer = wb.WinogradLayer(cfg.c, cfg.k, cfg.h, cfg.w, pad=1, m=4)
@@ -43,7 +46,7 @@ def timeit(fn, k=20):
     return ts[k // 2]
 
 
-for chunks in (1, 2, 4, 8):
+for chunks in (1, 2, 4, 8) if cfg.n < 64 else (1, 4, 8, [16, 16, 16, 8, 4, 4], [12, 12, 12, 12, 8, 4, 4], [8] * 7 + [4, 4]):
     ps = PipelinedHostStep(layer, cache, x, g, o, dw, di, chunks=chunks)
     full = GraphedStep(lambda: ps(h[0], h[1], *outs)).replay
     print(f"chunks {chunks}: full {timeit(full):.0f} us")
@@ -90,6 +93,26 @@ def compute():
 
 print(f"compute only: {timeit(GraphedStep(compute).replay):.0f} us")
 ps = PipelinedHostStep(layer, cache, x, g, o, dw, di, chunks=4)
+
+
+def in_then_out():
+    m = torch.cuda.current_stream()
+    s_in.wait_stream(m)
+    s_out.wait_stream(m)
+    e = torch.cuda.Event()
+    with torch.cuda.stream(s_in):
+        x.copy_(h[0], non_blocking=True)
+        e.record()
+        g.copy_(h[1], non_blocking=True)
+    with torch.cuda.stream(s_out):
+        s_out.wait_event(e)
+        outs[0].copy_(o, non_blocking=True)
+        outs[2].copy_(di, non_blocking=True)
+    m.wait_stream(s_in)
+    m.wait_stream(s_out)
+
+
+print(f"copies, D2H starting after the first H2D tensor: {timeit(GraphedStep(in_then_out).replay):.0f} us")
 
 
 def ranges_only():

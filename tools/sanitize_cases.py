@@ -17,6 +17,8 @@ CASES = [  # (name, C, K, H, n, sparsity, mode, operands)
     ("csr-tmem-s2", 256, 256, 12, 2, 0.9, "csr", "tmem"),
     ("csr-tmem-s4-unstaged", 384, 512, 9, 2, 0.5, "csr", "tmem"),
     ("ragged-tmem", 161, 203, 11, 3, 0.7, "csr", "tmem"),
+    ("csr-hybrid", 256, 256, 12, 2, 0.9, "csr", "hybrid"),
+    ("ragged-hybrid-unstaged", 161, 203, 11, 3, 0.3, "csr", "hybrid"),
     ("fb", 256, 256, 12, 2, 0.9, "fb", "auto"),
     ("dense", 128, 128, 12, 2, 0.0, "dense", "auto"),
     ("tc", 256, 256, 12, 2, 0.9, "tc", "auto"),

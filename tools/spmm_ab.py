@@ -58,9 +58,10 @@ def main():
             cfg = with_sparsity(cfg, float(sp))
         a, ta = run(cfg, "tmem")
         b, tb = run(cfg, "smem")
-        same = all(np.array_equal(x, y) for x, y in zip(a, b))
+        c, tc = run(cfg, "hybrid")
+        same = all(np.array_equal(x, y) for x, y in zip(a, b)) and all(np.array_equal(x, y) for x, y in zip(c, b))
         ok &= same
-        print(f"{nm:8s} bitwise={'yes' if same else 'NO'}  tmem {ta}  smem {tb}", flush=True)
+        print(f"{nm:8s} bitwise={'yes' if same else 'NO'}  tmem {ta}  smem {tb}  hybrid {tc}", flush=True)
     sys.exit(0 if ok or os.environ.get("SPMM_AB_NOFAIL") else 1)
 
 
