@@ -604,10 +604,26 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
         int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c,
                                                                 (256 + T - 1) / T}));
         const size_t smem = (size_t)cg * per_c;
-        set_smem_attr(wino::input_grad_kernel<M, P, CF>, (int)std::max<size_t>(smem, 48 * 1024));
-        wino::input_grad_kernel<M, P, CF><<<dim3((p->C + cg - 1) / cg, n), 256, smem, st>>>(
-            DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg,
-            0x8000000080000000ull);
+        const dim3 grid((p->C + cg - 1) / cg, n);
+        // whole warps over the block's (channel, tile) items (c3: 196 tiles -> 224 threads)
+        const int threads = (int)std::min<int64_t>(256, round_up((int64_t)cg * T, 32));
+        bool aligned = false;
+        if constexpr (M == 4 && P == 6)
+            aligned = p->pad == 1 && p->H == 4 * (int)g.tiles_y && p->W == 4 * (int)g.tiles_x &&
+                      (reinterpret_cast<uintptr_t>(dI) & 15) == 0;
+        if (aligned) {
+            if constexpr (M == 4 && P == 6) {
+                set_smem_attr(wino::input_grad_kernel<M, P, CF, true>, (int)std::max<size_t>(smem, 48 * 1024));
+                wino::input_grad_kernel<M, P, CF, true><<<grid, threads, smem, st>>>(
+                    DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg,
+                    0x8000000080000000ull);
+            }
+        } else {
+            set_smem_attr(wino::input_grad_kernel<M, P, CF>, (int)std::max<size_t>(smem, 48 * 1024));
+            wino::input_grad_kernel<M, P, CF><<<grid, threads, smem, st>>>(
+                DV, dI, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_y, (int)g.tiles_x, T, (int)NTs, cg,
+                0x8000000080000000ull);
+        }
     } else {
         const int64_t total = (int64_t)n * p->C * p->H * p->W;
         wino::input_grad_direct_kernel<M, P, CF><<<grid_for(total, 256, p->sm_count), 256, 0, st>>>(

@@ -248,7 +248,7 @@ __device__ __forceinline__ float tile_grad_entry(const float* __restrict__ dv, i
     return acc;
 }
 
-template <int M, int P, class CF>
+template <int M, int P, class CF, bool ALIGNED = false>
 __global__ void __launch_bounds__(256)
 input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Coefs cf, int C,
                   int H, int W, int pad, int tiles_y, int tiles_x, int T, int NTs, int CG,
@@ -296,6 +296,49 @@ input_grad_kernel(const float* __restrict__ DV, float* __restrict__ dI, const Co
     // (ty,tx) — ascending t, the reference's order — at compile-time offsets (+M when the
     // pixel lies in a neighbour's overlap band, i.e. local index < P-M).
     constexpr int O = P - M;
+    if constexpr (ALIGNED) {
+        // F(4x4,3x3), pad 1, H = 4·tiles_y, W = 4·tiles_x: the thread of tile (ty,tx) owns the
+        // 16-byte-aligned pixels y = 4ty + a, x = 4tx + b (a, b < 4).  Padded row Y = 4ty + a + 1
+        // lies in tile row ty (local a+1), in ty-1 (local 5) when a = 0 and in ty+1 (local 0) when
+        // a = 3; columns likewise: ≤ 4 contributions per pixel, all at compile-time offsets, added
+        // in ascending t from +0 (the reference's order); one float4 store per pixel row.
+        static_assert(!ALIGNED || (M == 4 && P == 6), "aligned K7 is F(4x4,3x3) only");
+        for (int idx = threadIdx.x; idx < CG * T; idx += blockDim.x) {
+            const int cl = idx / T, t = idx - cl * T;
+            const int c = c0 + cl;
+            if (c >= C) continue;
+            const int ty = t / tiles_x, tx = t - ty * tiles_x;
+            const float* g0 = gsm + (int64_t)idx * TS;
+            const float* gu = g0 - tiles_x * TS;  // (ty-1, tx)
+            const float* gd = g0 + tiles_x * TS;  // (ty+1, tx)
+            const bool up = ty > 0, dn = ty < tiles_y - 1, lf = tx > 0, rt = tx < tiles_x - 1;
+            float* dst = dI + (((int64_t)n * C + c) * H + 4 * ty) * W + 4 * tx;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                float r[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    float acc = 0.f;
+                    if (a == 0 && up) {
+                        if (b == 0 && lf) acc = __fadd_rn(acc, gu[-TS + 5 * P + 5]);
+                        acc = __fadd_rn(acc, gu[5 * P + b + 1]);
+                        if (b == 3 && rt) acc = __fadd_rn(acc, gu[TS + 5 * P]);
+                    }
+                    if (b == 0 && lf) acc = __fadd_rn(acc, g0[-TS + (a + 1) * P + 5]);
+                    acc = __fadd_rn(acc, g0[(a + 1) * P + b + 1]);
+                    if (b == 3 && rt) acc = __fadd_rn(acc, g0[TS + (a + 1) * P]);
+                    if (a == 3 && dn) {
+                        if (b == 0 && lf) acc = __fadd_rn(acc, gd[-TS + 5]);
+                        acc = __fadd_rn(acc, gd[b + 1]);
+                        if (b == 3 && rt) acc = __fadd_rn(acc, gd[TS]);
+                    }
+                    r[b] = acc;
+                }
+                *reinterpret_cast<float4*>(dst + a * W) = make_float4(r[0], r[1], r[2], r[3]);
+            }
+        }
+        return;
+    }
     for (int idx = threadIdx.x; idx < CG * T; idx += blockDim.x) {
         const int cl = idx / T, t = idx - cl * T;
         const int c = c0 + cl;
