@@ -333,7 +333,7 @@ class LayerBench:
         if self.dense:
             return "dense plan: tcgen05 3xTF32 Z/dĨ_F"
         return {"csr": "csr (reference order)", "tc": "tcgen05 3xTF32 on zero-filled W_F",
-                "auto": "auto (tcgen05 at density >= 8%, else csr)"}[self.contraction]
+                "auto": "auto (tcgen05 at density >= 11% for 128 < C,K <= 256, >= 8% otherwise; else csr)"}[self.contraction]
 
     def compute(self):  # one call, scheduled by data dependence (wino_forward_backward)
         if self.fwd_only:

@@ -226,7 +226,8 @@ WINO_API int wino_recompress(wino_plan* plan, double zero_tol);
  *       coordinates stay exactly zero (the operands are re-scattered from the CSR values on
  *       every update).  Requires C, K multiples of 4.
  *     2 auto — tensor cores when the plan's density reaches WINO_OPT_AUTO_DENSITY per mille
- *       (default 80), else the CSR kernels; re-decided whenever the weights change. */
+ *       (default: the measured crossover — 110 for 128 < C, K <= 256, where the hybrid CSR kernel
+ *       runs, 80 otherwise), else the CSR kernels; re-decided whenever the weights change. */
 #define WINO_OPT_CONTRACTION 2
 #define WINO_OPT_AUTO_DENSITY 3
 /*   WINO_OPT_SPMM_OPERANDS: where the CSR kernels keep their dense operand chunk (Ĩ_F / dZ):

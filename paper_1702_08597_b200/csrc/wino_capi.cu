@@ -207,7 +207,9 @@ struct wino_plan {
     bool tc_ready = false;
     int contraction = 0;       // sparse plan, in effect: 0 = CSR kernels (reference order), 1 = tcgen05 on zero-filled W_F
     int contraction_mode = 0;  // as requested: 0 csr, 1 tc, 2 auto (tc when dense enough)
-    int auto_permille = 80;    // auto: tensor cores at density >= this / 1000 (measured crossover 5-10%)
+    int auto_permille = -1;    // auto: tensor cores at density >= this / 1000; -1: the measured default
+                               // (110 where the hybrid CSR kernel applies, 128 < C, K <= 256: c3 crossover
+                               // 10.7%; 80 elsewhere: c1 9%, c2 6%)
     int64_t* d_slice_off = nullptr;
     // TMEM SpMM (wino_spmm_tm.cuh): the padded stage-segment streams of the CSR [0] and CSC [1],
     // rebuilt whenever the structure changes, values refreshed by wino_values_updated
@@ -1000,7 +1002,9 @@ int apply_contraction(wino_plan* p) {
     int eff = p->contraction_mode;
     if (eff == 2) {
         const double density = (double)p->nnz / ((double)p->P2 * p->K * p->C);
-        eff = (density * 1000.0 >= p->auto_permille && p->C % 4 == 0 && p->K % 4 == 0) ? 1 : 0;
+        const bool hyb_shape = p->C > 128 && p->C <= 256 && p->K > 128 && p->K <= 256;
+        const int thr = p->auto_permille >= 0 ? p->auto_permille : (hyb_shape ? 110 : 80);
+        eff = (density * 1000.0 >= thr && p->C % 4 == 0 && p->K % 4 == 0) ? 1 : 0;
     }
     p->contraction = eff;
     if (eff == 1) {

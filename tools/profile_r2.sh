@@ -12,7 +12,7 @@ $C2 > gpurun_out/prof_plain_c2.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv $C3 > gpurun_out/ncu_l.log 2>&1
 # warm-up + launch-count steps precede the timed ones: skip them, then one launch of each kernel
 ncu --set full --clock-control none --import-source on \
-    -k regex:"digits|amax|spmm_tmem|output_transform|input_grad|gemm_kernel|reduce_sparse" -s 40 -c 10 \
+    -k regex:"digits|amax|spmm_hyb|spmm_tmem|output_transform|input_grad|gemm_kernel|reduce_sparse" -s 40 -c 10 \
     -o gpurun_out/full_c3 $C3 > gpurun_out/ncu_f3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"gemm_3xtf32" -s 8 -c 2 \
     -o gpurun_out/full_c3d $C3D > gpurun_out/ncu_f3d.log 2>&1

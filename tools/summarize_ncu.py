@@ -24,7 +24,7 @@ PROF = ROOT / "profiles"
 KIND = [("input_transform_digits", "input_transform"), ("input_transform", "input_transform"),
         ("grad_z_digits", "grad_z"), ("output_transform", "output_transform"), ("input_grad", "input_grad"),
         ("plane_amax", "amax"), ("xdw::gemm_kernel", "dw_gemm_i8"), ("reduce_sparse", "dw_reduce"),
-        ("reduce_dense", "dw_reduce"), ("spmm_tmem", "spmm"), ("spmm_kernel", "spmm"),
+        ("reduce_dense", "dw_reduce"), ("spmm_hyb", "spmm"), ("spmm_tmem", "spmm"), ("spmm_kernel", "spmm"),
         ("gemm_3xtf32", "dense_tc"), ("tm_", "stream_build"), ("stage_bounds", "stream_build")]
 
 METRICS = OrderedDict([
