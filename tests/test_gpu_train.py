@@ -345,3 +345,47 @@ def test_in_backward_exchange_over_a_torch_nccl_group():
         assert torch.isfinite(st.bucket.flat).all()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("h,world", [(24, 3), (22, 4)])
+def test_tile_split_bands_match_the_whole_layer(h, world):
+    """Tile-axis split (dist.py: bands of tile rows, one per rank; here the ranks' bands run one
+    after another on the one GPU): every band through the unchanged kernels on its window of the
+    zero-padded image (pad=0 plan).  O is bitwise the whole-image layer's rows; the summed dW_F
+    (what the all-reduce forms) and the halo-merged dI meet the tolerance against the f64 oracle
+    and the whole-image layer."""
+    from paper_1702_08597_b200.dist import band_input, band_rows, merge_bands, tile_bands
+    from helpers import assert_parity
+
+    rng = np.random.default_rng(h * 10 + world)
+    c, k, n, w = 24, 40, 2, 20
+    img = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    go = rng.standard_normal((n, k, h, w)).astype(np.float32)
+    w_f = rng.standard_normal((k, c, 6, 6)) * np.sqrt(2.0 / (9 * c)) * (rng.random((k, c, 6, 6)) >= 0.7)
+    whole = wb.WinogradLayer(c, k, h, w, pad=1, m=4)
+    whole.set_weights(w_f, dense=False)
+    cache = whole.new_cache(n)
+    o_ref = whole.forward(dev(img), cache).cpu().numpy()
+    dw_ref, di_ref = whole.backward(dev(go), cache)
+    dw_ref, di_ref = dw_ref.cpu().numpy().astype(np.float64), di_ref.cpu().numpy()
+    bands = tile_bands(h, world)
+    x = dev(img)
+    o_parts, di_parts, dw_sum = [], [], np.zeros_like(dw_ref)
+    for a, b in bands:
+        _, rows, o0, on = band_rows(h, a, b)
+        if rows == 0:
+            di_parts.append(None)
+            continue
+        lay = wb.WinogradLayer(c, k, rows, w + 2, pad=0, m=4)
+        lay.set_weights(w_f, dense=False)
+        cb = lay.new_cache(n)
+        o_parts.append(lay.forward(band_input(x, a, b), cb).cpu().numpy())
+        dw, di = lay.backward(dev(go[:, :, o0:o0 + on, :]), cb)
+        dw_sum += dw.cpu().numpy().astype(np.float64)
+        di_parts.append(di.clone())
+        lay.close()
+    assert np.array_equal(np.concatenate(o_parts, axis=2), o_ref), "band O differs from the whole-image O"
+    assert_parity(dw_sum, dw_ref, "tile-split dW_F vs whole layer")
+    di = merge_bands(di_parts, bands, h).cpu().numpy()
+    assert_parity(di, di_ref, "tile-split dI vs whole layer")
+    whole.close()
