@@ -810,6 +810,10 @@ int launch_input_fused(wino_plan* p, cudaStream_t st, const float* in, float* V,
     constexpr int smem = x::digit_smem_bytes<P * P>();
     auto kern = x::input_transform_digits_kernel<M, P, CF>;
     set_smem_attr(kern, smem);
+    static int per_sm = 0;  // resident blocks per SM: the L2 prefetch distance of the gather
+    if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, x::kTileItems, smem) != cudaSuccess)
+        per_sm = 2;
+    const int pf = per_sm * p->sm_count;
     const int64_t plane = (int64_t)p->P2 * p->C * c->NTd;
     for (int g = g0; g < g1; ++g) {
         const DwSeg& sg = c->segs[g];
@@ -821,7 +825,7 @@ int launch_input_fused(wino_plan* p, cudaStream_t st, const float* in, float* V,
             in + (int64_t)(sg.n0 - n_base) * p->C * p->H * p->W, V + voff, c->dig_v,
             c->e_v + (int64_t)g * p->P2 * p->C, c->amax_v + (int64_t)g * p->C, p->cf, p->cfd, p->nrm_v, p->C, p->H,
             p->W, p->pad, (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
-            (int)sg.col0);
+            (int)sg.col0, pf);
         int rc = L.done();
         if (rc) return rc;
     }
@@ -847,11 +851,14 @@ int launch_grad_fused(wino_plan* p, cudaStream_t st, const float* dO, const floa
         Launch L(p, st, K_GRADZ);
         auto go = [&](auto kern) {
             set_smem_attr(kern, smem);
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, x::kTileItems, smem) != cudaSuccess)
+                per_sm = 3;
             kern<<<grid, x::kTileItems, smem, st>>>(
                 dO + off, relu ? relu + off : nullptr, DZ + voff, c->dig_z, c->e_z + (int64_t)g * p->P2 * p->K,
                 c->amax_z + (int64_t)g * p->K, p->cf, p->cfd, p->nrm_z, p->K, (int)p->g.h_o, (int)p->g.w_o,
                 (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
-                (int)sg.col0);
+                (int)sg.col0, per_sm * p->sm_count);
         };
         if (mask) go(x::grad_z_digits_kernel<M, P, true, CF>);
         else go(x::grad_z_digits_kernel<M, P, false, CF>);

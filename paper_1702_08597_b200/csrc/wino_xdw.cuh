@@ -208,7 +208,7 @@ input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ 
                               int* __restrict__ Eout, const unsigned* __restrict__ amax, const Coefs cf,
                               const CoefsD cfd, const Norms nrm, int C, int H, int W, int pad, int tiles_x, int T,
                               int ncols, int vcols, int ncols_pad, int64_t NTs, int64_t NTd, int64_t plane,
-                              int col0) {
+                              int col0, int pf) {
     constexpr int P2 = P * P;
     extern __shared__ __align__(16) uint32_t xdw_smem[];
     uint32_t* slo = xdw_smem;
@@ -261,6 +261,23 @@ input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ 
         for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int k = 0; k < P; ++k) d[i][k] = 0.f;
+    }
+    // The gather is this kernel's exposed latency (2 blocks per SM): pull the patch rows of the
+    // block that will run `pf` blocks later (launch order, x fastest; pf = resident blocks) into
+    // L2 now, behind this block's own loads.
+    if (pf > 0) {
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf;
+        const int pc = (int)(lin / gridDim.x);
+        const int pj = (int)(lin - (long long)pc * gridDim.x) * kTileItems + threadIdx.x;
+        if (pc < (int)gridDim.y && pj < ncols) {
+            const int n = pj / T, t = pj - n * T;
+            const int ty = t / tiles_x, tx = t - ty * tiles_x;
+            const int y0 = ty * M - pad, x0 = max(tx * M - pad, 0);
+            const float* src = in + ((int64_t)n * C + pc) * H * W + x0;
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+                if ((unsigned)(y0 + i) < (unsigned)H) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (y0 + i) * W));
+        }
     }
     __syncthreads();  // scales
     const bool vok = j < vcols;
@@ -317,7 +334,8 @@ __global__ void __launch_bounds__(kTileItems, (P <= 6) ? 2 : 1)
 grad_z_digits_kernel(const float* __restrict__ dO, const float* __restrict__ relu_out, float* __restrict__ DZ,
                      int8_t* __restrict__ dig, int* __restrict__ Eout, const unsigned* __restrict__ amax,
                      const Coefs cf, const CoefsD cfd, const Norms nrm, int K, int Ho, int Wo, int tiles_x, int T,
-                     int ncols, int vcols, int ncols_pad, int64_t NTs, int64_t NTd, int64_t plane, int col0) {
+                     int ncols, int vcols, int ncols_pad, int64_t NTs, int64_t NTd, int64_t plane, int col0,
+                     int pf) {
     constexpr int P2 = P * P;
     extern __shared__ __align__(16) uint32_t xdw_smem[];
     uint32_t* slo = xdw_smem;
@@ -336,19 +354,56 @@ grad_z_digits_kernel(const float* __restrict__ dO, const float* __restrict__ rel
         const int n = j / T, t = j - n * T;
         const int ty = t / tiles_x, tx = t - ty * tiles_x;
         const int64_t base = ((int64_t)n * K + k) * Ho * Wo;
+        const bool al16 = ((reinterpret_cast<uintptr_t>(dO) | (MASK ? reinterpret_cast<uintptr_t>(relu_out) : 0)) & 15) == 0;
+        if (M == 4 && (Wo & 3) == 0 && al16 && ty * M + M <= Ho) {
+            // whole tile inside the image, 16-byte-aligned rows: one load per tile row
 #pragma unroll
-        for (int y = 0; y < M; ++y) {
-            const int oy = ty * M + y;
+            for (int y = 0; y < M; ++y) {
+                const int64_t o = base + (ty * M + y) * Wo + tx * M;
+                float4 v = __ldg(reinterpret_cast<const float4*>(dO + o));
+                if (MASK) {
+                    const float4 r = __ldg(reinterpret_cast<const float4*>(relu_out + o));
+                    v.x = __fmul_rn(v.x, r.x > 0.f ? 1.f : 0.f);
+                    v.y = __fmul_rn(v.y, r.y > 0.f ? 1.f : 0.f);
+                    v.z = __fmul_rn(v.z, r.z > 0.f ? 1.f : 0.f);
+                    v.w = __fmul_rn(v.w, r.w > 0.f ? 1.f : 0.f);
+                }
+                d[y][0] = v.x;
+                d[y][1] = v.y;
+                d[y][2] = v.z;
+                d[y][3] = v.w;
+            }
+        } else {
 #pragma unroll
-            for (int x = 0; x < M; ++x) {
-                const int ox = tx * M + x;
-                if (oy < Ho && ox < Wo) {
-                    const int64_t o = base + oy * Wo + ox;
-                    float v = __ldg(dO + o);
-                    if (MASK) v = __fmul_rn(v, __ldg(relu_out + o) > 0.f ? 1.f : 0.f);
-                    d[y][x] = v;
+            for (int y = 0; y < M; ++y) {
+                const int oy = ty * M + y;
+#pragma unroll
+                for (int x = 0; x < M; ++x) {
+                    const int ox = tx * M + x;
+                    if (oy < Ho && ox < Wo) {
+                        const int64_t o = base + oy * Wo + ox;
+                        float v = __ldg(dO + o);
+                        if (MASK) v = __fmul_rn(v, __ldg(relu_out + o) > 0.f ? 1.f : 0.f);
+                        d[y][x] = v;
+                    }
                 }
             }
+        }
+    }
+    if (pf > 0) {  // the dO rows of the block `pf` blocks ahead -> L2 (as in K1)
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf;
+        const int pk = (int)(lin / gridDim.x);
+        const int pj = (int)(lin - (long long)pk * gridDim.x) * kTileItems + threadIdx.x;
+        if (pk < (int)gridDim.y && pj < ncols) {
+            const int n = pj / T, t = pj - n * T;
+            const int ty = t / tiles_x, tx = t - ty * tiles_x;
+            const int64_t o = ((int64_t)n * K + pk) * Ho * Wo + (int64_t)(ty * M) * Wo + min(tx * M, Wo - 1);
+#pragma unroll
+            for (int y = 0; y < M; ++y)
+                if (ty * M + y < Ho) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(dO + o + y * Wo));
+                    if (MASK) asm volatile("prefetch.global.L2 [%0];" ::"l"(relu_out + o + y * Wo));
+                }
         }
     }
     __syncthreads();  // scales
