@@ -585,7 +585,7 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, f
         return L.done();
     }
     Launch L(p, st, K_OUTPUT);
-    const int grid = grid_for((int64_t)p->K * NT, 256, p->sm_count);
+    const dim3 grid((unsigned)((NT + 255) / 256), (unsigned)p->K);
     if (flags & WINO_FWD_RELU)
         wino::output_transform_kernel<M, P, true, CF><<<grid, 256, 0, st>>>(
             Z, out, p->cf, p->K, (int)g.h_o, (int)g.w_o, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs);

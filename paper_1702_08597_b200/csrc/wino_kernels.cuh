@@ -182,43 +182,55 @@ template <int M, int P, bool RELU, class CF>
 __global__ void __launch_bounds__(256)
 output_transform_kernel(const float* __restrict__ Z, float* __restrict__ O, const Coefs cf, int K,
                         int Ho, int Wo, int tiles_x, int T, int NT, int NTs) {
-    const int64_t total = (int64_t)K * NT;
+    // grid (column blocks, K): k = blockIdx.y, nt = blockIdx.x·256 + thread — 32-bit index math,
+    // the 36 slice loads by pointer steps, the output rows by row pointers
+    const int k = blockIdx.y;
+    const int nt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (nt >= NT) return;
     const int64_t plane = (int64_t)K * NTs;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-         gid += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(gid / NT);
-        const int nt = (int)(gid - (int64_t)k * NT);
-        const float* zp = Z + (int64_t)k * NTs + nt;
-        float z[P][P];
+    const float* zp = Z + (int64_t)k * NTs + nt;
+    float z[P][P];
 #pragma unroll
-        for (int i = 0; i < P; ++i)
+    for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int j = 0; j < P; ++j) z[i][j] = __ldg(zp + (int64_t)(i * P + j) * plane);
-        float tmp[M][P];
+        for (int j = 0; j < P; ++j, zp += plane) z[i][j] = __ldg(zp);
+    float tmp[M][P];
 #pragma unroll
-        for (int y = 0; y < M; ++y)
+    for (int y = 0; y < M; ++y)
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                float acc = 0.f;
+        for (int j = 0; j < P; ++j) {
+            float acc = 0.f;
 #pragma unroll
-                for (int i = 0; i < P; ++i) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), z[i][j]);
-                tmp[y][j] = acc;
+            for (int i = 0; i < P; ++i) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, i * M + y), z[i][j]);
+            tmp[y][j] = acc;
+        }
+    const int n = nt / T, t = nt - n * T;
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const int oy0 = ty * M, ox0 = tx * M;
+    float* orow = O + (((int64_t)n * K + k) * Ho + oy0) * Wo + ox0;
+    // whole tile inside the image and 16-byte-aligned rows: one vector store per output row
+    const bool vec = M == 4 && (Wo & 3) == 0 && oy0 + M <= Ho && (reinterpret_cast<uintptr_t>(O) & 15) == 0;
+#pragma unroll
+    for (int y = 0; y < M; ++y, orow += Wo) {
+        float r[M];
+#pragma unroll
+        for (int x = 0; x < M; ++x) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < P; ++j) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), tmp[y][j]);
+            if (RELU) acc = acc > 0.f ? acc : 0.f;  // train.cpp:76-83
+            r[x] = acc;
+        }
+        if constexpr (M == 4) {
+            if (vec) {
+                *reinterpret_cast<float4*>(orow) = make_float4(r[0], r[1], r[2], r[3]);
+                continue;
             }
-        const int n = nt / T, t = nt - n * T;
-        const int ty = t / tiles_x, tx = t - ty * tiles_x;
-        float* op = O + ((int64_t)n * K + k) * Ho * Wo;
+        }
+        if (oy0 + y < Ho) {
 #pragma unroll
-        for (int y = 0; y < M; ++y) {
-            const int oy = ty * M + y;
-#pragma unroll
-            for (int x = 0; x < M; ++x) {
-                float acc = 0.f;
-#pragma unroll
-                for (int j = 0; j < P; ++j) acc = cmadd<CF>(acc, coef_a<CF, M, P>(cf, j * M + x), tmp[y][j]);
-                if (RELU) acc = acc > 0.f ? acc : 0.f;  // train.cpp:76-83
-                const int ox = tx * M + x;
-                if (oy < Ho && ox < Wo) op[oy * Wo + ox] = acc;
-            }
+            for (int x = 0; x < M; ++x)
+                if (ox0 + x < Wo) orow[x] = r[x];
         }
     }
 }
