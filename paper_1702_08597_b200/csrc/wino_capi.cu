@@ -799,6 +799,13 @@ int launch_amax(wino_plan* p, cudaStream_t st, const float* x, const float* relu
     return L.done();
 }
 
+// gather prefetch distance of the fused K1 / K4 (blocks ahead in launch order, x fastest) as
+// (rows ahead) << 16 | (column blocks ahead); 0 = off (distances that do not fit the fields)
+static int pack_prefetch(int blocks, unsigned gx) {
+    if (blocks <= 0 || gx == 0 || gx > 0xffffu || blocks / gx > 0x7fffu) return 0;
+    return (int)((blocks / gx) << 16 | (blocks % gx));
+}
+
 // K1 fused with the Ĩ_F digits, segments [g0, g1) of the cache: `in` holds images from n_base on,
 // V points at image n_base's first column (row stride NTs), `owned` = V columns this call writes
 // (from image n_base on; beyond the last image: the batch's zero padding).
@@ -813,7 +820,7 @@ int launch_input_fused(wino_plan* p, cudaStream_t st, const float* in, float* V,
     static int per_sm = 0;  // resident blocks per SM: the L2 prefetch distance of the gather
     if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, x::kTileItems, smem) != cudaSuccess)
         per_sm = 2;
-    const int pf = per_sm * p->sm_count;
+    const int pf_blocks = per_sm * p->sm_count;
     const int64_t plane = (int64_t)p->P2 * p->C * c->NTd;
     for (int g = g0; g < g1; ++g) {
         const DwSeg& sg = c->segs[g];
@@ -821,7 +828,9 @@ int launch_input_fused(wino_plan* p, cudaStream_t st, const float* in, float* V,
         const int64_t vcols = g == g1 - 1 ? owned - voff : ncols;
         const int64_t cols = std::max(vcols, sg.ncols_pad);
         Launch L(p, st, K_INPUT);
-        kern<<<dim3((unsigned)((cols + x::kTileItems - 1) / x::kTileItems), (unsigned)p->C), x::kTileItems, smem, st>>>(
+        const unsigned gx = (unsigned)((cols + x::kTileItems - 1) / x::kTileItems);
+        const int pf = pack_prefetch(pf_blocks, gx);
+        kern<<<dim3(gx, (unsigned)p->C), x::kTileItems, smem, st>>>(
             in + (int64_t)(sg.n0 - n_base) * p->C * p->H * p->W, V + voff, c->dig_v,
             c->e_v + (int64_t)g * p->P2 * p->C, c->amax_v + (int64_t)g * p->C, p->cf, p->cfd, p->nrm_v, p->C, p->H,
             p->W, p->pad, (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
@@ -858,7 +867,7 @@ int launch_grad_fused(wino_plan* p, cudaStream_t st, const float* dO, const floa
                 dO + off, relu ? relu + off : nullptr, DZ + voff, c->dig_z, c->e_z + (int64_t)g * p->P2 * p->K,
                 c->amax_z + (int64_t)g * p->K, p->cf, p->cfd, p->nrm_z, p->K, (int)p->g.h_o, (int)p->g.w_o,
                 (int)p->g.tiles_x, (int)T, (int)ncols, (int)vcols, (int)sg.ncols_pad, NTs, c->NTd, plane,
-                (int)sg.col0, per_sm * p->sm_count);
+                (int)sg.col0, pack_prefetch(per_sm * p->sm_count, grid.x));
         };
         if (mask) go(x::grad_z_digits_kernel<M, P, true, CF>);
         else go(x::grad_z_digits_kernel<M, P, false, CF>);

@@ -263,12 +263,12 @@ input_transform_digits_kernel(const float* __restrict__ in, float* __restrict__ 
             for (int k = 0; k < P; ++k) d[i][k] = 0.f;
     }
     // The gather is this kernel's exposed latency (2 blocks per SM): pull the patch rows of the
-    // block that will run `pf` blocks later (launch order, x fastest; pf = resident blocks) into
-    // L2 now, behind this block's own loads.
-    if (pf > 0) {
-        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf;
-        const int pc = (int)(lin / gridDim.x);
-        const int pj = (int)(lin - (long long)pc * gridDim.x) * kTileItems + threadIdx.x;
+    // block that will run one resident wave of blocks later (launch order, x fastest) into L2 now,
+    // behind this block's own loads.
+    if (pf > 0) {  // pf = (blocks ahead / gridDim.x) << 16 | (blocks ahead % gridDim.x): no division here
+        int pbx = (int)blockIdx.x + (pf & 0xffff), pc = (int)blockIdx.y + (pf >> 16);
+        if (pbx >= (int)gridDim.x) pbx -= gridDim.x, ++pc;
+        const int pj = pbx * kTileItems + threadIdx.x;
         if (pc < (int)gridDim.y && pj < ncols) {
             const int n = pj / T, t = pj - n * T;
             const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -390,10 +390,10 @@ grad_z_digits_kernel(const float* __restrict__ dO, const float* __restrict__ rel
             }
         }
     }
-    if (pf > 0) {  // the dO rows of the block `pf` blocks ahead -> L2 (as in K1)
-        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf;
-        const int pk = (int)(lin / gridDim.x);
-        const int pj = (int)(lin - (long long)pk * gridDim.x) * kTileItems + threadIdx.x;
+    if (pf > 0) {  // the dO rows of the block `pf` blocks ahead -> L2 (as in K1; pf packed likewise)
+        int pbx = (int)blockIdx.x + (pf & 0xffff), pk = (int)blockIdx.y + (pf >> 16);
+        if (pbx >= (int)gridDim.x) pbx -= gridDim.x, ++pk;
+        const int pj = pbx * kTileItems + threadIdx.x;
         if (pk < (int)gridDim.y && pj < ncols) {
             const int n = pj / T, t = pj - n * T;
             const int ty = t / tiles_x, tx = t - ty * tiles_x;
