@@ -580,7 +580,7 @@ int fwd_transforms(wino_plan* p, cudaStream_t st, const float* in, float* out, f
     const wino_geometry& g = p->g;
     if (stage == 0) {
         Launch L(p, st, K_INPUT);
-        wino::input_transform_kernel<M, P, CF><<<grid_for((int64_t)p->C * NTr, 256, p->sm_count), 256, 0, st>>>(
+        wino::input_transform_kernel<M, P, CF><<<dim3((unsigned)((NTr + 255) / 256), (unsigned)p->C), 256, 0, st>>>(
             in, V, p->cf, p->C, p->H, p->W, p->pad, (int)g.tiles_x, (int)g.t, (int)NT, (int)NTs, (int)NTr);
         return L.done();
     }

@@ -121,20 +121,39 @@ template <int M, int P, class CF>
 __global__ void __launch_bounds__(256)
 input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, const Coefs cf, int C,
                        int H, int W, int pad, int tiles_x, int T, int NT, int NTs, int NTr) {
-    // columns [0, NTr) of V rows with stride NTs; columns ≥ NT are the zero padding.  (Training
-    // steps run the same product fused with the exact dW_F digits, wino_xdw.cuh.)
+    // grid (column blocks, C): c = blockIdx.y, nt = blockIdx.x·256 + thread.  Columns [0, NTr) of
+    // V rows with stride NTs; columns >= NT are the zero padding.  (Training steps run the same
+    // product fused with the exact dW_F digits, wino_xdw.cuh.)
+    const int c = blockIdx.y;
+    const int nt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (nt >= NTr) return;
     const int64_t plane = (int64_t)C * NTs;
-    const int64_t items = (int64_t)C * NTr;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
-         gid += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(gid / NTr);
-        const int nt = (int)(gid - (int64_t)c * NTr);
-        float d[P][P];
-        if (nt < NT) {
-            const int n = nt / T, t = nt - n * T;
-            const int ty = t / tiles_x, tx = t - ty * tiles_x;
-            const int y0 = ty * M - pad, x0 = tx * M - pad;
-            const float* src = in + ((int64_t)n * C + c) * H * W;
+    float d[P][P];
+    if (nt < NT) {
+        const int n = nt / T, t = nt - n * T;
+        const int ty = t / tiles_x, tx = t - ty * tiles_x;
+        const int y0 = ty * M - pad, x0 = tx * M - pad;
+        const float* src = in + ((int64_t)n * C + c) * H * W;
+        if (M == 4 && P == 6 && pad == 1 && (W & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+            // patch row = 4tx-1 | 4tx .. 4tx+3 (one aligned 16-byte load, always inside the row) | 4tx+4
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int y = y0 + i;
+                if ((unsigned)y < (unsigned)H) {
+                    const float* row = src + y * W + (x0 + 1);
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(row));
+                    d[i][0] = x0 >= 0 ? __ldg(row - 1) : 0.f;
+                    d[i][1] = v.x;
+                    d[i][2] = v.y;
+                    d[i][3] = v.z;
+                    d[i][4] = v.w;
+                    d[i][5] = x0 + 5 < W ? __ldg(row + 4) : 0.f;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < P; ++j) d[i][j] = 0.f;
+                }
+            }
+        } else {
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 const int y = y0 + i;
@@ -145,33 +164,33 @@ input_transform_kernel(const float* __restrict__ in, float* __restrict__ V, cons
                     d[i][j] = (yok && (unsigned)x < (unsigned)W) ? __ldg(src + y * W + x) : 0.f;
                 }
             }
-        } else {
-#pragma unroll
-            for (int i = 0; i < P; ++i)
-#pragma unroll
-                for (int j = 0; j < P; ++j) d[i][j] = 0.f;
         }
-        float tmp[P][P];
+    } else {
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + i), d[k][j]);
-                tmp[i][j] = acc;
-            }
-        float* vp = V + (int64_t)c * NTs + nt;
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-#pragma unroll
-            for (int j = 0; j < P; ++j, vp += plane) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
-                *vp = acc;
-            }
+            for (int j = 0; j < P; ++j) d[i][j] = 0.f;
     }
+    float tmp[P][P];
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + i), d[k][j]);
+            tmp[i][j] = acc;
+        }
+    float* vp = V + (int64_t)c * NTs + nt;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int j = 0; j < P; ++j, vp += plane) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc = cmadd<CF>(acc, coef_b<CF, M, P>(cf, k * P + j), tmp[i][k]);
+            *vp = acc;
+        }
 }
 
 // ---------------------------------------------------------------------------------
