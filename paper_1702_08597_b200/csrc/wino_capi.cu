@@ -602,9 +602,9 @@ int launch_input_grad(wino_plan* p, cudaStream_t st, const float* DV, float* dI,
     const int64_t per_c = (int64_t)T * (P * P + 1) * sizeof(float);
     Launch L(p, st, K_INGRAD);
     if (per_c <= 96 * 1024) {
-        // channels per block: fill >= 256 (c,t) items for phase 1 within ~48 KB of tiles
-        int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c,
-                                                                (256 + T - 1) / T}));
+        // channels per block: as many whole (c, all tiles) planes as fit 256 threads in one pass
+        // (c4: T = 49 -> 5 channels, 245 items; 6 would leave a second pass 15% full), within ~48 KB
+        int cg = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)p->C, (48 * 1024) / per_c, 256 / T}));
         const size_t smem = (size_t)cg * per_c;
         const dim3 grid((p->C + cg - 1) / cg, n);
         // whole warps over the block's (channel, tile) items (c3: 196 tiles -> 224 threads)
