@@ -786,6 +786,8 @@ int find_segments(const wino_cache* c, int n0, int n1, int* g0, int* g1) {
 
 // max|x| per (segment, row) over images [0, n) of x = [n][R][HW] (segments of seg_images(p)
 // images from amax[0]); mask: of dO·[relu > 0]
+// (The digit exponent only needs an upper bound of the row's values: for a ReLU-masked dO the
+// callers pass mask = false — max|dO| >= max|dO·mask| — and save the pass over the ReLU output.)
 int launch_amax(wino_plan* p, cudaStream_t st, const float* x, const float* relu, bool mask, unsigned* amax, int R,
                 int64_t HW, int n) {
     const int64_t planes = (int64_t)n * R;
@@ -1551,7 +1553,7 @@ static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_
     c->z_segs = 0;
     int rc;
     if ((zero && (rc = zero_rows(c->amax_z, 0, nseg, p->K, st))) ||
-        (rc = launch_amax(p, st, grad_output, relu_out, mask, c->amax_z, p->K, p->g.h_o * p->g.w_o, c->n)) ||
+        (rc = launch_amax(p, st, grad_output, nullptr, false, c->amax_z, p->K, p->g.h_o * p->g.w_o, c->n)) ||
         (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, c->DZ, c->NTs, c->NTs, 0, c, 0,
                           nseg)))
         return rc;
@@ -1744,7 +1746,7 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
     if (g0 != c->z_segs)
         return set_err(WINO_CONSISTENCY_ERROR, "backward image ranges of a batch must be issued in order from image 0");
     if ((rc = zero_rows(c->amax_z, g0, g1, p->K, st)) ||
-        (rc = launch_amax(p, st, grad_output, relu_out, mask, c->amax_z + (int64_t)g0 * p->K, p->K,
+        (rc = launch_amax(p, st, grad_output, nullptr, false, c->amax_z + (int64_t)g0 * p->K, p->K,
                           p->g.h_o * p->g.w_o, n1 - n0)) ||
         (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, DZ, r.NTs, r.NTr, n0, c, g0, g1)))
         return rc;

@@ -127,7 +127,7 @@ plane_amax_kernel(const float* __restrict__ x, const float* __restrict__ relu, u
         if ((HW & 3) == 0) {
             const float4* s4 = reinterpret_cast<const float4*>(src);
             const float4* r4 = reinterpret_cast<const float4*>(rl);
-#pragma unroll 4
+#pragma unroll 8
             for (int i = lane; i < (HW >> 2); i += 32) {
                 float4 v = __ldg(s4 + i);
                 if (MASK) {
