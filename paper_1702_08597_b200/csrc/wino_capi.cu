@@ -785,19 +785,13 @@ int find_segments(const wino_cache* c, int n0, int n1, int* g0, int* g1) {
 }
 
 // max|x| per (segment, row) over images [0, n) of x = [n][R][HW] (segments of seg_images(p)
-// images from amax[0]); mask: of dO·[relu > 0]
-// (The digit exponent only needs an upper bound of the row's values: for a ReLU-masked dO the
-// callers pass mask = false — max|dO| >= max|dO·mask| — and save the pass over the ReLU output.)
-int launch_amax(wino_plan* p, cudaStream_t st, const float* x, const float* relu, bool mask, unsigned* amax, int R,
-                int64_t HW, int n) {
+// images from amax[0]).  A ReLU-masked dO is passed unmasked: an upper bound is all the digit
+// exponent needs, and it saves the pass over the ReLU output.
+int launch_amax(wino_plan* p, cudaStream_t st, const float* x, unsigned* amax, int R, int64_t HW, int n) {
     const int64_t planes = (int64_t)n * R;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((planes + 7) / 8, (int64_t)p->sm_count * 16));
     Launch L(p, st, K_AMAX);
-    if (mask)
-        wino::xdw::plane_amax_kernel<true><<<grid, 256, 0, st>>>(x, relu, amax, R, (int)HW, seg_images(p), (int)planes);
-    else
-        wino::xdw::plane_amax_kernel<false><<<grid, 256, 0, st>>>(x, nullptr, amax, R, (int)HW, seg_images(p),
-                                                                  (int)planes);
+    wino::xdw::plane_amax_kernel<<<grid, 256, 0, st>>>(x, amax, R, (int)HW, seg_images(p), (int)planes);
     return L.done();
 }
 
@@ -1510,7 +1504,7 @@ int wino_forward(wino_plan* p, int n, const float* input, float* output, wino_ca
         if ((rc = plan_segments(p, cache, 0, n, true))) return rc;
         const int nseg = (int)cache->segs.size();
         if ((rc = zero_rows(cache->amax_v, 0, nseg, p->C, st)) ||
-            (rc = launch_amax(p, st, input, nullptr, false, cache->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
+            (rc = launch_amax(p, st, input, cache->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
             (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, V, NTs, NTs, 0, cache, 0, nseg)))
             return rc;
     } else if ((rc = DISPATCH_MP(p, fwd_transforms, p, st, input, output, V, p->d_z, n, NT, NTs, flags, 0, NTs))) {
@@ -1553,7 +1547,7 @@ static int bwd_grad_z(wino_plan* p, const float* grad_output, const float* relu_
     c->z_segs = 0;
     int rc;
     if ((zero && (rc = zero_rows(c->amax_z, 0, nseg, p->K, st))) ||
-        (rc = launch_amax(p, st, grad_output, nullptr, false, c->amax_z, p->K, p->g.h_o * p->g.w_o, c->n)) ||
+        (rc = launch_amax(p, st, grad_output, c->amax_z, p->K, p->g.h_o * p->g.w_o, c->n)) ||
         (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, c->DZ, c->NTs, c->NTs, 0, c, 0,
                           nseg)))
         return rc;
@@ -1644,7 +1638,7 @@ int wino_forward_backward(wino_plan* p, int n, const float* input, float* output
     CUDA_TRY(cudaEventRecord(p->ev_dz, p->side2));
     if ((rc = bwd_input(p, c, grad_input, p->side2))) return rc;
     // caller's stream: Ĩ_F and its digits, then Z = W_F·Ĩ_F and O
-    if ((rc = launch_amax(p, st, input, nullptr, false, c->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
+    if ((rc = launch_amax(p, st, input, c->amax_v, p->C, (int64_t)p->H * p->W, n)) ||
         (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, c->V, NTs, NTs, 0, c, 0, nseg)))
         return rc;
     CUDA_TRY(cudaEventRecord(p->ev_v, st));
@@ -1708,7 +1702,7 @@ int wino_forward_range(wino_plan* p, int n_total, int n0, int n1, const float* i
     if ((rc = zero_rows(cache->amax_v, g0, g1, p->C, st))) return rc;
     float* V = cache->V + r.a;
     float* Z = p->d_z + r.a;
-    if ((rc = launch_amax(p, st, input, nullptr, false, cache->amax_v + (int64_t)g0 * p->C, p->C,
+    if ((rc = launch_amax(p, st, input, cache->amax_v + (int64_t)g0 * p->C, p->C,
                           (int64_t)p->H * p->W, n1 - n0)) ||
         (rc = DISPATCH_MP(p, launch_input_fused, p, st, input, V, r.NTs, r.NTr, n0, cache, g0, g1)))
         return rc;
@@ -1746,7 +1740,7 @@ int wino_backward_range(wino_plan* p, int n0, int n1, const float* grad_output, 
     if (g0 != c->z_segs)
         return set_err(WINO_CONSISTENCY_ERROR, "backward image ranges of a batch must be issued in order from image 0");
     if ((rc = zero_rows(c->amax_z, g0, g1, p->K, st)) ||
-        (rc = launch_amax(p, st, grad_output, nullptr, false, c->amax_z + (int64_t)g0 * p->K, p->K,
+        (rc = launch_amax(p, st, grad_output, c->amax_z + (int64_t)g0 * p->K, p->K,
                           p->g.h_o * p->g.w_o, n1 - n0)) ||
         (rc = DISPATCH_MP(p, launch_grad_fused, p, st, grad_output, relu_out, mask, DZ, r.NTs, r.NTr, n0, c, g0, g1)))
         return rc;

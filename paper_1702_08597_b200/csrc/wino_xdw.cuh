@@ -112,41 +112,28 @@ __device__ __forceinline__ void to_digits(double x, double scale, uint32_t& lo, 
     hi = ((uint32_t)(b >> 32) & 0xffu) ^ 0x80u;
 }
 
-// max|x| per (segment, row) of x = [n][R][HW] images (MASK: of x·[relu > 0], the masked dO of
-// train.cpp:193): amax[(n / seg_imgs)·R + r] as float bits (atomicMax: non-negative floats order
-// as their bits).  One warp per (n, r) plane; the a-priori exponent bound of the digits.
-template <bool MASK>
+// max|x| per (segment, row) of x = [n][R][HW] images: amax[(n / seg_imgs)·R + r] as float bits
+// (atomicMax: non-negative floats order as their bits).  One warp per (n, r) plane; the a-priori
+// exponent bound of the digits.  For a ReLU-masked dO (train.cpp:193) the callers still pass dO
+// itself: max|dO| >= max|dO·mask|, and an upper bound is all the exponent needs.
 __global__ void __launch_bounds__(256)
-plane_amax_kernel(const float* __restrict__ x, const float* __restrict__ relu, unsigned* __restrict__ amax, int R,
-                  int HW, int seg_imgs, int n_planes) {
+plane_amax_kernel(const float* __restrict__ x, unsigned* __restrict__ amax, int R, int HW, int seg_imgs,
+                  int n_planes) {
     const int lane = threadIdx.x & 31;
     for (int pl = blockIdx.x * 8 + (threadIdx.x >> 5); pl < n_planes; pl += gridDim.x * 8) {
         const float* src = x + (int64_t)pl * HW;
-        const float* rl = MASK ? relu + (int64_t)pl * HW : nullptr;
         unsigned mx = 0;
-        if ((HW & 3) == 0) {
+        if ((HW & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
             const float4* s4 = reinterpret_cast<const float4*>(src);
-            const float4* r4 = reinterpret_cast<const float4*>(rl);
 #pragma unroll 8
             for (int i = lane; i < (HW >> 2); i += 32) {
-                float4 v = __ldg(s4 + i);
-                if (MASK) {
-                    const float4 r = __ldg(r4 + i);
-                    v.x = r.x > 0.f ? v.x : 0.f;
-                    v.y = r.y > 0.f ? v.y : 0.f;
-                    v.z = r.z > 0.f ? v.z : 0.f;
-                    v.w = r.w > 0.f ? v.w : 0.f;
-                }
+                const float4 v = __ldg(s4 + i);
                 mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
                                  max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
             }
         } else {
 #pragma unroll 4
-            for (int i = lane; i < HW; i += 32) {
-                float v = __ldg(src + i);
-                if (MASK && !(__ldg(rl + i) > 0.f)) v = 0.f;
-                mx = max(mx, __float_as_uint(v) & 0x7fffffffu);
-            }
+            for (int i = lane; i < HW; i += 32) mx = max(mx, __float_as_uint(__ldg(src + i)) & 0x7fffffffu);
         }
         mx = __reduce_max_sync(0xffffffffu, mx);
         const int n = pl / R, r = pl - n * R;
