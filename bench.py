@@ -278,8 +278,11 @@ def kernel_table(prof, steps, cfg, layer, n, pk, sm_mhz=None):
             mac = layer.nnz * nt / (ms * 1e-3) / (148 * clk)
             k["on_chip"] = {"mac_per_clk_sm": mac, "tmem_bound": TMEM_MAC_PER_CLK, "lds_bound": LDS_MAC_PER_CLK,
                             "frac_of_tmem_bound": mac / TMEM_MAC_PER_CLK,
+                            "frac_of_tmem_plus_lds_bound": mac / (TMEM_MAC_PER_CLK + LDS_MAC_PER_CLK),
                             "note": "nnz·n·T multiply-adds per pass / time / (148 SMs · SM clock); the "
-                                    "operand bytes per multiply-add come from TMEM (or shared memory), not HBM"}
+                                    "operand bytes per multiply-add come from TMEM and/or shared memory, not "
+                                    "HBM (the hybrid kernel, 128 < C,K <= 256 with a staged stream, reads "
+                                    "half its operands through each: its bound is the sum)"}
         out[name] = k
     return out
 
